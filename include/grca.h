@@ -1,0 +1,181 @@
+/*
+ * include/grca.h -- C ABI of the B200-native GRCA hot path (libgrca.so).
+ *
+ * The operation ("Problem Statement"): a LiDAR fires rays
+ * into a scene of triangles; "for each ray the simulation must find the
+ * closest triangle it intersects and its distance", with no acceleration
+ * structure: each triangle's emitter-centric angular footprint selects the
+ * channels and the ray range it can hit (Observations 1-2;
+ * SURVEY.md 8(a) rows A0-A9), and only those (triangle, ray) pairs are tested.
+ *
+ * Conventions
+ *  - Emitter n has gamma_n channels (elevations phi_j, ascending) and chi_n rays
+ *    per channel; ray (n, j, i) has global index g = O_n + j*chi_n + i with
+ *    O_n = sum_{m<n} gamma_m chi_m.  Direction (PAPER.md:418-435,
+ *    Eq. ray_dir): d = RN32(cos(th_i)cos(phi_j) f + sin(th_i)cos(phi_j) r + sin(phi_j) u)
+ *    evaluated in fp64, th_i = -floor(chi/2)*dth + i*dth, dth = H/chi, H = 2*pi (360 deg)
+ *    or pi (180 deg).  The reported distance is the ray parameter t of that d.
+ *  - Hit: closed triangle, 0 < t <= max_range, two-sided unless `faces` says
+ *    otherwise; per ray the minimum t wins, equal fp32 t -> smaller triangle id.
+ *    Miss: distance +inf, id -1.
+ *  - Results are exact up to rounding: no culling approximation is applied
+ *    (SURVEY 8(c)); see DESIGN.md for the precision contract.
+ *
+ * Errors: every call returns grca_status; nothing throws across the ABI.
+ * grca_last_error(h) returns a message for the last failing call on h.
+ * A handle is not thread-safe; distinct handles are independent.
+ */
+#ifndef GRCA_H
+#define GRCA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct grca_ctx *grca_t;
+
+typedef enum {
+    GRCA_OK = 0,
+    GRCA_E_INVALID = 1,  /* bad argument (see grca_last_error) */
+    GRCA_E_STATE = 2,    /* call order: cast before set_emitters / update_triangles */
+    GRCA_E_CAPACITY = 3, /* counts above the capacities fixed at create */
+    GRCA_E_CUDA = 4,     /* a CUDA runtime error (message has cudaGetErrorString) */
+    GRCA_E_NCCL = 5,     /* reserved for the in-library collective path */
+    GRCA_E_OOM = 6       /* device allocation failed at create */
+} grca_status;
+
+/* Face modes (PAPER.md:614-620 back-face rule).  N = (v1-v0)x(v2-v0). */
+enum {
+    GRCA_FACES_TWO_SIDED = 0, /* default: both sides hit */
+    GRCA_FACES_KEEP_POS = 1,  /* keep hits with d.N > 0  <=> (c - o).N > 0 */
+    GRCA_FACES_KEEP_NEG = 2   /* keep hits with d.N < 0 */
+};
+
+/* Debug / instrumentation flags (grca_create_info.debug_flags). */
+enum {
+    GRCA_DEBUG_COUNT_ALL_HITS = 1u, /* per-ray count of every accepted hit (all-hits invariant) */
+    GRCA_DEBUG_NO_CULL = 2u,        /* every (tri, emitter) pair tests the full ray grid */
+    GRCA_PROFILE_KERNELS = 4u,      /* CUDA events around each kernel; see grca_kernel_times */
+    GRCA_DEBUG_FORCE_FP64 = 8u      /* every candidate takes the fp64 path (precision check) */
+};
+
+typedef struct {
+    int32_t device;          /* CUDA device ordinal */
+    void *stream;            /* cudaStream_t (e.g. torch's current stream); NULL -> library-owned stream */
+    int32_t nranks, rank;    /* informational: the caller shards triangles / emitters and merges */
+    int64_t max_triangles;   /* per handle; fixes scratch sizes so grca_cast never allocates */
+    int64_t max_rays;        /* upper bound of sum_n gamma_n chi_n */
+    int64_t max_large_items; /* capacity of the large-pair list (0 -> default); overflow is
+                                handled inline (slower, never dropped) and counted in stats */
+    int32_t faces;           /* GRCA_FACES_* */
+    uint32_t debug_flags;    /* GRCA_DEBUG_* | GRCA_PROFILE_KERNELS */
+    int32_t small_max;       /* pairs with <= small_max candidates are tested inline by the
+                                culling kernel (0 -> default 512) */
+    int32_t reserved[7];
+} grca_create_info;
+
+/* One spinning LiDAR (ray origin); SPEC SensorConfig. */
+typedef struct {
+    float origin[3];
+    float forward[3], right[3], up[3]; /* orthonormal within 1e-3 (any such frame is exact) */
+    const float *channel_elev_rad;     /* host pointer, gamma entries, strictly ascending,
+                                          |phi| <= RN32(pi/2); copied by grca_set_emitters */
+    int32_t n_channels;                /* gamma_n in [1, 65535] */
+    int32_t rays_per_channel;          /* chi_n in [1, 65535] */
+    int32_t hfov_deg;                  /* 360 or 180 */
+    float max_range;                   /* D_max > 0; <= 0 or +inf -> unlimited */
+} grca_emitter;
+
+/* Per-cast counters (SURVEY 5 "Metrics"; Eq. 1 and 2131-2144 Eq. rtic_reduced). */
+typedef struct {
+    int64_t pairs;           /* (triangle, emitter) pairs considered = tau * Omega */
+    int64_t range_culled;    /* dropped by Step 1.3 range cull */
+    int64_t channel_culled;  /* no channel in the elevation interval */
+    int64_t azimuth_culled;  /* no ray in the azimuth arc, degenerate, or face mode */
+    int64_t survivors;       /* pairs with >= 1 candidate */
+    int64_t small_pairs;     /* tested inline by the cull kernel */
+    int64_t large_pairs;     /* binned to the large list */
+    int64_t chunks;          /* load-balanced work chunks made from the large list */
+    int64_t rtic_tested;     /* ray-triangle tests performed (candidates) */
+    int64_t rtic_brute;      /* Eq. 1: sum gamma chi * tau */
+    int64_t fp64_fallbacks;  /* candidates decided by the fp64 path */
+    int64_t hits_recorded;   /* accepted intersections (before the closest-hit min) */
+    int64_t overflow_inline; /* large pairs processed inline because the list was full */
+    int32_t overflow;        /* 1 if any capacity fallback happened */
+    float ms_total;          /* device time of the last cast if GRCA_PROFILE_KERNELS */
+    float ms_k[8];           /* per kernel: K0 init, K2 cull, K3 bin, K4 intersect, K5 unpack */
+} grca_stats;
+
+/* Create a handle bound to ci->device.  Allocates all device scratch.
+ * Errors: GRCA_E_INVALID (null/negative sizes, bad faces), GRCA_E_CUDA, GRCA_E_OOM. */
+grca_status grca_create(const grca_create_info *ci, grca_t *out);
+
+/* Destroy the handle and free its memory (synchronizes its stream).  NULL is a no-op. */
+grca_status grca_destroy(grca_t h);
+
+/* Set the emitters (copies everything; host arrays may be freed after return).
+ * Builds the fp32 ray table in fp64 on the host (O1 above; PAPER.md:2322-2325 ray setup)
+ * and uploads it with the per-emitter records and sin(phi_j) tables (synchronous).
+ * Errors: GRCA_E_INVALID for n_emitters not in [1, 255], gamma/chi out of range, an
+ * unsorted or non-strict elevation table, |phi| > RN32(pi/2), a non-orthonormal frame,
+ * hfov not 180/360, sum gamma > 4096; GRCA_E_CAPACITY if sum gamma chi > max_rays. */
+grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitters);
+
+/* Borrow this frame's triangles (no copy).  d_vertices: device float4 (x, y, z, w unused),
+ * 16-byte stride.  d_indices: device uint32, 3 per triangle, or NULL -> non-indexed: triangle
+ * k is vertices 3k, 3k+1, 3k+2.  d_tri_ids: device int32 global id per triangle, or NULL ->
+ * id = tri_id_base + k.  Ids must be in [0, 2^31 - 1).  Buffers must stay alive and
+ * unmodified until the cast consuming them completes on the handle's stream.
+ * Errors: GRCA_E_INVALID (null vertices with n_triangles > 0, indexed with n_vertices < 1),
+ * GRCA_E_CAPACITY (n_triangles > max_triangles). */
+grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_vertices,
+                                  const uint32_t *d_indices, int64_t n_triangles,
+                                  const int32_t *d_tri_ids, int32_t tri_id_base);
+
+/* Cast one frame: K0 init -> K2 cull (+ inline small work) -> K3 bin -> K4 intersect ->
+ * K5 unpack, all enqueued on the handle's stream (no allocation, no host sync unless
+ * h_stats != NULL).  d_out_dist: device float[n_rays] (+inf on a miss); d_out_tri: device
+ * int32[n_rays] (-1 on a miss).  Either output may be NULL to skip K5.
+ * Errors: GRCA_E_STATE (no emitters), GRCA_E_CUDA. */
+grca_status grca_cast(grca_t h, float *d_out_dist, int32_t *d_out_tri, grca_stats *h_stats);
+
+/* Split form for multi-rank merges: grca_cast_packed runs K0..K4 into the handle's packed
+ * hit buffer (uint64 per ray: fp32 distance bits << 32 | triangle id; miss =
+ * 0x7F800000FFFFFFFF; ordered like (t, id), positive as int64 so a signed or unsigned
+ * min-allreduce merges shards exactly).  grca_hits_packed returns its device pointer.
+ * grca_unpack runs K5 from that buffer (after the caller's merge). */
+grca_status grca_cast_packed(grca_t h);
+grca_status grca_hits_packed(grca_t h, uint64_t **d_hits, int64_t *n_rays);
+grca_status grca_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri);
+
+/* Counters of the last cast (synchronizes the stream). */
+grca_status grca_get_stats(grca_t h, grca_stats *h_stats);
+
+/* Sum of per-kernel device times over the last n_last casts (GRCA_PROFILE_KERNELS only;
+ * n_last in [1, 64]; synchronizes).  ms_per_kernel[8]: [0] K0 init, [1] K2 cull (incl. inline
+ * small work), [2] K3 bin, [3] K4 intersect, [4] K5 unpack, [7] whole cast. */
+grca_status grca_kernel_times(grca_t h, int32_t n_last, float *ms_per_kernel);
+
+/* Per-ray all-hit counts of the last cast (GRCA_DEBUG_COUNT_ALL_HITS only):
+ * device pointer to uint32[n_rays]. */
+grca_status grca_debug_all_hits(grca_t h, const uint32_t **d_counts);
+
+/* n_rays_total and ray_offsets[n_emitters + 1] (O_n) of the current emitters. */
+grca_status grca_get_layout(grca_t h, int64_t *n_rays_total, int64_t *ray_offsets);
+
+/* Copy the fp32 ray table to host memory h_xyz[3 * n_rays] (test-only: bit-compare). */
+grca_status grca_debug_ray_table(grca_t h, float *h_xyz);
+
+/* Last error message of the handle (or of the last failed grca_create if h is NULL). */
+const char *grca_last_error(grca_t h);
+
+/* Library version string. */
+const char *grca_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GRCA_H */

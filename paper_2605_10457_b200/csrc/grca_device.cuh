@@ -1,0 +1,408 @@
+// grca_device.cuh -- device math of the GRCA hot path (sm_100a).
+//
+// Rows of SURVEY.md 8(a) implemented here:
+//   A1  triangle load (fused "K1": coalesced float4 gathers, indexed or not)
+//   A2  range cull          (Step 1.3; delta_min per Ericson)
+//   A3  elevation interval -> channel range   (Obs. 2)
+//   A4  azimuth arc -> ray range              (g(j,i) 760-763)
+//   A6  certified edge-function ray-triangle test + closest-hit key
+//       (Moller-Trumbore 756; f_sort 2340-2356)
+//
+// Precision contract: every cull is conservative (outward
+// padding larger than the fp32 error bound), every fp32 hit/miss decision is
+// certified by an a-priori error bound, and uncertain candidates are decided in
+// fp64 -- so the result equals the exact-arithmetic closest hit of the fp32 ray
+// table up to the 1e-16-relative fp64 boundary cases the parity contract excuses.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace grca {
+
+constexpr float kU = 5.9604644775390625e-8f;   // 2^-24, unit roundoff of fp32
+constexpr float kPadS = 4e-6f;                 // sin(elevation) padding (>> 3u ray rounding)
+constexpr float kPadTheta = 5e-5f;             // azimuth padding in radians
+constexpr float kNearAxis2 = 1e-3f;            // |x_h|^2 < 1e-3 |x|^2 -> full azimuth
+constexpr float kChordSmall2 = 4e-2f;          // chord^2 below which the L^2/8 edge pad is used
+constexpr float kTRel = 4.5e-6f;               // certified relative error of fp32 t
+constexpr int kChunkItems = 1024;              // target items per load-balanced chunk
+constexpr int kColMax = 1024;                  // max columns per chunk row segment
+
+// Per-emitter record (device + shared memory).  A = M^-1 with M = [f r u] (fp64 inverse,
+// rounded): x = A (p - o) are the coordinates in which ray (j,i) is exactly
+// (cos th cos phi, sin th cos phi, sin phi) -- so the cull is exact for any given frame.
+struct EmDev {
+    float o[3];
+    float A[9];
+    float theta0, dtheta, inv_dtheta;
+    float dmax_lo, dmax_hi;   // certified accept / reject bounds around D_max (+inf if none)
+    double dmax;              // fp64 D_max for the fallback (+inf if none)
+    int gamma, chi, hfov, ray_base, sin_base, pole_lo, pole_hi, pad_;
+};
+
+struct f3 {
+    float x, y, z;
+};
+struct d3 {
+    double x, y, z;
+};
+
+__device__ __forceinline__ f3 mk(float4 a) { return {a.x, a.y, a.z}; }
+// Fixed operation order (no contraction freedom): bit-identical wherever inlined.
+__device__ __forceinline__ f3 subf(f3 a, f3 b) { return {__fsub_rn(a.x, b.x), __fsub_rn(a.y, b.y), __fsub_rn(a.z, b.z)}; }
+__device__ __forceinline__ float dotf(f3 a, f3 b) {
+    return __fmaf_rn(a.z, b.z, __fmaf_rn(a.y, b.y, __fmul_rn(a.x, b.x)));
+}
+__device__ __forceinline__ f3 crossf(f3 a, f3 b) {
+    return {__fmaf_rn(a.y, b.z, -__fmul_rn(a.z, b.y)), __fmaf_rn(a.z, b.x, -__fmul_rn(a.x, b.z)),
+            __fmaf_rn(a.x, b.y, -__fmul_rn(a.y, b.x))};
+}
+__device__ __forceinline__ f3 scalef(f3 a, float s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ d3 tod(f3 a) { return {(double)a.x, (double)a.y, (double)a.z}; }
+__device__ __forceinline__ d3 subd(d3 a, d3 b) { return {__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y), __dsub_rn(a.z, b.z)}; }
+__device__ __forceinline__ double dotd(d3 a, d3 b) {
+    return __fma_rn(a.z, b.z, __fma_rn(a.y, b.y, __dmul_rn(a.x, b.x)));
+}
+__device__ __forceinline__ d3 crossd(d3 a, d3 b) {
+    return {__fma_rn(a.y, b.z, -__dmul_rn(a.z, b.y)), __fma_rn(a.z, b.x, -__dmul_rn(a.x, b.z)),
+            __fma_rn(a.x, b.y, -__dmul_rn(a.y, b.x))};
+}
+// Lexicographic order of fp32 points: the canonical edge direction (watertightness).
+__device__ __forceinline__ bool lexless(f3 p, f3 q) {
+    return p.x < q.x || (p.x == q.x && (p.y < q.y || (p.y == q.y && p.z < q.z)));
+}
+__device__ __forceinline__ bool finite3(f3 a) { return isfinite(a.x) && isfinite(a.y) && isfinite(a.z); }
+
+// ----------------------------------------------------------------- A1 load --
+struct TriSrc {
+    const float4 *v;
+    const uint32_t *idx;   // NULL -> non-indexed triplets
+    const int32_t *ids;    // NULL -> id_base + local
+    int32_t id_base;
+};
+__device__ __forceinline__ void load_tri(const TriSrc &T, long long t, f3 v[3]) {
+    if (T.idx) {
+        const uint32_t i0 = __ldg(T.idx + 3 * t), i1 = __ldg(T.idx + 3 * t + 1), i2 = __ldg(T.idx + 3 * t + 2);
+        v[0] = mk(__ldg(T.v + i0));
+        v[1] = mk(__ldg(T.v + i1));
+        v[2] = mk(__ldg(T.v + i2));
+    } else {
+        v[0] = mk(__ldg(T.v + 3 * t));
+        v[1] = mk(__ldg(T.v + 3 * t + 1));
+        v[2] = mk(__ldg(T.v + 3 * t + 2));
+    }
+}
+__device__ __forceinline__ uint32_t tri_id(const TriSrc &T, long long t) {
+    return T.ids ? (uint32_t)__ldg(T.ids + t) : (uint32_t)(T.id_base + (int32_t)t);
+}
+
+// -------------------------------------------------------- A2 range (delta_min) --
+// Closest distance from the origin (0) to the closed triangle a0,a1,a2 (relative coords),
+// Ericson-style: plane distance when the projection is inside, else nearest edge.
+__device__ __forceinline__ float seg_dist2(f3 a, f3 b) {
+    f3 e = subf(b, a);
+    float ee = dotf(e, e);
+    float t = ee > 0.f ? fminf(fmaxf(-dotf(a, e) / ee, 0.f), 1.f) : 0.f;
+    f3 p = {a.x + t * e.x, a.y + t * e.y, a.z + t * e.z};
+    return dotf(p, p);
+}
+__device__ float tri_dist(const f3 a[3]) {
+    f3 N = crossf(subf(a[1], a[0]), subf(a[2], a[0]));
+    float w0 = dotf(crossf(a[0], a[1]), N), w1 = dotf(crossf(a[1], a[2]), N), w2 = dotf(crossf(a[2], a[0]), N);
+    float nn = dotf(N, N);
+    if (nn > 0.f && ((w0 >= 0.f && w1 >= 0.f && w2 >= 0.f) || (w0 <= 0.f && w1 <= 0.f && w2 <= 0.f)))
+        return fabsf(dotf(N, a[0])) * rsqrtf(nn);
+    float d2 = fminf(seg_dist2(a[0], a[1]), fminf(seg_dist2(a[1], a[2]), seg_dist2(a[2], a[0])));
+    return sqrtf(d2);
+}
+
+// ------------------------------------------------------ A3/A4 angular bounds --
+struct Rect {
+    int c_from, c_to;   // channel range (inclusive)
+    int r_lo, r_len;    // ray range start (mod chi) and length; r_len == chi -> full
+    int pole_rows;      // 1 if the range touches pole channels (full-azimuth rows)
+};
+
+enum { CULL_KEEP = 0, CULL_RANGE = 1, CULL_CHANNEL = 2, CULL_AZIMUTH = 3, CULL_DEGENERATE = 4 };
+
+__device__ __forceinline__ int lower_bound_f(const float *t, int n, float x) {   // first j: t[j] >= x
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (t[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+__device__ __forceinline__ int upper_bound_f(const float *t, int n, float x) {   // first j: t[j] > x
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (t[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Does direction T lie on the great-circle arc from p to q (normal m = p x q)?  Tolerant
+// (returns true when unsure) -- including an extreme that is not attained is conservative.
+__device__ __forceinline__ bool on_arc(f3 p, f3 q, f3 m, f3 T) {
+    float q1 = dotf(crossf(p, T), m), q2 = dotf(crossf(T, q), m);
+    float tol = 1e-4f * sqrtf(dotf(p, p) * dotf(T, T)) * sqrtf(dotf(m, m));
+    float tol2 = 1e-4f * sqrtf(dotf(q, q) * dotf(T, T)) * sqrtf(dotf(m, m));
+    return q1 >= -tol && q2 >= -tol2;
+}
+
+// Conservative (channel, ray) rectangle of triangle v seen from emitter E.
+__device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, bool nocull, Rect &R) {
+    const f3 o = {E.o[0], E.o[1], E.o[2]};
+    f3 a[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) a[k] = subf(v[k], o);
+    if (!(finite3(a[0]) && finite3(a[1]) && finite3(a[2]))) return CULL_DEGENERATE;
+    if (nocull) {
+        R.c_from = 0; R.c_to = E.gamma - 1; R.r_lo = 0; R.r_len = E.chi; R.pole_rows = 0;
+        return CULL_KEEP;
+    }
+    // A2: Step 1.3 range cull (delta_min > D_max), exact per-ray t <= D_max is in the test.
+    if (E.dmax_hi < CUDART_INF_F) {
+        const float lim = E.dmax_hi * (1.f + 1e-5f);
+        float m2 = fminf(dotf(a[0], a[0]), fminf(dotf(a[1], a[1]), dotf(a[2], a[2])));
+        if (m2 > lim * lim && tri_dist(a) > lim) return CULL_RANGE;
+    }
+    // sensor coordinates x = A a  (x = (x_f, x_r, x_u))
+    f3 x[3];
+    float r2[3], inv[3], s[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        x[k].x = E.A[0] * a[k].x + E.A[1] * a[k].y + E.A[2] * a[k].z;
+        x[k].y = E.A[3] * a[k].x + E.A[4] * a[k].y + E.A[5] * a[k].z;
+        x[k].z = E.A[6] * a[k].x + E.A[7] * a[k].y + E.A[8] * a[k].z;
+        r2[k] = x[k].x * x[k].x + x[k].y * x[k].y + x[k].z * x[k].z;
+    }
+    if (!(r2[0] > 0.f && r2[1] > 0.f && r2[2] > 0.f)) return CULL_DEGENERATE;   // o is a vertex: Vol = 0
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        inv[k] = rsqrtf(r2[k]);
+        s[k] = x[k].z * inv[k];
+    }
+    float slo = fminf(s[0], fminf(s[1], s[2])), shi = fmaxf(s[0], fmaxf(s[1], s[2]));
+    // pole containment: does the spin axis pass through T?  (2-D winding in the x_f x_r plane)
+    bool pos = false, neg = false, near_axis = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int k1 = (k + 1) % 3;
+        float w = x[k].x * x[k1].y - x[k].y * x[k1].x;
+        float eps = 8.f * kU * sqrtf(r2[k] * r2[k1]);
+        pos |= (w > eps);
+        neg |= (w < -eps);
+        near_axis |= (x[k].x * x[k].x + x[k].y * x[k].y) < kNearAxis2 * r2[k];
+    }
+    const bool pole = !(pos && neg);
+    if (pole) {
+        if (shi > 0.f) shi = 1.f;
+        if (slo < 0.f) slo = -1.f;
+    }
+    // interior extremes of edges: small arcs -> L^2/8 pad, long arcs -> great-circle extreme
+    float pad_e = 0.f;
+    bool longedge = false;
+    f3 xh[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) xh[k] = scalef(x[k], inv[k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const int k1 = (k + 1) % 3;
+        f3 dv = subf(xh[k], xh[k1]);
+        float c2 = dotf(dv, dv);
+        if (c2 <= kChordSmall2) {
+            pad_e = fmaxf(pad_e, 0.31f * c2);
+        } else {
+            longedge = true;
+            f3 m = crossf(x[k], x[k1]);
+            float mh2 = m.x * m.x + m.y * m.y;
+            float mm = mh2 + m.z * m.z;
+            if (!(mm > 0.f)) { shi = fmaxf(shi, 1.f); slo = fminf(slo, -1.f); continue; }
+            float S = sqrtf(mh2 / mm);
+            f3 T = {-m.z * m.x, -m.z * m.y, mh2};   // top of the great circle (u - (u.m)m) * mm
+            if (on_arc(x[k], x[k1], m, T)) shi = fmaxf(shi, S);
+            f3 Tb = {-T.x, -T.y, -T.z};
+            if (on_arc(x[k], x[k1], m, Tb)) slo = fminf(slo, -S);
+        }
+    }
+    const float pad = kPadS + pad_e + (longedge ? 1e-5f : 0.f);
+    R.c_from = lower_bound_f(sinTab, E.gamma, slo - pad);
+    R.c_to = upper_bound_f(sinTab, E.gamma, shi + pad) - 1;
+    if (R.c_from > R.c_to) return CULL_CHANNEL;
+    // A4: azimuth arc -> ray index range
+    const bool full = pole || near_axis;
+    if (full) {
+        R.r_lo = 0; R.r_len = E.chi; R.pole_rows = 0;
+        return CULL_KEEP;
+    }
+    float th[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) th[k] = atan2f(x[k].y, x[k].x);
+    // sort 3 angles
+    float t0 = fminf(th[0], fminf(th[1], th[2]));
+    float t2 = fmaxf(th[0], fmaxf(th[1], th[2]));
+    float t1 = th[0] + th[1] + th[2] - t0 - t2;
+    t1 = fminf(fmaxf(t1, t0), t2);
+    const float TWO_PI = 6.283185307179586f;
+    float g01 = t1 - t0, g12 = t2 - t1, g20 = t0 + TWO_PI - t2;
+    float start, len;
+    if (g20 >= g01 && g20 >= g12) { start = t0; len = t2 - t0; }
+    else if (g01 >= g12) { start = t1; len = (t0 + TWO_PI) - t1; }
+    else { start = t2; len = (t1 + TWO_PI) - t2; }
+    if (len > 3.1f) {   // arc near pi with the axis outside T only by rounding: be safe
+        R.r_lo = 0; R.r_len = E.chi; R.pole_rows = 0;
+        return CULL_KEEP;
+    }
+    float xlo = (start - kPadTheta - E.theta0) * E.inv_dtheta;
+    float xhi = (start + len + kPadTheta - E.theta0) * E.inv_dtheta;
+    int ilo = (int)ceilf(xlo), ihi = (int)floorf(xhi);
+    if (E.hfov == 360) {
+        int n = ihi - ilo + 1;
+        if (n <= 0) return CULL_AZIMUTH;
+        if (n >= E.chi) { R.r_lo = 0; R.r_len = E.chi; }
+        else { int r = ilo % E.chi; R.r_lo = r < 0 ? r + E.chi : r; R.r_len = n; }
+    } else {
+        // 180 deg: valid indices [0, chi-1]; the arc may also appear one period (2 chi) lower.
+        int lo = INT_MAX, hi = INT_MIN;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            int a0 = ilo - c * 2 * E.chi, a1 = ihi - c * 2 * E.chi;
+            a0 = max(a0, 0);
+            a1 = min(a1, E.chi - 1);
+            if (a0 <= a1) { lo = min(lo, a0); hi = max(hi, a1); }
+        }
+        if (lo > hi) return CULL_AZIMUTH;
+        R.r_lo = lo; R.r_len = hi - lo + 1;
+    }
+    R.pole_rows = (R.r_len < E.chi) && (R.c_from < E.pole_lo || R.c_to > E.gamma - 1 - E.pole_hi);
+    return CULL_KEEP;
+}
+
+// number of candidate (channel, ray) items of a rectangle (pole rows take all chi rays)
+__device__ __forceinline__ long long rect_items(const Rect &R, const EmDev &E) {
+    long long rows = R.c_to - R.c_from + 1;
+    if (!R.pole_rows) return rows * R.r_len;
+    int plo = max(0, min(R.c_to, E.pole_lo - 1) - R.c_from + 1);
+    int phi = max(0, R.c_to - max(R.c_from, E.gamma - E.pole_hi) + 1);
+    return (long long)(plo + phi) * E.chi + (rows - plo - phi) * R.r_len;
+}
+
+// --------------------------------------------------- A6 setup + certified test --
+struct Setup {
+    f3 n0, n1, n2;     // sigma_k * s * n_k: hit <=> all d.n_k >= 0
+    float B0, B1, B2;  // certified error bounds of d.n_k
+    f3 N;              // s * (e1 x e2): d.N > 0 for hits
+    float habs;        // |N . a0|
+    float TN;          // fp32 t certified iff d.N >= TN
+};
+
+// fp64 Vol = (e1 x e2) . (v0 - o)
+__device__ __noinline__ double exact_vol(const f3 v[3], f3 o) {
+    d3 V0 = tod(v[0]);
+    d3 e1 = subd(tod(v[1]), V0), e2 = subd(tod(v[2]), V0);
+    return dotd(crossd(e1, e2), subd(V0, tod(o)));
+}
+
+// Returns false when the pair can never hit (Vol == 0: origin in the plane / degenerate
+// triangle) or is rejected by the face mode.  setup64 counts fp64 plane-side decisions.
+__device__ __forceinline__ bool make_setup(const f3 v[3], f3 o, int faces, Setup &S, unsigned &setup64) {
+    f3 n[3];
+    float B[3], sg[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        f3 P = v[k], Q = v[(k + 1) % 3];
+        const bool sw = lexless(Q, P);
+        if (sw) { f3 t = P; P = Q; Q = t; }
+        sg[k] = sw ? -1.f : 1.f;
+        f3 aP = subf(P, o), e = subf(Q, P);
+        n[k] = crossf(aP, e);
+        B[k] = 16.f * kU * sqrtf(dotf(aP, aP)) * sqrtf(dotf(e, e));
+    }
+    f3 e1 = subf(v[1], v[0]), e2 = subf(v[2], v[0]);
+    f3 N = crossf(e1, e2);
+    f3 a0 = subf(v[0], o);
+    float h = dotf(N, a0);
+    float nE = sqrtf(dotf(e1, e1)) * sqrtf(dotf(e2, e2));
+    float nN = sqrtf(dotf(N, N));
+    float na0 = sqrtf(dotf(a0, a0));
+    float Bh = (8.f * kU * nE + 6.f * kU * nN) * na0;
+    float s;
+    bool force64 = false;
+    if (!(fabsf(h) > 2.f * Bh)) {
+        double h64 = exact_vol(v, o);
+        ++setup64;
+        if (!(h64 > 0.0 || h64 < 0.0)) return false;
+        s = h64 > 0.0 ? 1.f : -1.f;
+        force64 = true;
+    } else {
+        s = h > 0.f ? 1.f : -1.f;
+    }
+    if ((faces == 1 && s < 0.f) || (faces == 2 && s > 0.f)) return false;
+    S.n0 = scalef(n[0], s * sg[0]);
+    S.n1 = scalef(n[1], s * sg[1]);
+    S.n2 = scalef(n[2], s * sg[2]);
+    S.B0 = B[0]; S.B1 = B[1]; S.B2 = B[2];
+    S.N = scalef(N, s);
+    S.habs = fabsf(h);
+    const float rh = Bh / fabsf(h);
+    const float Bn = 8.f * kU * nE + 4.f * kU * nN;
+    S.TN = (force64 || !(rh < 2e-6f)) ? CUDART_INF_F : Bn / (kTRel - 2.f * kU - rh);
+    return true;
+}
+
+// 0 = certified miss, 1 = certified hit (t set), 2 = uncertain -> fp64
+__device__ __forceinline__ int test_fast(float4 d4, const Setup &S, float dmax_lo, float dmax_hi, float &t) {
+    const f3 d = {d4.x, d4.y, d4.z};
+    const float F0 = dotf(d, S.n0), F1 = dotf(d, S.n1), F2 = dotf(d, S.n2);
+    if (F0 < -S.B0 || F1 < -S.B1 || F2 < -S.B2) return 0;
+    if (!(F0 > S.B0 && F1 > S.B1 && F2 > S.B2)) return 2;
+    const float dN = dotf(d, S.N);
+    if (!(dN >= S.TN)) return 2;
+    t = __fdiv_rn(S.habs, dN);
+    if (t <= dmax_lo) return 1;
+    if (t > dmax_hi) return 0;
+    return 2;
+}
+
+// fp64 decision (canonical edges, closed triangle, 0 < t <= dmax).  1 = hit.
+__device__ __noinline__ int test_exact(const f3 v[3], f3 o, float4 d4, double dmax, int faces, float &tout) {
+    const d3 d = {(double)d4.x, (double)d4.y, (double)d4.z};
+    const d3 O = tod(o);
+    double F[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        f3 P = v[k], Q = v[(k + 1) % 3];
+        const bool sw = lexless(Q, P);
+        if (sw) { f3 t = P; P = Q; Q = t; }
+        d3 aP = subd(tod(P), O), e = subd(tod(Q), tod(P));
+        double f = dotd(d, crossd(aP, e));
+        F[k] = sw ? -f : f;
+    }
+    d3 V0 = tod(v[0]);
+    d3 N = crossd(subd(tod(v[1]), V0), subd(tod(v[2]), V0));
+    double h = dotd(N, subd(V0, O));
+    if (!(h > 0.0 || h < 0.0)) return 0;
+    if ((faces == 1 && h < 0.0) || (faces == 2 && h > 0.0)) return 0;
+    if (h < 0.0) { F[0] = -F[0]; F[1] = -F[1]; F[2] = -F[2]; }
+    if (F[0] < 0.0 || F[1] < 0.0 || F[2] < 0.0) return 0;
+    double dN = dotd(d, N);
+    if (!(dN > 0.0 || dN < 0.0)) return 0;
+    double t = h / dN;
+    if (!(t > 0.0 && t <= dmax)) return 0;
+    tout = (float)t;
+    return 1;
+}
+
+// Closest-hit update on the packed key (fp32 t bits << 32 | id).  t > 0 so the raw bits
+// order like the value (PAPER.md:2343-2356 f_sort, widened with the id as tie-break).
+__device__ __forceinline__ void record_hit(unsigned long long *hits, unsigned *allhits, int g, float t, uint32_t id) {
+    const unsigned long long key = ((unsigned long long)__float_as_uint(t) << 32) | id;
+    if (allhits) atomicAdd(allhits + g, 1u);
+    const unsigned long long cur = __ldcg(hits + g);
+    if (key < cur) atomicMin(hits + g, key);
+}
+
+}  // namespace grca

@@ -381,3 +381,58 @@ def random_scene(seed: int, n_tris: int = 300, n_emitters: int = 2, gamma: int =
                            max_range=(INF if max_range is None else max_range * (1 + k))))
     tris = random_triangles(rng, n_tris, center=(0, 0, 0), half_extent=extent, edge_lo=0.05, edge_hi=6.0)
     return ems, tris
+
+
+def place_emitters(n: int, bbox, seed: int, gamma: int = 128, chi: int = 4096, hfovs=None,
+                   max_range: Optional[float] = 1000.0, height: float = 2.0) -> List[Emitter]:
+    """seeded uniform positions inside the bbox footprint at 2 m above ground,
+    yaw uniform, level (u = +z); the paper's full-sphere grid."""
+    rng = np.random.default_rng([int(seed), 0xE317])
+    X, Y, _ = bbox
+    out = []
+    for k in range(n):
+        pos = (rng.uniform(0.1 * X, 0.9 * X), rng.uniform(0.1 * Y, 0.9 * Y), height)
+        f, r, u = yaw_frame(rng.uniform(-math.pi, math.pi))
+        out.append(Emitter(origin=pos, forward=f, right=r, up=u, elev=full_sphere_elev(gamma), rays_per_channel=chi,
+                           hfov_deg=(hfovs[k] if hfovs else 360),
+                           max_range=INF if max_range is None else float(max_range)))
+    return out
+
+
+WORKLOADS = {
+    # name: (n_emitters, hfovs, bbox, n_static, n_cars, default range, car scale range)
+    "C2": (2, None, (240.0, 80.0, 60.0), 700_000, 1, None, (0.001, 30.0)),
+    "C3": (4, [360, 360, 180, 180], (400.0, 150.0, 120.0), 3_500_000, 5, 50.0, (0.001, 30.0)),
+    "C4": (8, None, (611.0, 186.0, 249.0), 12_759_246, 30, 1000.0, (0.001, 30.0)),
+    "C5": (2, None, (240.0, 80.0, 60.0), 700_000, 1, None, (1.0, 1.0)),
+}
+
+
+def workload(name: str, frame: int = 0, deformation: str = "ND", static_scale: float = 1.0,
+             max_range=-1.0, subdiv: int = 0, n_cars: Optional[int] = None) -> dict:
+    """BASELINE.json configs as concrete seeded scenes.
+
+    Returns dict(emitters, tris = static + dynamic (n, 3, 3) fp32, n_static, n_dynamic, bbox,
+    poses).  Scene seed = config id; motion seed = (config id, frame).
+    """
+    if name == "C1":
+        return {"emitters": [c1_emitter()], "tris": c1_scene(), "n_static": 2000, "n_dynamic": 0,
+                "bbox": (40.0, 40.0, 30.0), "poses": []}
+    n_em, hfovs, bbox, n_static, cars, rng_default, (slo, shi) = WORKLOADS[name]
+    seed = int(name[1:])
+    if n_cars is not None:
+        cars = n_cars
+    rng_m = rng_default if (max_range is not None and max_range < 0) else max_range
+    ems = place_emitters(n_em, bbox, seed, hfovs=hfovs, max_range=rng_m)
+    static = plant(max(1, int(n_static * static_scale)), bbox=bbox, seed=seed)
+    local = car()
+    if subdiv:
+        local = subdivide(local, subdiv)
+    poses = pose_instances(cars, bbox, seed, frame, scale_lo=slo, scale_hi=shi)
+    dyn = [apply_pose(local, p) for p in poses]
+    dynamic = np.concatenate(dyn, 0) if dyn else np.zeros((0, 3, 3), np.float32)
+    if deformation == "SWD":
+        dynamic = swd(dynamic, bbox, seed, frame)
+    tris = np.ascontiguousarray(np.concatenate([static, dynamic], 0))
+    return {"emitters": ems, "tris": tris, "n_static": static.shape[0], "n_dynamic": dynamic.shape[0],
+            "bbox": bbox, "poses": poses, "car_local": local}

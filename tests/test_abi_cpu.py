@@ -1,0 +1,96 @@
+"""Host-side checks of the C-ABI library (no GPU needed): it builds for sm_100a, loads, and
+exports every entry point include/grca.h declares; the binding raises without the .so."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2605_10457_b200.build import build
+
+    path = build()
+    from paper_2605_10457_b200 import grca
+
+    return grca.load(path)
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "grca.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(grca_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_boundary():
+    names = _declared()
+    for must in ("grca_create", "grca_set_emitters", "grca_update_triangles", "grca_cast", "grca_destroy"):
+        assert must in names
+    from paper_2605_10457_b200.grca import EXPORTS
+
+    assert sorted(EXPORTS) == names
+
+
+def test_library_exports_every_symbol(lib):
+    for name in _declared():
+        assert hasattr(lib, name), name
+    nm = subprocess.run(["nm", "-D", "--defined-only", lib._name], capture_output=True, text=True).stdout
+    for name in _declared():
+        assert re.search(rf"\bT {name}\b", nm), name
+
+
+def test_version_and_sm100a(lib):
+    from paper_2605_10457_b200 import grca
+
+    assert "sm_100a" in grca.version()
+    out = subprocess.run(["cuobjdump", "--list-elf", lib._name], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_create_without_gpu_fails_cleanly(lib):
+    """On a host with no device, grca_create returns an error status (no crash, no fallback)."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("has a GPU")
+    import ctypes as C
+
+    from paper_2605_10457_b200.grca import CreateInfo
+
+    ci = CreateInfo()
+    ci.max_triangles, ci.max_rays = 10, 10
+    h = C.c_void_p()
+    st = lib.grca_create(C.byref(ci), C.byref(h))
+    assert st != 0 and not h.value
+    assert len(lib.grca_last_error(None)) > 0
+
+
+def test_binding_raises_without_library(tmp_path):
+    from paper_2605_10457_b200 import grca
+
+    saved = grca._lib
+    grca._lib = None
+    try:
+        with pytest.raises(ImportError):
+            grca.load(str(tmp_path / "missing.so"))
+    finally:
+        grca._lib = saved
+
+
+def test_oracle_not_imported_by_product():
+    """The product package never imports the oracle, and the oracle never imports the product."""
+    pkg = os.path.join(ROOT, "paper_2605_10457_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, flags=re.M), f
+                assert "liboracle" not in txt and "grca_oracle" not in txt, f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".py", ".c")):
+            txt = open(os.path.join(ROOT, "oracle", f)).read()
+            assert not re.search(r"^\s*(import|from)\s+paper_2605_10457_b200\b", txt, flags=re.M), f
+            assert '#include "grca.h"' not in txt and "libgrca" not in txt, f

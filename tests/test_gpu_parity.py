@@ -1,0 +1,313 @@
+"""Parity of the CUDA path (through the C ABI) with the brute-force oracle (-m gpu).
+
+Contract (BASELINE.json north star; oracle/compare.py): >= 99.999 % of rays agree, every
+disagreement lies within 1e-6 barycentric of a triangle edge, |t_G - t_O| <= 1e-5 t_O, ids
+equal except at near-ties.  Scenes are seeded synthetic (scenegen); sizes span several K2
+tiles (256 triangles) with ragged tails; full-size configs are checked on sampled rays.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import scenegen as sg
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU hosts collect but skip
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2605_10457_b200 import Grca, GrcaError, tris_to_float4  # noqa: E402
+from paper_2605_10457_b200 import grca as G  # noqa: E402
+
+
+def run(ems, tris, ids=None, faces=0, flags=0, small_max=0, max_large=0, indexed=False, handle=None):
+    n_rays = sg.n_rays_total(ems)
+    g = handle or Grca(device=0, max_triangles=max(1, len(tris)), max_rays=n_rays, faces=faces, debug_flags=flags,
+                       small_max=small_max, max_large_items=max_large)
+    g.set_emitters(ems)
+    tid = None if ids is None else torch.as_tensor(np.asarray(ids, np.int32), device="cuda")
+    if indexed and len(tris):
+        flat = np.asarray(tris, np.float32).reshape(-1, 3)
+        uniq, inv = np.unique(flat, axis=0, return_inverse=True)
+        v4 = tris_to_float4(uniq)
+        idx = torch.as_tensor(inv.astype(np.int32).reshape(-1), device="cuda")
+        g.update_triangles(v4, indices=idx, tri_ids=tid)
+    else:
+        v4 = tris_to_float4(tris) if len(tris) else torch.zeros((4, 4), device="cuda")
+        g.update_triangles(v4, tri_ids=tid, n_triangles=len(tris))
+    dist, tri, st = g.cast(stats=True)
+    torch.cuda.synchronize()
+    return dist.cpu().numpy(), tri.cpu().numpy(), st, g
+
+
+def check(ems, tris, dist, tri, ids=None, faces=0, rays=None, ref=None):
+    if ref is None:
+        ref = oracle.cast(ems, tris, ids=ids, faces=faces, rays=rays, want_t64=True)
+    sel = ref["rays"]
+    rep = oracle.compare(ems, tris, dist[sel], tri[sel], ref, ids=ids, faces=faces)
+    assert rep["passed"], {k: rep[k] for k in ("rays", "agree_frac", "unexcused", "kinds", "details")}
+    return rep, ref
+
+
+# ------------------------------------------------------------- ray table ----
+
+def test_ray_table_bit_identical_to_oracle():
+    """O1: the library's host-fp64 ray table equals the oracle's bit for bit."""
+    rng = np.random.default_rng(0)
+    ems = [sg.c1_emitter()]
+    for k in range(4):
+        f, r, u = sg.random_frame(rng)
+        ems.append(sg.Emitter(origin=rng.normal(size=3) * 50, forward=f, right=r, up=u,
+                              elev=sg.full_sphere_elev(64) if k % 2 else sg.vlp16_elev(),
+                              rays_per_channel=1000 + 37 * k, hfov_deg=360 if k % 2 else 180))
+    g = Grca(device=0, max_triangles=1, max_rays=sg.n_rays_total(ems))
+    g.set_emitters(ems)
+    mine = g.debug_ray_table()
+    ref = oracle.ray_table(ems)
+    assert mine.shape == ref.shape
+    assert np.array_equal(mine.view(np.uint32), ref.view(np.uint32))
+
+
+# ------------------------------------------------------------------ C1 ------
+
+@pytest.mark.parametrize("max_range", [math.inf, 10.0])
+def test_c1_full_frame(max_range):
+    """BASELINE config 1: 1 LiDAR 16x512, 2,000-triangle static scene, every ray."""
+    ems = [sg.c1_emitter(max_range=max_range)]
+    tris = sg.c1_scene()
+    dist, tri, st, _ = run(ems, tris)
+    rep, ref = check(ems, tris, dist, tri)
+    assert rep["oracle_hits"] > 1000
+    assert st["rtic_tested"] < st["rtic_brute"]
+    assert st["pairs"] == len(tris)
+
+
+@pytest.mark.parametrize("fixture", ["quad", "seam", "ground", "room", "zenith"])
+def test_fixtures_alone(fixture):
+    """SURVEY 8c fixtures as unit scenes (quad at known distance, seam straddler, nadir, box)."""
+    em = sg.c1_emitter()
+    o = em.origin.astype(np.float64)
+    tris = {
+        "quad": sg.quad_x5(o), "seam": sg.seam_triangle(o), "ground": sg.ground_quad(1.5, 50.0, o),
+        "room": sg.room_box(o + [-2, -3, -1], o + [4, 2, 2.5]),
+        "zenith": np.array([[[-1.0, -1.0, 4.0], [2.0, -1.0, 4.0], [0.0, 2.0, 4.0]]], np.float32),
+    }[fixture]
+    dist, tri, _, _ = run([em], tris)
+    rep, ref = check([em], tris, dist, tri)
+    assert rep["oracle_hits"] > 0
+    if fixture == "quad":
+        g = 8 * 512 + 256
+        assert dist[g] == 5.0 and tri[g] == 0
+    if fixture == "seam":
+        assert tri[8 * 512] == 0 and tri[8 * 512 + 511] == 0
+    if fixture == "ground":
+        assert np.all(dist[:512] == np.float32(1.5))   # nadir channel: all 512 rays at t = h
+    if fixture == "room":
+        assert np.all(tri >= 0)
+
+
+def test_watertight_shared_diagonal():
+    """Rays aimed at the shared diagonal of a quad: every one hits at least one triangle."""
+    em = sg.Emitter(origin=(0, 0, 0), elev=np.linspace(-0.19, 0.19, 401).astype(np.float32),
+                    rays_per_channel=4096)
+    tris = sg.quad_x5()
+    dist, tri, _, _ = run([em], tris)
+    check([em], tris, dist, tri)
+    D = oracle.ray_table([em]).astype(np.float64)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        y = 5 * D[:, 1] / D[:, 0]
+        z = 5 * D[:, 2] / D[:, 0]
+    near_diag = (D[:, 0] > 0) & (np.abs(y - z) < 1e-3) & (np.abs(y) < 0.99) & (np.abs(z) < 0.99)
+    assert near_diag.sum() > 50
+    assert np.all(tri[near_diag] >= 0)
+
+
+# ------------------------------------------------------- random sweeps ------
+
+@pytest.mark.parametrize("seed", list(range(20)))
+def test_random_scenes(seed):
+    """20 seeded scenes: random frames, 360/180 deg, non-uniform tables, range limits, ragged sizes."""
+    n_em = 1 + seed % 3
+    ems, tris = sg.random_scene(seed, n_tris=257 + 97 * seed, n_emitters=n_em, gamma=8 + seed % 9,
+                                chi=64 + 13 * seed, extent=6.0 + seed,
+                                max_range=None if seed % 4 else 5.0 + seed)
+    dist, tri, st, _ = run(ems, tris)
+    rep, _ = check(ems, tris, dist, tri)
+    assert st["rtic_tested"] <= st["rtic_brute"]
+
+
+def test_all_hits_invariant():
+    """Culling never drops a brute-force hit: per-ray all-hit counts equal the oracle's."""
+    for seed in (1, 2, 3):
+        ems, tris = sg.random_scene(100 + seed, n_tris=800, n_emitters=2, gamma=16, chi=200, extent=8.0)
+        dist, tri, st, g = run(ems, tris, flags=G.DEBUG_COUNT_ALL_HITS)
+        counts = g.debug_all_hits().cpu().numpy()
+        ref = oracle.cast(ems, tris, want_t64=True, want_allhits=True)
+        check(ems, tris, dist, tri, ref=ref)
+        diff = np.nonzero(counts != ref["allhits"])[0]
+        assert len(diff) <= 1e-5 * len(counts) + 1, (len(diff), diff[:10])
+    ems = [sg.c1_emitter()]
+    tris = sg.c1_scene()
+    dist, tri, st, g = run(ems, tris, flags=G.DEBUG_COUNT_ALL_HITS)
+    ref = oracle.cast(ems, tris, want_allhits=True)
+    assert np.array_equal(g.debug_all_hits().cpu().numpy(), ref["allhits"])
+
+
+def test_no_cull_and_fp64_modes_bit_identical():
+    """Invariant (5): culling off (full grid per pair) and all-fp64 give the same packed result."""
+    ems, tris = sg.random_scene(7, n_tris=600, n_emitters=2, gamma=12, chi=128)
+    base = run(ems, tris)
+    nocull = run(ems, tris, flags=G.DEBUG_NO_CULL)
+    f64 = run(ems, tris, flags=G.DEBUG_FORCE_FP64)
+    for other in (nocull, f64):
+        assert np.array_equal(base[1], other[1])
+        assert np.array_equal(base[0].view(np.uint32), other[0].view(np.uint32))
+    assert nocull[2]["rtic_tested"] == nocull[2]["rtic_brute"]
+    check(ems, tris, base[0], base[1])
+
+
+@pytest.mark.parametrize("small_max,max_large", [(1, 0), (100000, 0), (0, 3), (1, 2)])
+def test_binning_and_capacity_paths(small_max, max_large):
+    """All-large, all-inline and capacity-overflow fallbacks give identical results."""
+    ems, tris = sg.random_scene(11, n_tris=700, n_emitters=2, gamma=16, chi=300, extent=5.0)
+    base = run(ems, tris)
+    alt = run(ems, tris, small_max=small_max, max_large=max_large)
+    assert np.array_equal(base[1], alt[1]) and np.array_equal(base[0].view(np.uint32), alt[0].view(np.uint32))
+    if max_large:
+        assert alt[2]["overflow"] == 1
+
+
+@pytest.mark.parametrize("faces", [1, 2])
+def test_face_modes(faces):
+    ems, tris = sg.random_scene(21, n_tris=500, n_emitters=2)
+    dist, tri, _, _ = run(ems, tris, faces=faces)
+    check(ems, tris, dist, tri, faces=faces)
+
+
+def test_indexed_ids_and_determinism():
+    """Indexed meshes == triangle soup; custom ids travel; two casts are bit-identical."""
+    tris = np.concatenate([sg.car(40, 40, dims=(4.0, 2.0, 1.2)) + np.float32([6, 1, 0]),
+                           sg.grid_mesh(20, 20, -10, -10, 10, 10, -1.5)], 0)
+    ems = [sg.Emitter(origin=(0, 0, 0), elev=sg.full_sphere_elev(32), rays_per_channel=720)]
+    ids = (np.arange(len(tris), dtype=np.int32) * 3 + 5)
+    a = run(ems, tris, ids=ids)
+    b = run(ems, tris, ids=ids, indexed=True)
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
+    check(ems, tris, a[0], a[1], ids=ids)
+    g = a[3]
+    d2, t2 = g.cast()
+    assert np.array_equal(d2.cpu().numpy().view(np.uint32), a[0].view(np.uint32))
+
+
+def test_virtual_shards_min_merge():
+    """1-shard == min over P block-interleaved shards of the packed hit buffers (bit-exact)."""
+    ems, tris = sg.random_scene(31, n_tris=3000, n_emitters=2, gamma=16, chi=256, extent=10.0)
+    n = len(tris)
+    g = Grca(device=0, max_triangles=n, max_rays=sg.n_rays_total(ems))
+    g.set_emitters(ems)
+    v4 = tris_to_float4(tris)
+    g.update_triangles(v4)
+    g.cast_packed()
+    full = g.hits_packed().clone()
+    for P in (2, 3, 4):
+        blk = 256
+        owner = (np.arange(n) // blk) % P
+        merged = None
+        for r in range(P):
+            idx = np.nonzero(owner == r)[0]
+            g.update_triangles(tris_to_float4(tris[idx]), tri_ids=torch.as_tensor(idx.astype(np.int32), device="cuda"))
+            g.cast_packed()
+            h = g.hits_packed().clone()
+            merged = h if merged is None else torch.minimum(merged, h)
+        assert torch.equal(merged, full)
+    dist = torch.empty(g.n_rays, device="cuda")
+    tri = torch.empty(g.n_rays, dtype=torch.int32, device="cuda")
+    g.update_triangles(v4)
+    g.cast_packed()
+    g.unpack(dist, tri)
+    check(ems, tris, dist.cpu().numpy(), tri.cpu().numpy())
+
+
+def test_edge_cases():
+    """Empty scene, degenerate / NaN / origin-coplanar triangles, origin on a vertex."""
+    em = sg.c1_emitter()
+    o = em.origin
+    dist, tri, _, _ = run([em], np.zeros((0, 3, 3), np.float32))
+    assert np.all(tri == -1) and np.all(np.isinf(dist))
+    bad = np.array([
+        [[5, 0, 0], [5, 0, 0], [5, 1, 1]],                                   # zero-area
+        [[np.nan, 0, 0], [5, 1, 0], [5, 0, 1]],                              # NaN
+        [o, o + [1, 0, 0], o + [0, 1, 0]],                                   # origin is a vertex
+        [o + [1, -1, 0], o + [2, 1, 0], o + [3, -1, 0]],                     # plane through origin
+        [o + [4, -1, -1], o + [4, 1, -1], o + [4, 0, 1]],                    # a normal one
+    ], dtype=np.float32)
+    dist, tri, _, _ = run([em], bad)
+    check([em], bad, dist, tri)
+    assert set(np.unique(tri)) <= {-1, 4}
+
+
+def test_api_errors():
+    g = Grca(device=0, max_triangles=10, max_rays=1000)
+    with pytest.raises(GrcaError) as e:
+        g.cast()
+    assert e.value.status == G.GRCA_E_STATE
+    with pytest.raises(GrcaError) as e:
+        g.set_emitters([sg.Emitter(origin=(0, 0, 0), elev=np.float32([0.1, 0.0]), rays_per_channel=10)])
+    assert e.value.status == G.GRCA_E_INVALID
+    with pytest.raises(GrcaError) as e:
+        g.set_emitters([sg.Emitter(origin=(0, 0, 0), elev=sg.full_sphere_elev(16), rays_per_channel=512)])
+    assert e.value.status == G.GRCA_E_CAPACITY
+    with pytest.raises(GrcaError):
+        g.set_emitters([sg.Emitter(origin=(0, 0, 0), forward=(1, 0, 0), right=(1, 0, 0), elev=np.float32([0]),
+                                   rays_per_channel=8)])
+    g.set_emitters([sg.Emitter(origin=(0, 0, 0), elev=np.float32([0.0]), rays_per_channel=8)])
+    with pytest.raises(GrcaError) as e:
+        g.update_triangles(tris_to_float4(np.zeros((11, 3, 3), np.float32)))
+    assert e.value.status == G.GRCA_E_CAPACITY
+
+
+# --------------------------------------------------- larger, sampled rays ----
+
+def _sampled(ems, n_per_emitter, seed):
+    rng = np.random.default_rng(seed)
+    out, base = [], 0
+    for e in ems:
+        out.append(base + rng.choice(e.n_rays, size=min(n_per_emitter, e.n_rays), replace=False))
+        base += e.n_rays
+    return np.sort(np.concatenate(out)).astype(np.int64)
+
+
+def test_c2_like_sampled():
+    """C2-shaped (2 LiDARs 128x4096, plant + car, f.i), reduced triangle count, 4,096 sampled rays."""
+    w = sg.workload("C2", frame=0, static_scale=0.25)
+    tris = w["tris"]
+    dist, tri, st, _ = run(w["emitters"], tris)
+    rays = _sampled(w["emitters"], 2048, 5)
+    rep, _ = check(w["emitters"], tris, dist, tri, rays=rays)
+    assert rep["oracle_hits"] > 100
+    assert st["rtic_tested"] < 1e-3 * st["rtic_brute"]
+
+
+@pytest.mark.parametrize("rng_m", [10.0, 50.0])
+def test_c3_like_ranged_sampled(rng_m):
+    """C3-shaped: 4 LiDARs mixed 360/180 deg with range culling; reduced scene; sampled rays."""
+    w = sg.workload("C3", frame=1, static_scale=0.05, max_range=rng_m)
+    dist, tri, st, _ = run(w["emitters"], w["tris"])
+    rays = _sampled(w["emitters"], 1024, 6)
+    check(w["emitters"], w["tris"], dist, tri, rays=rays)
+    assert st["range_culled"] > 0
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled():
+    """C4 at full size (8 x 128x4096 rays, ~21.8M triangles), in the launch configuration
+    bench.py times, checked on sampled rays against the oracle (all triangles per ray)."""
+    w = sg.workload("C4", frame=0)
+    dist, tri, st, _ = run(w["emitters"], w["tris"])
+    rays = _sampled(w["emitters"], 24, 9)
+    rep, _ = check(w["emitters"], w["tris"], dist, tri, rays=rays)
+    assert st["pairs"] == len(w["tris"]) * 8
+    assert rep["oracle_hits"] > 20
