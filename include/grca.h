@@ -63,7 +63,8 @@ enum {
 
 typedef struct {
     int32_t device;          /* CUDA device ordinal */
-    void *stream;            /* cudaStream_t (e.g. torch's current stream); NULL -> library-owned stream */
+    void *stream;            /* cudaStream_t all work is enqueued on (e.g. torch's current stream);
+                                NULL -> the legacy default stream */
     int32_t nranks, rank;    /* informational: the caller shards triangles / emitters and merges */
     int64_t max_triangles;   /* per handle; fixes scratch sizes so grca_cast never allocates */
     int64_t max_rays;        /* upper bound of sum_n gamma_n chi_n */

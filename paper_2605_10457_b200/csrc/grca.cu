@@ -584,16 +584,9 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
         return GRCA_E_CUDA;
     }
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, h->device);
-    if (ci->stream) {
-        h->stream = (cudaStream_t)ci->stream;
-    } else {
-        if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
-            g_create_err = "cudaStreamCreate failed";
-            delete h;
-            return GRCA_E_CUDA;
-        }
-        h->own_stream = true;
-    }
+    // NULL -> the legacy default stream (what torch's default stream is), never a private one
+    h->stream = (cudaStream_t)ci->stream;
+    h->own_stream = false;
     const long long mt = std::max<long long>(1, ci->max_triangles);
     h->cap_large = ci->max_large_items > 0 ? ci->max_large_items : std::max<long long>(1ll << 20, mt / 4);
     h->cap_chunks = 4 * h->cap_large;

@@ -58,7 +58,7 @@ __device__ __forceinline__ f3 crossf(f3 a, f3 b) {
     return {__fmaf_rn(a.y, b.z, -__fmul_rn(a.z, b.y)), __fmaf_rn(a.z, b.x, -__fmul_rn(a.x, b.z)),
             __fmaf_rn(a.x, b.y, -__fmul_rn(a.y, b.x))};
 }
-__device__ __forceinline__ f3 scalef(f3 a, float s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ f3 scalef(f3 a, float s) { return {__fmul_rn(a.x, s), __fmul_rn(a.y, s), __fmul_rn(a.z, s)}; }
 __device__ __forceinline__ d3 tod(f3 a) { return {(double)a.x, (double)a.y, (double)a.z}; }
 __device__ __forceinline__ d3 subd(d3 a, d3 b) { return {__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y), __dsub_rn(a.z, b.z)}; }
 __device__ __forceinline__ double dotd(d3 a, d3 b) {
@@ -319,16 +319,16 @@ __device__ __forceinline__ bool make_setup(const f3 v[3], f3 o, int faces, Setup
         sg[k] = sw ? -1.f : 1.f;
         f3 aP = subf(P, o), e = subf(Q, P);
         n[k] = crossf(aP, e);
-        B[k] = 16.f * kU * sqrtf(dotf(aP, aP)) * sqrtf(dotf(e, e));
+        B[k] = __fmul_rn(__fmul_rn(16.f * kU, sqrtf(dotf(aP, aP))), sqrtf(dotf(e, e)));
     }
     f3 e1 = subf(v[1], v[0]), e2 = subf(v[2], v[0]);
     f3 N = crossf(e1, e2);
     f3 a0 = subf(v[0], o);
     float h = dotf(N, a0);
-    float nE = sqrtf(dotf(e1, e1)) * sqrtf(dotf(e2, e2));
+    float nE = __fmul_rn(sqrtf(dotf(e1, e1)), sqrtf(dotf(e2, e2)));
     float nN = sqrtf(dotf(N, N));
     float na0 = sqrtf(dotf(a0, a0));
-    float Bh = (8.f * kU * nE + 6.f * kU * nN) * na0;
+    float Bh = __fmul_rn(__fadd_rn(__fmul_rn(8.f * kU, nE), __fmul_rn(6.f * kU, nN)), na0);
     float s;
     bool force64 = false;
     if (!(fabsf(h) > 2.f * Bh)) {
@@ -347,9 +347,9 @@ __device__ __forceinline__ bool make_setup(const f3 v[3], f3 o, int faces, Setup
     S.B0 = B[0]; S.B1 = B[1]; S.B2 = B[2];
     S.N = scalef(N, s);
     S.habs = fabsf(h);
-    const float rh = Bh / fabsf(h);
-    const float Bn = 8.f * kU * nE + 4.f * kU * nN;
-    S.TN = (force64 || !(rh < 2e-6f)) ? CUDART_INF_F : Bn / (kTRel - 2.f * kU - rh);
+    const float rh = __fdiv_rn(Bh, fabsf(h));
+    const float Bn = __fadd_rn(__fmul_rn(8.f * kU, nE), __fmul_rn(4.f * kU, nN));
+    S.TN = (force64 || !(rh < 2e-6f)) ? CUDART_INF_F : __fdiv_rn(Bn, __fsub_rn(kTRel - 2.f * kU, rh));
     return true;
 }
 
