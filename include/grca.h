@@ -163,6 +163,10 @@ grca_status grca_kernel_times(grca_t h, int32_t n_last, float *ms_per_kernel);
  * device pointer to uint32[n_rays]. */
 grca_status grca_debug_all_hits(grca_t h, const uint32_t **d_counts);
 
+/* Test/diagnostic: copy up to cap entries of the last cast's large-pair list to host memory as
+ * int32[4] {tri, emitter | c_from << 8, c_to, r_lo | r_len << 16}; *n_out = entries appended. */
+grca_status grca_debug_large_list(grca_t h, int32_t *h_out, int64_t cap, int64_t *n_out);
+
 /* n_rays_total and ray_offsets[n_emitters + 1] (O_n) of the current emitters. */
 grca_status grca_get_layout(grca_t h, int64_t *n_rays_total, int64_t *ray_offsets);
 

@@ -930,6 +930,18 @@ grca_status grca_debug_all_hits(grca_t h, const uint32_t **d_counts) {
     return GRCA_OK;
 }
 
+grca_status grca_debug_large_list(grca_t h, int32_t *h_out, int64_t cap, int64_t *n_out) {
+    if (!h || !n_out) return GRCA_E_INVALID;
+    DeviceGuard dg(h->device);
+    unsigned n = 0;
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(&n, h->d_ctrl, sizeof(unsigned), cudaMemcpyDeviceToHost));
+    const long long m = std::min<long long>(std::min<long long>(n, h->cap_large), cap);
+    if (h_out && m > 0) CK(cudaMemcpy(h_out, h->d_large, sizeof(int4) * m, cudaMemcpyDeviceToHost));
+    *n_out = n;
+    return GRCA_OK;
+}
+
 grca_status grca_get_layout(grca_t h, int64_t *n_rays_total, int64_t *ray_offsets) {
     if (!h) return GRCA_E_INVALID;
     if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");

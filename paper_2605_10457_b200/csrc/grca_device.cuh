@@ -197,7 +197,12 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, boo
         neg |= (w < -eps);
         near_axis |= (x[k].x * x[k].x + x[k].y * x[k].y) < kNearAxis2 * r2[k];
     }
-    const bool pole = !(pos && neg);
+    // The axis can only meet T if T's horizontal projection straddles it on both coordinates
+    // (this rejects degenerate, e.g. radial vertical, projections whose windings all round to ~0).
+    const float tolb = 16.f * kU * sqrtf(fmaxf(r2[0], fmaxf(r2[1], r2[2])));
+    const bool straddle = fminf(x[0].x, fminf(x[1].x, x[2].x)) <= tolb && fmaxf(x[0].x, fmaxf(x[1].x, x[2].x)) >= -tolb &&
+                          fminf(x[0].y, fminf(x[1].y, x[2].y)) <= tolb && fmaxf(x[0].y, fmaxf(x[1].y, x[2].y)) >= -tolb;
+    const bool pole = straddle && !(pos && neg);
     if (pole) {
         if (shi > 0.f) shi = 1.f;
         if (slo < 0.f) slo = -1.f;

@@ -22,7 +22,7 @@ DEBUG_COUNT_ALL_HITS, DEBUG_NO_CULL, PROFILE_KERNELS, DEBUG_FORCE_FP64 = 1, 2, 4
 EXPORTS = [
     "grca_create", "grca_destroy", "grca_set_emitters", "grca_update_triangles", "grca_cast",
     "grca_cast_packed", "grca_hits_packed", "grca_unpack", "grca_get_stats", "grca_kernel_times",
-    "grca_debug_all_hits", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
+    "grca_debug_all_hits", "grca_debug_large_list", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
 ]
 
 
@@ -85,6 +85,7 @@ def load(path: str = LIB_PATH):
         "grca_get_stats": ([vp, C.POINTER(Stats)], C.c_int),
         "grca_kernel_times": ([vp, i32, C.POINTER(C.c_float)], C.c_int),
         "grca_debug_all_hits": ([vp, C.POINTER(vp)], C.c_int),
+        "grca_debug_large_list": ([vp, vp, i64, C.POINTER(i64)], C.c_int),
         "grca_get_layout": ([vp, C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "grca_debug_ray_table": ([vp, vp], C.c_int),
         "grca_last_error": ([vp], C.c_char_p),
@@ -254,6 +255,15 @@ class Grca:
         p = C.c_void_p()
         self._check(self._L.grca_debug_all_hits(self._h, C.byref(p)))
         return torch.as_tensor(_CudaArray(int(p.value), self.n_rays, "<u4"), device=f"cuda:{self.device}")
+
+    def debug_large_list(self, cap: int = 1 << 22):
+        """Large-pair list of the last cast: int32 (n, 4) {tri, e | c_from << 8, c_to, r_lo | r_len << 16}."""
+        import numpy as np
+
+        out = np.empty((cap, 4), dtype=np.int32)
+        n = C.c_int64()
+        self._check(self._L.grca_debug_large_list(self._h, out.ctypes.data, cap, C.byref(n)))
+        return out[: min(cap, int(n.value))]
 
     def debug_ray_table(self):
         import numpy as np
