@@ -106,7 +106,7 @@ typedef struct {
     int64_t overflow_inline; /* large pairs processed inline because the list was full */
     int32_t overflow;        /* 1 if any capacity fallback happened */
     float ms_total;          /* device time of the last cast if GRCA_PROFILE_KERNELS */
-    float ms_k[8];           /* per kernel: K0 init, K2 cull, K3 bin, K4 intersect, K5 unpack */
+    float ms_k[8];           /* per kernel: K0 init, K2 cull, K2b refine+inline, K3 bin, K4 intersect, K5 unpack */
 } grca_stats;
 
 /* Create a handle bound to ci->device.  Allocates all device scratch.
@@ -155,8 +155,8 @@ grca_status grca_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri);
 grca_status grca_get_stats(grca_t h, grca_stats *h_stats);
 
 /* Sum of per-kernel device times over the last n_last casts (GRCA_PROFILE_KERNELS only;
- * n_last in [1, 64]; synchronizes).  ms_per_kernel[8]: [0] K0 init, [1] K2 cull (incl. inline
- * small work), [2] K3 bin, [3] K4 intersect, [4] K5 unpack, [7] whole cast. */
+ * n_last in [1, 64]; synchronizes).  ms_per_kernel[8]: [0] K0 init, [1] K2 cull (phase A),
+ * [2] K2b refine + inline small work, [3] K3 bin, [4] K4 intersect, [5] K5 unpack, [7] whole cast. */
 grca_status grca_kernel_times(grca_t h, int32_t n_last, float *ms_per_kernel);
 
 /* Per-ray all-hit counts of the last cast (GRCA_DEBUG_COUNT_ALL_HITS only):

@@ -31,6 +31,7 @@ constexpr int K2_THREADS = 256;
 constexpr int K4_THREADS = 256;
 constexpr int kMaxEmitters = 255;
 constexpr int kMaxSin = 4096;
+constexpr int kLutMaxEm = 16;   // channel LUTs staged in smem for up to 16 emitters
 
 enum Stat {
     ST_PAIRS = 0, ST_RANGE, ST_CHANNEL, ST_AZIMUTH, ST_SURV, ST_SMALL, ST_LARGE, ST_ITEMS_SMALL,
@@ -56,12 +57,16 @@ struct KParams {
     unsigned long long *stats;
     int faces, nocull, force64, small_max;
     long long n_rays;
+    const EmLite *lite;
+    const unsigned short *lut;   // NULL -> binary search
+    unsigned short *surv;        // per tile: K2_THREADS * n_em entries (local_tri << 8 | emitter)
+    int *tile_count;
 };
 
 // slot fields (SoA per warp in shared memory) for the inline small-pair expansion
 enum SlotF {
     SF_N0 = 0, SF_N1 = 3, SF_N2 = 6, SF_B = 9, SF_N = 12, SF_HABS = 15, SF_TN = 16, SF_ID = 17,
-    SF_TRI = 18, SF_CFROM = 19, SF_RLO = 20, SF_LEN = 21, SF_INVLEN = 22, SF_EXCL = 23, NF = 24
+    SF_TRI = 18, SF_CFROM = 19, SF_RLO = 20, SF_LEN = 21, SF_INVLEN = 22, SF_EXCL = 23, SF_EM = 24, NF = 25
 };
 
 __device__ __forceinline__ f3 em_o(const EmDev &E) { return {E.o[0], E.o[1], E.o[2]}; }
@@ -96,8 +101,89 @@ __global__ void k_init(unsigned long long *hits, unsigned *allhits, long long n,
     if (tid < 4) ctrl[tid] = 0u;
 }
 
-// ---------------------------------------------------- K2 cull + inline small --
+// ------------------------------------------------------- K2 cull (phase A) --
+// Lean and dense: per triangle (fused K1 load) x per emitter, the O(1) elevation pre-test
+// (quick_cull).  Survivors are compacted per 256-triangle tile in shared memory and written to
+// the tile's own slot of the survivor buffer (no global atomics); K2b refines them.
 __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    EmLite *sL = reinterpret_cast<EmLite *>(smem);
+    float *sSin = reinterpret_cast<float *>(sL + P.n_em);
+    unsigned short *sLut = reinterpret_cast<unsigned short *>(sSin + ((P.n_sin + 3) & ~3));
+    unsigned short *sQ = sLut + (P.lut ? ((P.n_em * kLutBins + 7) & ~7) : 0);
+    __shared__ int qn;
+    __shared__ unsigned long long acc[ST_COUNT];
+    {
+        const int nw = P.n_em * (int)(sizeof(EmLite) / 4);
+        const int *src = reinterpret_cast<const int *>(P.lite);
+        int *dst = reinterpret_cast<int *>(sL);
+        for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = src[i];
+        for (int i = threadIdx.x; i < P.n_sin; i += blockDim.x) sSin[i] = P.sin[i];
+        if (P.lut)
+            for (int i = threadIdx.x; i < P.n_em * kLutBins; i += blockDim.x) sLut[i] = P.lut[i];
+        if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
+    }
+    const int lane = threadIdx.x & 31;
+    unsigned long long cnt[ST_COUNT];
+#pragma unroll
+    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
+    unsigned c_pairs = 0, c_range = 0, c_chan = 0;
+    const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (threadIdx.x == 0) qn = 0;
+        __syncthreads();
+        const long long t = tile * K2_THREADS + threadIdx.x;
+        const bool valid = t < P.n_tri;
+        f3 v[3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+        float emax = 0.f;
+        if (valid) {   // A1 (fused K1): coalesced float4 vertex loads, triangle diameter
+            load_tri(P.tri, t, v);
+            const float l0 = (v[1].x - v[0].x) * (v[1].x - v[0].x) + (v[1].y - v[0].y) * (v[1].y - v[0].y) +
+                             (v[1].z - v[0].z) * (v[1].z - v[0].z);
+            const float l1 = (v[2].x - v[1].x) * (v[2].x - v[1].x) + (v[2].y - v[1].y) * (v[2].y - v[1].y) +
+                             (v[2].z - v[1].z) * (v[2].z - v[1].z);
+            const float l2 = (v[0].x - v[2].x) * (v[0].x - v[2].x) + (v[0].y - v[2].y) * (v[0].y - v[2].y) +
+                             (v[0].z - v[2].z) * (v[0].z - v[2].z);
+            emax = sqrtf(fmaxf(l0, fmaxf(l1, l2))) * (1.f + 1e-5f);
+        }
+        for (int e = 0; e < P.n_em; ++e) {
+            int st = -1;
+            if (valid) {
+                ++c_pairs;
+                st = P.nocull ? CULL_KEEP
+                              : quick_cull(v, emax, sL[e], sSin + sL[e].sin_base,
+                                           P.lut ? sLut + sL[e].lut_base : nullptr);
+                c_range += (st == CULL_RANGE);
+                c_chan += (st == CULL_CHANNEL);
+            }
+            const bool keep = st == CULL_KEEP;
+            const unsigned m = __ballot_sync(FULL, keep);
+            if (m) {   // warp-aggregated append to the tile's shared-memory queue
+                const int leader = __ffs(m) - 1;
+                int base = 0;
+                if (lane == leader) base = atomicAdd(&qn, __popc(m));
+                base = __shfl_sync(FULL, base, leader);
+                if (keep) sQ[base + __popc(m & ((1u << lane) - 1u))] = (unsigned short)((threadIdx.x << 8) | e);
+            }
+        }
+        __syncthreads();
+        const int n = qn;
+        unsigned short *dst = P.surv + tile * (long long)K2_THREADS * P.n_em;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = sQ[i];
+        if (threadIdx.x == 0) P.tile_count[tile] = n;
+        __syncthreads();
+    }
+    cnt[ST_PAIRS] = c_pairs;
+    cnt[ST_RANGE] = c_range;
+    cnt[ST_CHANNEL] = c_chan;
+    block_flush(acc, P.stats, cnt);
+}
+
+// --------------------------------------------- K2b refine + inline small work --
+// Dense over the survivors of K2: exact bounds (cull_pair), then small rectangles are expanded
+// with a warp prefix scan and intersected inline; large ones are appended (warp-aggregated,
+// PAPER.md:2383-2393) to the large list for K3/K4.
+__global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     EmDev *sE = reinterpret_cast<EmDev *>(smem);
     float *sSin = reinterpret_cast<float *>(sE + P.n_em);
@@ -121,22 +207,29 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
 
     const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const long long t = tile * K2_THREADS + threadIdx.x;
-        const bool valid = t < P.n_tri;
-        f3 v[3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
-        uint32_t id = 0;
-        if (valid) {   // A1 (fused K1): coalesced float4 vertex gathers
-            load_tri(P.tri, t, v);
-            id = tri_id(P.tri, t);
-        }
-        for (int e = 0; e < P.n_em; ++e) {
-            const EmDev &E = sE[e];
+        const int n = P.tile_count[tile];
+        const unsigned short *q = P.surv + tile * (long long)K2_THREADS * P.n_em;
+        for (int b0 = 0; b0 < n; b0 += K2_THREADS) {
+            const int idx = b0 + threadIdx.x;
+            const bool act = idx < n;
+            int e = 0;
+            long long t = 0;
+            f3 v[3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+            uint32_t id = 0;
             Rect R;
-            int st = valid ? cull_pair(v, E, sSin + E.sin_base, P.nocull != 0, R) : -1;
+            int st = -1;
+            if (act) {
+                const unsigned ent = q[idx];
+                e = ent & 255;
+                t = tile * K2_THREADS + (ent >> 8);
+                load_tri(P.tri, t, v);
+                id = tri_id(P.tri, t);
+                st = cull_pair(v, sE[e], sSin + sE[e].sin_base, P.nocull != 0, R);
+            }
+            const EmDev &E = sE[e];
             long long items = 0;
             bool small = false, large = false;
             Setup S;
-            if (valid) cnt[ST_PAIRS]++;
             if (st == CULL_KEEP) {
                 items = rect_items(R, E);
                 if (items <= P.small_max && !R.pole_rows) {
@@ -150,7 +243,6 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
             else if (st == CULL_CHANNEL) cnt[ST_CHANNEL]++;
             else if (st == CULL_AZIMUTH) cnt[ST_AZIMUTH]++;
             else if (st == CULL_DEGENERATE) cnt[ST_DEGEN]++;
-            // large: warp-aggregated append (one atomic per warp)
             const unsigned lm = __ballot_sync(FULL, large);
             if (lm) {
                 const int leader = __ffs(lm) - 1;
@@ -190,8 +282,9 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
                 sl[SF_RLO * 32] = __int_as_float(R.r_lo);
                 sl[SF_LEN * 32] = __int_as_float(R.r_len);
                 sl[SF_INVLEN * 32] = 1.f / (float)R.r_len;
+                sl[SF_EM * 32] = __int_as_float(e);
             }
-            // A5: warp-level prefix scan work expansion of the small rectangles
+            // A5: warp-level prefix-scan work expansion of the small rectangles
             int incl = my;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -202,16 +295,17 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
             const int total = __shfl_sync(FULL, incl, 31);
             __syncwarp();
             for (int b = 0; b < total; b += 32) {
-                const int q = b + lane;
+                const int qi = b + lane;
                 int ow = 0;
 #pragma unroll
                 for (int s = 16; s > 0; s >>= 1) {
                     const int vv = __shfl_sync(FULL, incl, ow + s - 1);
-                    if (vv <= q) ow += s;
+                    if (vv <= qi) ow += s;
                 }
-                if (q < total) {
+                if (qi < total) {
                     const float *sl = slot + ow;
-                    const int local = q - __float_as_int(sl[SF_EXCL * 32]);
+                    const EmDev &EO = sE[__float_as_int(sl[SF_EM * 32])];
+                    const int local = qi - __float_as_int(sl[SF_EXCL * 32]);
                     const int len = __float_as_int(sl[SF_LEN * 32]);
                     int row = (int)(((float)local + 0.5f) * sl[SF_INVLEN * 32]);
                     int col = local - row * len;
@@ -219,8 +313,8 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
                     if (col >= len) { ++row; col -= len; }
                     const int j = __float_as_int(sl[SF_CFROM * 32]) + row;
                     int i = __float_as_int(sl[SF_RLO * 32]) + col;
-                    if (i >= E.chi) i -= E.chi;
-                    const int g = E.ray_base + j * E.chi + i;
+                    if (i >= EO.chi) i -= EO.chi;
+                    const int g = EO.ray_base + j * EO.chi + i;
                     const float4 d = __ldg(P.raytab + g);
                     Setup Q;
                     Q.n0 = {sl[(SF_N0 + 0) * 32], sl[(SF_N0 + 1) * 32], sl[(SF_N0 + 2) * 32]};
@@ -231,12 +325,12 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
                     Q.habs = sl[SF_HABS * 32];
                     Q.TN = sl[SF_TN * 32];
                     float th = 0.f;
-                    int r = P.force64 ? 2 : test_fast(d, Q, E.dmax_lo, E.dmax_hi, th);
+                    int r = P.force64 ? 2 : test_fast(d, Q, EO.dmax_lo, EO.dmax_hi, th);
                     if (r == 2) {
                         cnt[ST_FP64]++;
                         f3 w[3];
                         load_tri(P.tri, (long long)__float_as_int(sl[SF_TRI * 32]), w);
-                        r = test_exact(w, em_o(E), d, E.dmax, P.faces, th);
+                        r = test_exact(w, em_o(EO), d, EO.dmax, P.faces, th);
                     }
                     if (r == 1) {
                         cnt[ST_HITS]++;
@@ -449,7 +543,7 @@ __global__ void k_unpack(const unsigned long long *__restrict__ hits, float *__r
 using namespace grca;
 
 static constexpr int kRing = 64;
-static constexpr int kEv = 6;   // K0 start, after K0, after K2, after K3, after K4, after K5
+static constexpr int kEv = 7;   // K0 start, after K0, after K2, after K2b, after K3, after K4, after K5
 
 struct grca_ctx {
     int device = 0;
@@ -458,8 +552,8 @@ struct grca_ctx {
     grca_create_info ci{};
     std::string err;
     int num_sms = 148;
-    int k2_blocks_per_sm = 1, k4_blocks_per_sm = 1;
-    size_t k2_smem = 0;
+    int k2_blocks_per_sm = 1, k2b_blocks_per_sm = 1, k4_blocks_per_sm = 1;
+    size_t k2_smem = 0, k2b_smem = 0;
     // emitters
     int n_em = 0;
     int n_sin = 0;
@@ -471,6 +565,13 @@ struct grca_ctx {
     unsigned *d_allhits = nullptr;
     EmDev *d_em = nullptr;
     float *d_sin = nullptr;
+    EmLite *d_lite = nullptr;
+    unsigned short *d_lut = nullptr;   // n_em * kLutBins when n_em <= kLutMaxEm
+    bool use_lut = false;
+    unsigned short *d_surv = nullptr;  // K2 survivors, per tile K2_THREADS * n_em entries
+    int *d_tile_count = nullptr;
+    long long surv_cap_tiles = 0;
+    int surv_n_em = 0;
     int4 *d_large = nullptr;
     int4 *d_chunks = nullptr;
     unsigned *d_ctrl = nullptr;
@@ -522,6 +623,10 @@ void free_all(grca_t h) {
     cudaFree(h->d_allhits);
     cudaFree(h->d_em);
     cudaFree(h->d_sin);
+    cudaFree(h->d_lite);
+    cudaFree(h->d_lut);
+    cudaFree(h->d_surv);
+    cudaFree(h->d_tile_count);
     cudaFree(h->d_large);
     cudaFree(h->d_chunks);
     cudaFree(h->d_ctrl);
@@ -555,9 +660,21 @@ KParams params(grca_t h) {
     P.force64 = (h->ci.debug_flags & GRCA_DEBUG_FORCE_FP64) ? 1 : 0;
     P.small_max = h->ci.small_max > 0 ? h->ci.small_max : 512;
     P.n_rays = h->n_rays;
+    P.lite = h->d_lite;
+    P.lut = h->use_lut ? h->d_lut : nullptr;
+    P.surv = h->d_surv;
+    P.tile_count = h->d_tile_count;
     return P;
 }
 }  // namespace
+
+static size_t k2_smem_bytes(int n_em, int n_sin, bool lut) {
+    return sizeof(EmLite) * n_em + sizeof(float) * ((n_sin + 3) & ~3) +
+           (lut ? sizeof(unsigned short) * ((n_em * kLutBins + 7) & ~7) : 0) + sizeof(unsigned short) * K2_THREADS * n_em;
+}
+static size_t k2b_smem_bytes(int n_em, int n_sin) {
+    return sizeof(EmDev) * n_em + sizeof(float) * ((n_sin + 3) & ~3) + sizeof(float) * NF * K2_THREADS;
+}
 
 extern "C" {
 
@@ -599,6 +716,8 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     if (ci->debug_flags & GRCA_DEBUG_COUNT_ALL_HITS) alloc((void **)&h->d_allhits, sizeof(unsigned) * ci->max_rays);
     alloc((void **)&h->d_em, sizeof(EmDev) * kMaxEmitters);
     alloc((void **)&h->d_sin, sizeof(float) * kMaxSin);
+    alloc((void **)&h->d_lite, sizeof(EmLite) * kMaxEmitters);
+    alloc((void **)&h->d_lut, sizeof(unsigned short) * kLutMaxEm * kLutBins);
     alloc((void **)&h->d_large, sizeof(int4) * h->cap_large);
     alloc((void **)&h->d_chunks, sizeof(int4) * h->cap_chunks);
     alloc((void **)&h->d_ctrl, sizeof(unsigned) * 4);
@@ -619,8 +738,8 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     cudaMemsetAsync(h->d_ctrl, 0, sizeof(unsigned) * 4, h->stream);
     cudaMemsetAsync(h->d_stats, 0, sizeof(unsigned long long) * 32, h->stream);
     // occupancy of the persistent kernels (K2 smem depends on emitters: use the max)
-    h->k2_smem = sizeof(EmDev) * kMaxEmitters + sizeof(float) * kMaxSin + sizeof(float) * NF * K2_THREADS;
-    cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k2_smem);
+    cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2_smem_bytes(kMaxEmitters, kMaxSin, false));
+    cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2b_smem_bytes(kMaxEmitters, kMaxSin));
     cudaFuncSetAttribute(k_isect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(EmDev) * kMaxEmitters));
     cudaStreamSynchronize(h->stream);
     if (cudaGetLastError() != cudaSuccess) {
@@ -744,21 +863,83 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
             }
         }
     }
+    // K2 phase-A records (EmLite) and the O(1) channel LUTs
+    std::vector<EmLite> lites(n_emitters);
+    const bool use_lut = n_emitters <= kLutMaxEm;
+    std::vector<unsigned short> lut(use_lut ? (size_t)n_emitters * kLutBins : 0);
+    for (int n = 0; n < n_emitters; ++n) {
+        const grca_emitter &E = em[n];
+        const EmDev &D = recs[n];
+        EmLite &L = lites[n];
+        memset(&L, 0, sizeof(L));
+        for (int c = 0; c < 3; ++c) { L.o[c] = D.o[c]; L.Au[c] = D.A[6 + c]; }
+        double A[3][3], G[3][3];
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) A[r][c] = D.A[3 * r + c];
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) G[r][c] = A[0][r] * A[0][c] + A[1][r] * A[1][c] + A[2][r] * A[2][c];
+        L.G[0] = (float)G[0][0]; L.G[1] = (float)G[1][1]; L.G[2] = (float)G[2][2];
+        L.G[3] = (float)G[0][1]; L.G[4] = (float)G[0][2]; L.G[5] = (float)G[1][2];
+        double dev = 0;   // frame non-orthonormality
+        const double F[3] = {E.forward[0], E.forward[1], E.forward[2]}, Rr[3] = {E.right[0], E.right[1], E.right[2]},
+                     U[3] = {E.up[0], E.up[1], E.up[2]};
+        auto dot = [](const double *a, const double *b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; };
+        dev = std::max({fabs(dot(F, F) - 1), fabs(dot(Rr, Rr) - 1), fabs(dot(U, U) - 1), fabs(dot(F, Rr)),
+                        fabs(dot(F, U)), fabs(dot(Rr, U))});
+        L.ortho = dev <= 1e-6 ? 1 : 0;
+        L.pad0 = kPadS + (L.ortho ? (float)(4.0 * dev + 1e-7) : 0.f);
+        const bool ranged = E.max_range > 0.f && std::isfinite(E.max_range);
+        L.lim = ranged ? (float)((double)E.max_range * (1.0 + 1e-5)) : INFINITY;
+        L.gamma = E.n_channels;
+        L.sin_base = D.sin_base;
+        L.lut_base = n * kLutBins;
+        if (use_lut) {
+            const float *st = sins.data() + D.sin_base;
+            for (int b = 0; b < kLutBins; ++b) {   // under-estimate: first channel >= bin start - 1e-6
+                const float x = (float)(-1.0 + 2.0 * b / kLutBins - 1e-6);
+                int j = 0;
+                while (j < E.n_channels && st[j] < x) ++j;
+                lut[(size_t)n * kLutBins + b] = (unsigned short)j;
+            }
+        }
+    }
     DeviceGuard dg(h->device);
     CK(cudaStreamSynchronize(h->stream));
+    // survivor buffer of K2: K2_THREADS * n_em entries per tile of max_triangles
+    const long long tiles = (std::max<long long>(1, h->ci.max_triangles) + K2_THREADS - 1) / K2_THREADS;
+    if (!h->d_surv || h->surv_n_em < n_emitters) {
+        cudaFree(h->d_surv);
+        cudaFree(h->d_tile_count);
+        h->d_surv = nullptr;
+        h->d_tile_count = nullptr;
+        if (cudaMalloc((void **)&h->d_surv, sizeof(unsigned short) * tiles * K2_THREADS * n_emitters) != cudaSuccess ||
+            cudaMalloc((void **)&h->d_tile_count, sizeof(int) * tiles) != cudaSuccess) {
+            cudaGetLastError();
+            h->surv_n_em = 0;
+            return fail(h, GRCA_E_OOM, "survivor buffer allocation failed");
+        }
+        h->surv_n_em = n_emitters;
+        h->surv_cap_tiles = tiles;
+    }
     CK(cudaMemcpy(h->d_raytab, tab.data(), sizeof(float4) * tab.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->d_em, recs.data(), sizeof(EmDev) * recs.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->d_sin, sins.data(), sizeof(float) * sins.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_lite, lites.data(), sizeof(EmLite) * lites.size(), cudaMemcpyHostToDevice));
+    if (use_lut) CK(cudaMemcpy(h->d_lut, lut.data(), sizeof(unsigned short) * lut.size(), cudaMemcpyHostToDevice));
+    h->use_lut = use_lut;
     h->n_em = n_emitters;
     h->n_sin = (int)sins.size();
     h->n_rays = offs[n_emitters];
     h->offsets = offs;
-    // actual K2 dynamic smem for these emitters; occupancy of the persistent kernels
-    h->k2_smem = sizeof(EmDev) * n_emitters + sizeof(float) * ((h->n_sin + 3) & ~3) + sizeof(float) * NF * K2_THREADS;
-    int b2 = 0, b4 = 0;
+    // dynamic smem for these emitters; occupancy of the persistent kernels
+    h->k2_smem = k2_smem_bytes(n_emitters, h->n_sin, use_lut);
+    h->k2b_smem = k2b_smem_bytes(n_emitters, h->n_sin);
+    int b2 = 0, b2b = 0, b4 = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_cull, K2_THREADS, h->k2_smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2b, k_refine, K2_THREADS, h->k2b_smem));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_isect, K4_THREADS, sizeof(EmDev) * n_emitters));
     h->k2_blocks_per_sm = std::max(1, b2);
+    h->k2b_blocks_per_sm = std::max(1, b2b);
     h->k4_blocks_per_sm = std::max(1, b4);
     return GRCA_OK;
 }
@@ -805,18 +986,25 @@ static grca_status launch_packed(grca_t h) {
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][2], h->stream));
+    if (h->n_tri > 0) {   // K2b
+        const long long tiles = (h->n_tri + K2_THREADS - 1) / K2_THREADS;
+        const long long grid = std::min<long long>(tiles, (long long)h->num_sms * h->k2b_blocks_per_sm);
+        k_refine<<<(unsigned)grid, K2_THREADS, h->k2b_smem, h->stream>>>(P);
+        CK(cudaGetLastError());
+    }
+    if (prof) CK(cudaEventRecord(h->ev[slot][3], h->stream));
     if (h->n_tri > 0) {   // K3
         const long long grid = std::min<long long>((h->cap_large + 255) / 256, (long long)h->num_sms * 4);
         k_bin<<<(unsigned)grid, 256, 0, h->stream>>>(P);
         CK(cudaGetLastError());
     }
-    if (prof) CK(cudaEventRecord(h->ev[slot][3], h->stream));
+    if (prof) CK(cudaEventRecord(h->ev[slot][4], h->stream));
     if (h->n_tri > 0) {   // K4
         const int grid = h->num_sms * h->k4_blocks_per_sm;
         k_isect<<<grid, K4_THREADS, sizeof(EmDev) * h->n_em, h->stream>>>(P);
         CK(cudaGetLastError());
     }
-    if (prof) CK(cudaEventRecord(h->ev[slot][4], h->stream));
+    if (prof) CK(cudaEventRecord(h->ev[slot][5], h->stream));
     return GRCA_OK;
 }
 
@@ -829,7 +1017,7 @@ static grca_status launch_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri
                                                                                  h->n_rays);
         CK(cudaGetLastError());
     }
-    if (h->ev_ok) CK(cudaEventRecord(h->ev[slot][5], h->stream));
+    if (h->ev_ok) CK(cudaEventRecord(h->ev[slot][6], h->stream));
     return GRCA_OK;
 }
 
