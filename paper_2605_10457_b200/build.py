@@ -12,7 +12,7 @@ DEPS = SRC + [os.path.join(PKG, "csrc", "grca_device.cuh"), os.path.join(ROOT, "
 LIB = os.path.join(PKG, "libgrca.so")
 
 NVCC_FLAGS = [
-    "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+    "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-ftz=true",
     "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared", "-I", os.path.join(ROOT, "include"),
 ]
 

@@ -58,7 +58,7 @@ struct KParams {
     int faces, nocull, force64, small_max;
     long long n_rays;
     const EmLite *lite;
-    const unsigned short *lut;   // NULL -> binary search
+    const unsigned char *lut;    // NULL -> binary search
     unsigned short *surv;        // per tile: K2_THREADS * n_em entries (local_tri << 8 | emitter)
     int *tile_count;
 };
@@ -109,8 +109,8 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     EmLite *sL = reinterpret_cast<EmLite *>(smem);
     float *sSin = reinterpret_cast<float *>(sL + P.n_em);
-    unsigned short *sLut = reinterpret_cast<unsigned short *>(sSin + ((P.n_sin + 3) & ~3));
-    unsigned short *sQ = sLut + (P.lut ? ((P.n_em * kLutBins + 7) & ~7) : 0);
+    unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
+    unsigned short *sQ = reinterpret_cast<unsigned short *>(sLut + (P.lut ? ((P.n_em * kLutBins + 15) & ~15) : 0));
     __shared__ int qn;
     __shared__ unsigned long long acc[ST_COUNT];
     {
@@ -205,12 +205,16 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
     unsigned setup64 = 0;
 
+    // warp-per-tile scheduling: a tile holds ~5 % of its 256 x n_em pairs, so one warp per tile
+    // keeps all warps busy (block-per-tile left most warps idle at the final barrier)
     const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long tile = wid; tile < ntiles; tile += nwarps) {
         const int n = P.tile_count[tile];
         const unsigned short *q = P.surv + tile * (long long)K2_THREADS * P.n_em;
-        for (int b0 = 0; b0 < n; b0 += K2_THREADS) {
-            const int idx = b0 + threadIdx.x;
+        for (int b0 = 0; b0 < n; b0 += 32) {
+            const int idx = b0 + lane;
             const bool act = idx < n;
             int e = 0;
             long long t = 0;
@@ -566,7 +570,7 @@ struct grca_ctx {
     EmDev *d_em = nullptr;
     float *d_sin = nullptr;
     EmLite *d_lite = nullptr;
-    unsigned short *d_lut = nullptr;   // n_em * kLutBins when n_em <= kLutMaxEm
+    unsigned char *d_lut = nullptr;    // n_em * kLutBins when n_em <= kLutMaxEm and all gamma <= 255
     bool use_lut = false;
     unsigned short *d_surv = nullptr;  // K2 survivors, per tile K2_THREADS * n_em entries
     int *d_tile_count = nullptr;
@@ -670,7 +674,7 @@ KParams params(grca_t h) {
 
 static size_t k2_smem_bytes(int n_em, int n_sin, bool lut) {
     return sizeof(EmLite) * n_em + sizeof(float) * ((n_sin + 3) & ~3) +
-           (lut ? sizeof(unsigned short) * ((n_em * kLutBins + 7) & ~7) : 0) + sizeof(unsigned short) * K2_THREADS * n_em;
+           (lut ? sizeof(unsigned char) * ((n_em * kLutBins + 15) & ~15) : 0) + sizeof(unsigned short) * K2_THREADS * n_em;
 }
 static size_t k2b_smem_bytes(int n_em, int n_sin) {
     return sizeof(EmDev) * n_em + sizeof(float) * ((n_sin + 3) & ~3) + sizeof(float) * NF * K2_THREADS;
@@ -717,7 +721,7 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     alloc((void **)&h->d_em, sizeof(EmDev) * kMaxEmitters);
     alloc((void **)&h->d_sin, sizeof(float) * kMaxSin);
     alloc((void **)&h->d_lite, sizeof(EmLite) * kMaxEmitters);
-    alloc((void **)&h->d_lut, sizeof(unsigned short) * kLutMaxEm * kLutBins);
+    alloc((void **)&h->d_lut, sizeof(unsigned char) * kLutMaxEm * kLutBins);
     alloc((void **)&h->d_large, sizeof(int4) * h->cap_large);
     alloc((void **)&h->d_chunks, sizeof(int4) * h->cap_chunks);
     alloc((void **)&h->d_ctrl, sizeof(unsigned) * 4);
@@ -828,13 +832,14 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
             const double p = (double)E.channel_elev_rad[j];
             sins.push_back((float)sin(p));
         }
+        sins.push_back(INFINITY);   // sentinel: sinT[gamma] = +inf
         while (plo < E.n_channels && cos((double)E.channel_elev_rad[plo]) < 0.01) ++plo;
         while (phi < E.n_channels - plo && cos((double)E.channel_elev_rad[E.n_channels - 1 - phi]) < 0.01) ++phi;
         D.pole_lo = plo;
         D.pole_hi = phi;
         offs[n + 1] = offs[n] + (long long)E.n_channels * E.rays_per_channel;
     }
-    if ((int)sins.size() > kMaxSin) return fail(h, GRCA_E_INVALID, "sum of n_channels over emitters > 4096");
+    if ((int)sins.size() > kMaxSin) return fail(h, GRCA_E_INVALID, "sum of (n_channels + 1) over emitters > 4096");
     if (offs[n_emitters] > h->ci.max_rays) return fail(h, GRCA_E_CAPACITY, "sum gamma*chi exceeds max_rays");
     // A0: the fp32 ray table, built in fp64 on the host (Eq. ray_dir)
     std::vector<float4> tab((size_t)offs[n_emitters]);
@@ -865,8 +870,10 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     }
     // K2 phase-A records (EmLite) and the O(1) channel LUTs
     std::vector<EmLite> lites(n_emitters);
-    const bool use_lut = n_emitters <= kLutMaxEm;
-    std::vector<unsigned short> lut(use_lut ? (size_t)n_emitters * kLutBins : 0);
+    int max_gamma = 0;
+    for (int n = 0; n < n_emitters; ++n) max_gamma = std::max(max_gamma, (int)em[n].n_channels);
+    const bool use_lut = n_emitters <= kLutMaxEm && max_gamma <= 255;
+    std::vector<unsigned char> lut(use_lut ? (size_t)n_emitters * kLutBins : 0);
     for (int n = 0; n < n_emitters; ++n) {
         const grca_emitter &E = em[n];
         const EmDev &D = recs[n];
@@ -899,7 +906,7 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
                 const float x = (float)(-1.0 + 2.0 * b / kLutBins - 1e-6);
                 int j = 0;
                 while (j < E.n_channels && st[j] < x) ++j;
-                lut[(size_t)n * kLutBins + b] = (unsigned short)j;
+                lut[(size_t)n * kLutBins + b] = (unsigned char)j;
             }
         }
     }
@@ -925,7 +932,7 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     CK(cudaMemcpy(h->d_em, recs.data(), sizeof(EmDev) * recs.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->d_sin, sins.data(), sizeof(float) * sins.size(), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(h->d_lite, lites.data(), sizeof(EmLite) * lites.size(), cudaMemcpyHostToDevice));
-    if (use_lut) CK(cudaMemcpy(h->d_lut, lut.data(), sizeof(unsigned short) * lut.size(), cudaMemcpyHostToDevice));
+    if (use_lut) CK(cudaMemcpy(h->d_lut, lut.data(), sizeof(unsigned char) * lut.size(), cudaMemcpyHostToDevice));
     h->use_lut = use_lut;
     h->n_em = n_emitters;
     h->n_sin = (int)sins.size();

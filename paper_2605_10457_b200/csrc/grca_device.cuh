@@ -50,7 +50,7 @@ struct EmLite {
     float pad0;      // kPadS + frame non-orthonormality allowance
     int gamma, sin_base, lut_base, ortho;
 };
-constexpr int kLutBins = 1024;   // O(1) channel lookup: bins over sin(elevation) in [-1, 1]
+constexpr int kLutBins = 2048;   // O(1) channel lookup: u8 bins over sin(elevation) in [-1, 1]
 
 struct f3 {
     float x, y, z;
@@ -306,18 +306,14 @@ __device__ __forceinline__ long long rect_items(const Rect &R, const EmDev &E) {
     return (long long)(plo + phi) * E.chi + (rows - plo - phi) * R.r_len;
 }
 
-// First channel j with sin_j >= x (LUT start + short linear advance; exact for any LUT that
-// under-estimates), or a binary search when no LUT is staged.
-__device__ __forceinline__ int first_channel_ge(const float *sinT, int gamma, const unsigned short *lut, float x) {
-    int j;
-    if (lut) {
-        int b = (int)((x + 1.f) * (0.5f * kLutBins));
-        b = min(max(b, 0), kLutBins - 1);
-        j = lut[b];
-        while (j < gamma && sinT[j] < x) ++j;
-    } else {
-        j = lower_bound_f(sinT, gamma, x);
-    }
+// First channel j with sin_j >= x: LUT start (an under-estimate) + short linear advance over
+// the sentinel-terminated table (sinT[gamma] = +inf), or a binary search without a LUT.
+__device__ __forceinline__ int first_channel_ge(const float *sinT, int gamma, const unsigned char *lut, float x) {
+    if (!lut) return lower_bound_f(sinT, gamma, x);
+    int b = (int)((x + 1.f) * (0.5f * kLutBins));
+    b = min(max(b, 0), kLutBins - 1);
+    int j = lut[b];
+    while (sinT[j] < x) ++j;
     return j;
 }
 
@@ -327,21 +323,25 @@ __device__ __forceinline__ int first_channel_ge(const float *sinT, int gamma, co
 // emax / r_lb; the elevation excess of an edge interior over its endpoints is <= L^2/8 and a pole
 // inside T forces every |s_k| >= cos L >= 1 - L^2/2.  Returns CULL_KEEP (-> K2b) or the cull.
 __device__ __forceinline__ int quick_cull(const f3 v[3], float emax, const EmLite &L, const float *sinT,
-                                          const unsigned short *lut) {
+                                          const unsigned char *lut) {
     const f3 o = {L.o[0], L.o[1], L.o[2]};
     float s[3], r[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const f3 a = {v[k].x - o.x, v[k].y - o.y, v[k].z - o.z};
         const float w2 = a.x * a.x + a.y * a.y + a.z * a.z;
-        const float x2 = L.ortho ? w2
-                                 : L.G[0] * a.x * a.x + L.G[1] * a.y * a.y + L.G[2] * a.z * a.z +
-                                       2.f * (L.G[3] * a.x * a.y + L.G[4] * a.x * a.z + L.G[5] * a.y * a.z);
         const float xu = L.Au[0] * a.x + L.Au[1] * a.y + L.Au[2] * a.z;
-        s[k] = xu * rsqrtf(x2);
-        r[k] = w2;
+        const float iw = rsqrtf(w2);
+        r[k] = w2 * iw;   // |a_k| (world)
+        if (L.ortho) {
+            s[k] = xu * iw;
+        } else {
+            const float x2 = L.G[0] * a.x * a.x + L.G[1] * a.y * a.y + L.G[2] * a.z * a.z +
+                             2.f * (L.G[3] * a.x * a.y + L.G[4] * a.x * a.z + L.G[5] * a.y * a.z);
+            s[k] = xu * rsqrtf(x2);
+        }
     }
-    const float rmax = sqrtf(fmaxf(r[0], fmaxf(r[1], r[2])));
+    const float rmax = fmaxf(r[0], fmaxf(r[1], r[2]));
     const float rlb = rmax - emax;
     if (rlb > L.lim) return CULL_RANGE;
     if (!(rlb > 2.f * emax)) return CULL_KEEP;   // near (or degenerate / non-finite): exact path
@@ -353,7 +353,7 @@ __device__ __forceinline__ int quick_cull(const f3 v[3], float emax, const EmLit
     const float lo = fminf(s[0], fminf(s[1], s[2])) - pad;
     const float hi = fmaxf(s[0], fmaxf(s[1], s[2])) + pad;
     const int j = first_channel_ge(sinT, L.gamma, lut, lo);
-    if (j >= L.gamma || sinT[j] > hi) return CULL_CHANNEL;
+    if (sinT[j] > hi) return CULL_CHANNEL;   // sinT[gamma] = +inf sentinel
     return CULL_KEEP;
 }
 
