@@ -323,14 +323,14 @@ def main():
 
     # ---- roofline of the dominant kernel (per-kernel CUDA events on the launch stream)
     pk = peaks()
-    names = ["K0_init", "K2_cull", "K2b_refine", "K3_bin", "K4_intersect", "K5_unpack"]
+    names = ["K0_init", "K2_cull", "K2b_refine", "K4s_small", "K3_bin", "K4_large", "K5_unpack"]
     kernel_ms = {n: kms[i] for i, n in enumerate(names)}
     tri_bytes = 48 * scene.n_tri   # algorithmic: 3 float4 vertices per triangle (non-indexed)
     dom = max(names, key=lambda n: kernel_ms[n])
     alg = {
         "K0_init": 8 * n_rays, "K2_cull": tri_bytes, "K2b_refine": 50 * max(1, stats["survivors"]),
-        "K3_bin": 16 * max(1, stats["large_pairs"]),
-        "K4_intersect": 16 * max(1, stats["rtic_tested"] - 0), "K5_unpack": 16 * n_rays,
+        "K4s_small": 16 * max(1, stats["rtic_tested"]), "K3_bin": 16 * max(1, stats["large_pairs"]),
+        "K4_large": 16 * max(1, stats["rtic_tested"]), "K5_unpack": 16 * n_rays,
     }
     ach = alg[dom] / (kernel_ms[dom] / 1e3) / 1e9
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -362,7 +362,7 @@ def main():
             "kernel_ms": kernel_ms, "stats": {k: stats[k] for k in (
                 "pairs", "range_culled", "channel_culled", "azimuth_culled", "survivors", "small_pairs", "large_pairs",
                 "chunks", "fp64_fallbacks", "hits_recorded", "overflow")},
-            "roofline": roofline, "gpu_launches": 6 * args.steps, "clocks": clk,
+            "roofline": roofline, "gpu_launches": 7 * args.steps, "clocks": clk,
             "e2e": e2e, "cpu_baseline": cpu,
             "context": "paper (PAPER.md:1758-1762): GRCA_GPU 10.7 ms/frame on RTX 5090 for PP30 Omega=8 "
                        "(3.9e8 rays/s), 1.98x OptiX 9.1; other hardware, not a target",

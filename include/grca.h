@@ -72,8 +72,8 @@ typedef struct {
                                 handled inline (slower, never dropped) and counted in stats */
     int32_t faces;           /* GRCA_FACES_* */
     uint32_t debug_flags;    /* GRCA_DEBUG_* | GRCA_PROFILE_KERNELS */
-    int32_t small_max;       /* pairs with <= small_max candidates are tested inline by the
-                                culling kernel (0 -> default 512) */
+    int32_t small_max;       /* pairs with <= small_max candidates (<= 1023) take the small-rectangle
+                                path (K4s); larger ones are chunked (K3/K4).  0 -> default 512 */
     int32_t reserved[7];
 } grca_create_info;
 
@@ -106,7 +106,7 @@ typedef struct {
     int64_t overflow_inline; /* large pairs processed inline because the list was full */
     int32_t overflow;        /* 1 if any capacity fallback happened */
     float ms_total;          /* device time of the last cast if GRCA_PROFILE_KERNELS */
-    float ms_k[8];           /* per kernel: K0 init, K2 cull, K2b refine+inline, K3 bin, K4 intersect, K5 unpack */
+    float ms_k[8];           /* per kernel: K0 init, K2 cull, K2b refine, K4s small, K3 bin, K4 large, K5 unpack */
 } grca_stats;
 
 /* Create a handle bound to ci->device.  Allocates all device scratch.
@@ -156,7 +156,8 @@ grca_status grca_get_stats(grca_t h, grca_stats *h_stats);
 
 /* Sum of per-kernel device times over the last n_last casts (GRCA_PROFILE_KERNELS only;
  * n_last in [1, 64]; synchronizes).  ms_per_kernel[8]: [0] K0 init, [1] K2 cull (phase A),
- * [2] K2b refine + inline small work, [3] K3 bin, [4] K4 intersect, [5] K5 unpack, [7] whole cast. */
+ * [2] K2b refine, [3] K4s small-rectangle intersect, [4] K3 bin, [5] K4 large intersect,
+ * [6] K5 unpack, [7] whole cast. */
 grca_status grca_kernel_times(grca_t h, int32_t n_last, float *ms_per_kernel);
 
 /* Per-ray all-hit counts of the last cast (GRCA_DEBUG_COUNT_ALL_HITS only):

@@ -61,6 +61,7 @@ struct KParams {
     const unsigned char *lut;    // NULL -> binary search
     unsigned short *surv;        // per tile: K2_THREADS * n_em entries (local_tri << 8 | emitter)
     int *tile_count;
+    unsigned long long *desc;    // per survivor entry: small-rectangle descriptor (0 = none)
 };
 
 // slot fields (SoA per warp in shared memory) for the inline small-pair expansion
@@ -179,15 +180,23 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
     block_flush(acc, P.stats, cnt);
 }
 
-// --------------------------------------------- K2b refine + inline small work --
-// Dense over the survivors of K2: exact bounds (cull_pair), then small rectangles are expanded
-// with a warp prefix scan and intersected inline; large ones are appended (warp-aggregated,
-// PAPER.md:2383-2393) to the large list for K3/K4.
+// ------------------------------------------------------------- K2b refine --
+// Dense over the survivors of K2 (one warp per tile): exact conservative rectangle (cull_pair).
+// Small rectangles get a 64-bit descriptor at the survivor's own index (no atomics); large ones
+// are appended to the large list (warp-aggregated) for K3/K4.
+__device__ __forceinline__ unsigned long long pack_small(int c_from, int nrows, int r_lo, int r_len) {
+    return (unsigned long long)(unsigned)c_from | ((unsigned long long)nrows << 16) |
+           ((unsigned long long)(unsigned)r_lo << 26) | ((unsigned long long)r_len << 42);
+}
+
+__device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev &E, long long t, int row0, int nrows, int lo,
+                                      int len, unsigned long long *cnt, unsigned &setup64);
+
 __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     EmDev *sE = reinterpret_cast<EmDev *>(smem);
     float *sSin = reinterpret_cast<float *>(sE + P.n_em);
-    float *sSlot = sSin + ((P.n_sin + 3) & ~3);
+    unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
     __shared__ unsigned long long acc[ST_COUNT];
     {
         const int nw = P.n_em * (int)(sizeof(EmDev) / 4);
@@ -195,58 +204,50 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
         int *dst = reinterpret_cast<int *>(sE);
         for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = src[i];
         for (int i = threadIdx.x; i < P.n_sin; i += blockDim.x) sSin[i] = P.sin[i];
+        if (P.lut)
+            for (int i = threadIdx.x; i < P.n_em * kLutBins; i += blockDim.x) sLut[i] = P.lut[i];
         if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    float *slot = sSlot + (threadIdx.x >> 5) * (NF * 32);
     unsigned long long cnt[ST_COUNT];
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
     unsigned setup64 = 0;
-
-    // warp-per-tile scheduling: a tile holds ~5 % of its 256 x n_em pairs, so one warp per tile
-    // keeps all warps busy (block-per-tile left most warps idle at the final barrier)
     const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
     const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
     for (long long tile = wid; tile < ntiles; tile += nwarps) {
         const int n = P.tile_count[tile];
-        const unsigned short *q = P.surv + tile * (long long)K2_THREADS * P.n_em;
+        const long long region = tile * (long long)K2_THREADS * P.n_em;
         for (int b0 = 0; b0 < n; b0 += 32) {
             const int idx = b0 + lane;
             const bool act = idx < n;
-            int e = 0;
+            int e = 0, st = -1;
             long long t = 0;
-            f3 v[3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
-            uint32_t id = 0;
             Rect R;
-            int st = -1;
+            unsigned long long desc = 0ull;
+            bool large = false;
             if (act) {
-                const unsigned ent = q[idx];
+                const unsigned ent = P.surv[region + idx];
                 e = ent & 255;
                 t = tile * K2_THREADS + (ent >> 8);
+                f3 v[3];
                 load_tri(P.tri, t, v);
-                id = tri_id(P.tri, t);
-                st = cull_pair(v, sE[e], sSin + sE[e].sin_base, P.nocull != 0, R);
-            }
-            const EmDev &E = sE[e];
-            long long items = 0;
-            bool small = false, large = false;
-            Setup S;
-            if (st == CULL_KEEP) {
-                items = rect_items(R, E);
-                if (items <= P.small_max && !R.pole_rows) {
-                    if (make_setup(v, em_o(E), P.faces, S, setup64)) small = true;
-                    else st = CULL_DEGENERATE;
-                } else {
-                    large = true;
+                st = cull_pair(v, sE[e], sSin + sE[e].sin_base, P.lut ? sLut + e * kLutBins : nullptr,
+                               P.nocull != 0, R);
+                if (st == CULL_KEEP) {
+                    const long long items = rect_items(R, sE[e]);
+                    if (items <= P.small_max && !R.pole_rows) desc = pack_small(R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len);
+                    else large = true;
+                    cnt[ST_SURV]++;
                 }
+                else if (st == CULL_RANGE) cnt[ST_RANGE]++;
+                else if (st == CULL_CHANNEL) cnt[ST_CHANNEL]++;
+                else if (st == CULL_AZIMUTH) cnt[ST_AZIMUTH]++;
+                else cnt[ST_DEGEN]++;
+                P.desc[region + idx] = desc;
             }
-            if (st == CULL_RANGE) cnt[ST_RANGE]++;
-            else if (st == CULL_CHANNEL) cnt[ST_CHANNEL]++;
-            else if (st == CULL_AZIMUTH) cnt[ST_AZIMUTH]++;
-            else if (st == CULL_DEGENERATE) cnt[ST_DEGEN]++;
             const unsigned lm = __ballot_sync(FULL, large);
             if (lm) {
                 const int leader = __ffs(lm) - 1;
@@ -259,43 +260,96 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
                         P.large[pos] = make_int4((int)t, e | (R.c_from << 8), R.c_to,
                                                  (int)((unsigned)R.r_lo | ((unsigned)R.r_len << 16)));
                         cnt[ST_LARGE]++;
-                    } else {   // capacity fallback: process inline (never dropped)
+                    } else {   // capacity fallback: intersect here (slow, never dropped)
                         cnt[ST_OVF_LARGE]++;
-                        if (R.pole_rows) { R.r_lo = 0; R.r_len = E.chi; R.pole_rows = 0; }
-                        items = (long long)(R.c_to - R.c_from + 1) * R.r_len;
-                        if (make_setup(v, em_o(E), P.faces, S, setup64)) small = true;
+                        if (R.pole_rows) { R.r_lo = 0; R.r_len = sE[e].chi; }
+                        intersect_rect_serial(P, sE[e], t, R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len, cnt,
+                                              setup64);
                     }
                 }
             }
-            if (st == CULL_KEEP) cnt[ST_SURV]++;
-            const int my = small ? (int)items : 0;
-            if (small) {
-                cnt[ST_SMALL]++;
-                cnt[ST_ITEMS_SMALL] += (unsigned long long)my;
-                float *sl = slot + lane;
-                sl[(SF_N0 + 0) * 32] = S.n0.x; sl[(SF_N0 + 1) * 32] = S.n0.y; sl[(SF_N0 + 2) * 32] = S.n0.z;
-                sl[(SF_N1 + 0) * 32] = S.n1.x; sl[(SF_N1 + 1) * 32] = S.n1.y; sl[(SF_N1 + 2) * 32] = S.n1.z;
-                sl[(SF_N2 + 0) * 32] = S.n2.x; sl[(SF_N2 + 1) * 32] = S.n2.y; sl[(SF_N2 + 2) * 32] = S.n2.z;
-                sl[(SF_B + 0) * 32] = S.B0; sl[(SF_B + 1) * 32] = S.B1; sl[(SF_B + 2) * 32] = S.B2;
-                sl[(SF_N + 0) * 32] = S.N.x; sl[(SF_N + 1) * 32] = S.N.y; sl[(SF_N + 2) * 32] = S.N.z;
-                sl[SF_HABS * 32] = S.habs;
-                sl[SF_TN * 32] = S.TN;
-                sl[SF_ID * 32] = __uint_as_float(id);
-                sl[SF_TRI * 32] = __int_as_float((int)t);
-                sl[SF_CFROM * 32] = __int_as_float(R.c_from);
-                sl[SF_RLO * 32] = __int_as_float(R.r_lo);
-                sl[SF_LEN * 32] = __int_as_float(R.r_len);
-                sl[SF_INVLEN * 32] = 1.f / (float)R.r_len;
-                sl[SF_EM * 32] = __int_as_float(e);
+        }
+    }
+    cnt[ST_SETUP64] = setup64;
+    block_flush(acc, P.stats, cnt);
+}
+
+// -------------------------------------------------- K4s small intersection --
+// One warp per tile: lanes compute the certified setup of their small rectangles (one pair per
+// lane, into shared-memory slots), then the warp expands all items of the 32 pairs with an
+// inclusive prefix scan (A5) and tests them (A6) 32 at a time -- no lane idles on a short pair.
+__global__ void __launch_bounds__(K2_THREADS) k_small(const KParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    EmDev *sE = reinterpret_cast<EmDev *>(smem);
+    float *sSlot = reinterpret_cast<float *>(sE + P.n_em);
+    __shared__ unsigned long long acc[ST_COUNT];
+    {
+        const int nw = P.n_em * (int)(sizeof(EmDev) / 4);
+        const int *src = reinterpret_cast<const int *>(P.em);
+        int *dst = reinterpret_cast<int *>(sE);
+        for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = src[i];
+        if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    float *slot = sSlot + (threadIdx.x >> 5) * (NF * 32);
+    unsigned long long cnt[ST_COUNT];
+#pragma unroll
+    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
+    unsigned setup64 = 0;
+    const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
+    const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long tile = wid; tile < ntiles; tile += nwarps) {
+        const int n = P.tile_count[tile];
+        const long long region = tile * (long long)K2_THREADS * P.n_em;
+        for (int b0 = 0; b0 < n; b0 += 32) {
+            const int idx = b0 + lane;
+            int my = 0;
+            if (idx < n) {
+                const unsigned long long desc = P.desc[region + idx];
+                const int nrows = (int)((desc >> 16) & 1023u);
+                if (nrows) {
+                    const unsigned ent = P.surv[region + idx];
+                    const int e = ent & 255;
+                    const long long t = tile * K2_THREADS + (ent >> 8);
+                    const EmDev &E = sE[e];
+                    f3 v[3];
+                    load_tri(P.tri, t, v);
+                    Setup S;
+                    if (make_setup(v, em_o(E), P.faces, S, setup64)) {
+                        const int len = (int)((desc >> 42) & 1023u);
+                        my = nrows * len;
+                        cnt[ST_SMALL]++;
+                        cnt[ST_ITEMS_SMALL] += (unsigned long long)my;
+                        float *sl = slot + lane;
+                        sl[(SF_N0 + 0) * 32] = S.n0.x; sl[(SF_N0 + 1) * 32] = S.n0.y; sl[(SF_N0 + 2) * 32] = S.n0.z;
+                        sl[(SF_N1 + 0) * 32] = S.n1.x; sl[(SF_N1 + 1) * 32] = S.n1.y; sl[(SF_N1 + 2) * 32] = S.n1.z;
+                        sl[(SF_N2 + 0) * 32] = S.n2.x; sl[(SF_N2 + 1) * 32] = S.n2.y; sl[(SF_N2 + 2) * 32] = S.n2.z;
+                        sl[(SF_B + 0) * 32] = S.B0; sl[(SF_B + 1) * 32] = S.B1; sl[(SF_B + 2) * 32] = S.B2;
+                        sl[(SF_N + 0) * 32] = S.N.x; sl[(SF_N + 1) * 32] = S.N.y; sl[(SF_N + 2) * 32] = S.N.z;
+                        sl[SF_HABS * 32] = S.habs;
+                        sl[SF_TN * 32] = S.TN;
+                        sl[SF_ID * 32] = __uint_as_float(tri_id(P.tri, t));
+                        sl[SF_TRI * 32] = __int_as_float((int)t);
+                        sl[SF_CFROM * 32] = __int_as_float((int)(desc & 0xffffu));
+                        sl[SF_RLO * 32] = __int_as_float((int)((desc >> 26) & 0xffffu));
+                        sl[SF_LEN * 32] = __int_as_float(len);
+                        sl[SF_INVLEN * 32] = 1.f / (float)len;
+                        sl[SF_EM * 32] = __int_as_float(e);
+                    } else {
+                        cnt[ST_DEGEN]++;
+                    }
+                }
             }
-            // A5: warp-level prefix-scan work expansion of the small rectangles
+            // A5: warp-level prefix-scan work expansion
             int incl = my;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(FULL, incl, o);
                 if (lane >= o) incl += y;
             }
-            if (small) slot[SF_EXCL * 32 + lane] = __int_as_float(incl - my);
+            if (my) slot[SF_EXCL * 32 + lane] = __int_as_float(incl - my);
             const int total = __shfl_sync(FULL, incl, 31);
             __syncwarp();
             for (int b = 0; b < total; b += 32) {
@@ -377,7 +431,7 @@ __device__ __forceinline__ int group_chunks(const Group &G) {
     return (rows + rpc - 1) / rpc;
 }
 
-__device__ void intersect_rect_serial(const KParams &P, const EmDev &E, long long t, int row0, int nrows, int lo,
+__device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev &E, long long t, int row0, int nrows, int lo,
                                       int len, unsigned long long *cnt, unsigned &setup64) {
     f3 v[3];
     load_tri(P.tri, t, v);
@@ -547,7 +601,7 @@ __global__ void k_unpack(const unsigned long long *__restrict__ hits, float *__r
 using namespace grca;
 
 static constexpr int kRing = 64;
-static constexpr int kEv = 7;   // K0 start, after K0, after K2, after K2b, after K3, after K4, after K5
+static constexpr int kEv = 8;   // start, after K0, K2, K2b, K4s, K3, K4, K5
 
 struct grca_ctx {
     int device = 0;
@@ -556,8 +610,8 @@ struct grca_ctx {
     grca_create_info ci{};
     std::string err;
     int num_sms = 148;
-    int k2_blocks_per_sm = 1, k2b_blocks_per_sm = 1, k4_blocks_per_sm = 1;
-    size_t k2_smem = 0, k2b_smem = 0;
+    int k2_blocks_per_sm = 1, k2b_blocks_per_sm = 1, k4s_blocks_per_sm = 1, k4_blocks_per_sm = 1;
+    size_t k2_smem = 0, k2b_smem = 0, k4s_smem = 0;
     // emitters
     int n_em = 0;
     int n_sin = 0;
@@ -574,6 +628,7 @@ struct grca_ctx {
     bool use_lut = false;
     unsigned short *d_surv = nullptr;  // K2 survivors, per tile K2_THREADS * n_em entries
     int *d_tile_count = nullptr;
+    unsigned long long *d_desc = nullptr;
     long long surv_cap_tiles = 0;
     int surv_n_em = 0;
     int4 *d_large = nullptr;
@@ -631,6 +686,7 @@ void free_all(grca_t h) {
     cudaFree(h->d_lut);
     cudaFree(h->d_surv);
     cudaFree(h->d_tile_count);
+    cudaFree(h->d_desc);
     cudaFree(h->d_large);
     cudaFree(h->d_chunks);
     cudaFree(h->d_ctrl);
@@ -662,12 +718,13 @@ KParams params(grca_t h) {
     P.faces = h->ci.faces;
     P.nocull = (h->ci.debug_flags & GRCA_DEBUG_NO_CULL) ? 1 : 0;
     P.force64 = (h->ci.debug_flags & GRCA_DEBUG_FORCE_FP64) ? 1 : 0;
-    P.small_max = h->ci.small_max > 0 ? h->ci.small_max : 512;
+    P.small_max = std::min(1023, h->ci.small_max > 0 ? h->ci.small_max : 512);
     P.n_rays = h->n_rays;
     P.lite = h->d_lite;
     P.lut = h->use_lut ? h->d_lut : nullptr;
     P.surv = h->d_surv;
     P.tile_count = h->d_tile_count;
+    P.desc = h->d_desc;
     return P;
 }
 }  // namespace
@@ -676,9 +733,10 @@ static size_t k2_smem_bytes(int n_em, int n_sin, bool lut) {
     return sizeof(EmLite) * n_em + sizeof(float) * ((n_sin + 3) & ~3) +
            (lut ? sizeof(unsigned char) * ((n_em * kLutBins + 15) & ~15) : 0) + sizeof(unsigned short) * K2_THREADS * n_em;
 }
-static size_t k2b_smem_bytes(int n_em, int n_sin) {
-    return sizeof(EmDev) * n_em + sizeof(float) * ((n_sin + 3) & ~3) + sizeof(float) * NF * K2_THREADS;
+static size_t k2b_smem_bytes(int n_em, int n_sin, bool lut) {
+    return sizeof(EmDev) * n_em + sizeof(float) * ((n_sin + 3) & ~3) + (lut ? (size_t)n_em * kLutBins : 0);
 }
+static size_t k4s_smem_bytes(int n_em) { return sizeof(EmDev) * n_em + sizeof(float) * NF * K2_THREADS; }
 
 extern "C" {
 
@@ -743,7 +801,8 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     cudaMemsetAsync(h->d_stats, 0, sizeof(unsigned long long) * 32, h->stream);
     // occupancy of the persistent kernels (K2 smem depends on emitters: use the max)
     cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2_smem_bytes(kMaxEmitters, kMaxSin, false));
-    cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2b_smem_bytes(kMaxEmitters, kMaxSin));
+    cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2b_smem_bytes(kMaxEmitters, kMaxSin, false));
+    cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k4s_smem_bytes(kMaxEmitters));
     cudaFuncSetAttribute(k_isect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(EmDev) * kMaxEmitters));
     cudaStreamSynchronize(h->stream);
     if (cudaGetLastError() != cudaSuccess) {
@@ -917,10 +976,13 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     if (!h->d_surv || h->surv_n_em < n_emitters) {
         cudaFree(h->d_surv);
         cudaFree(h->d_tile_count);
+        cudaFree(h->d_desc);
         h->d_surv = nullptr;
         h->d_tile_count = nullptr;
+        h->d_desc = nullptr;
         if (cudaMalloc((void **)&h->d_surv, sizeof(unsigned short) * tiles * K2_THREADS * n_emitters) != cudaSuccess ||
-            cudaMalloc((void **)&h->d_tile_count, sizeof(int) * tiles) != cudaSuccess) {
+            cudaMalloc((void **)&h->d_tile_count, sizeof(int) * tiles) != cudaSuccess ||
+            cudaMalloc((void **)&h->d_desc, sizeof(unsigned long long) * tiles * K2_THREADS * n_emitters) != cudaSuccess) {
             cudaGetLastError();
             h->surv_n_em = 0;
             return fail(h, GRCA_E_OOM, "survivor buffer allocation failed");
@@ -940,10 +1002,13 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     h->offsets = offs;
     // dynamic smem for these emitters; occupancy of the persistent kernels
     h->k2_smem = k2_smem_bytes(n_emitters, h->n_sin, use_lut);
-    h->k2b_smem = k2b_smem_bytes(n_emitters, h->n_sin);
-    int b2 = 0, b2b = 0, b4 = 0;
+    h->k2b_smem = k2b_smem_bytes(n_emitters, h->n_sin, use_lut);
+    h->k4s_smem = k4s_smem_bytes(n_emitters);
+    int b2 = 0, b2b = 0, b4s = 0, b4 = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_cull, K2_THREADS, h->k2_smem));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2b, k_refine, K2_THREADS, h->k2b_smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4s, k_small, K2_THREADS, h->k4s_smem));
+    h->k4s_blocks_per_sm = std::max(1, b4s);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_isect, K4_THREADS, sizeof(EmDev) * n_emitters));
     h->k2_blocks_per_sm = std::max(1, b2);
     h->k2b_blocks_per_sm = std::max(1, b2b);
@@ -993,25 +1058,31 @@ static grca_status launch_packed(grca_t h) {
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][2], h->stream));
-    if (h->n_tri > 0) {   // K2b
-        const long long tiles = (h->n_tri + K2_THREADS - 1) / K2_THREADS;
-        const long long grid = std::min<long long>(tiles, (long long)h->num_sms * h->k2b_blocks_per_sm);
+    const long long tiles = (h->n_tri + K2_THREADS - 1) / K2_THREADS;
+    if (h->n_tri > 0) {   // K2b: warp per tile
+        const long long grid = std::min<long long>((tiles + 7) / 8, (long long)h->num_sms * h->k2b_blocks_per_sm);
         k_refine<<<(unsigned)grid, K2_THREADS, h->k2b_smem, h->stream>>>(P);
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][3], h->stream));
+    if (h->n_tri > 0) {   // K4s: warp per tile
+        const long long grid = std::min<long long>((tiles + 7) / 8, (long long)h->num_sms * h->k4s_blocks_per_sm);
+        k_small<<<(unsigned)grid, K2_THREADS, h->k4s_smem, h->stream>>>(P);
+        CK(cudaGetLastError());
+    }
+    if (prof) CK(cudaEventRecord(h->ev[slot][4], h->stream));
     if (h->n_tri > 0) {   // K3
         const long long grid = std::min<long long>((h->cap_large + 255) / 256, (long long)h->num_sms * 4);
         k_bin<<<(unsigned)grid, 256, 0, h->stream>>>(P);
         CK(cudaGetLastError());
     }
-    if (prof) CK(cudaEventRecord(h->ev[slot][4], h->stream));
+    if (prof) CK(cudaEventRecord(h->ev[slot][5], h->stream));
     if (h->n_tri > 0) {   // K4
         const int grid = h->num_sms * h->k4_blocks_per_sm;
         k_isect<<<grid, K4_THREADS, sizeof(EmDev) * h->n_em, h->stream>>>(P);
         CK(cudaGetLastError());
     }
-    if (prof) CK(cudaEventRecord(h->ev[slot][5], h->stream));
+    if (prof) CK(cudaEventRecord(h->ev[slot][6], h->stream));
     return GRCA_OK;
 }
 
@@ -1024,7 +1095,7 @@ static grca_status launch_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri
                                                                                  h->n_rays);
         CK(cudaGetLastError());
     }
-    if (h->ev_ok) CK(cudaEventRecord(h->ev[slot][6], h->stream));
+    if (h->ev_ok) CK(cudaEventRecord(h->ev[slot][7], h->stream));
     return GRCA_OK;
 }
 

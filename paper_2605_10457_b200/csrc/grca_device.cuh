@@ -154,6 +154,27 @@ __device__ __forceinline__ int upper_bound_f(const float *t, int n, float x) {  
     return lo;
 }
 
+// First channel j with sin_j >= x: LUT start (an under-estimate) + short linear advance over
+// the sentinel-terminated table (sinT[gamma] = +inf), or a binary search without a LUT.
+__device__ __forceinline__ int first_channel_ge(const float *sinT, int gamma, const unsigned char *lut, float x) {
+    if (!lut) return lower_bound_f(sinT, gamma, x);
+    int b = (int)((x + 1.f) * (0.5f * kLutBins));
+    b = min(max(b, 0), kLutBins - 1);
+    int j = lut[b];
+    while (sinT[j] < x) ++j;
+    return j;
+}
+
+// First channel j with sin_j > x (upper bound), same scheme.
+__device__ __forceinline__ int first_channel_gt(const float *sinT, int gamma, const unsigned char *lut, float x) {
+    if (!lut) return upper_bound_f(sinT, gamma, x);
+    int b = (int)((x + 1.f) * (0.5f * kLutBins));
+    b = min(max(b, 0), kLutBins - 1);
+    int j = lut[b];
+    while (sinT[j] <= x) ++j;
+    return j;
+}
+
 // Does direction T lie on the great-circle arc from p to q (normal m = p x q)?  Tolerant
 // (returns true when unsure) -- including an extreme that is not attained is conservative.
 __device__ __forceinline__ bool on_arc(f3 p, f3 q, f3 m, f3 T) {
@@ -164,7 +185,8 @@ __device__ __forceinline__ bool on_arc(f3 p, f3 q, f3 m, f3 T) {
 }
 
 // Conservative (channel, ray) rectangle of triangle v seen from emitter E.
-__device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, bool nocull, Rect &R) {
+__device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, const unsigned char *lut, bool nocull,
+                         Rect &R) {
     const f3 o = {E.o[0], E.o[1], E.o[2]};
     f3 a[3];
 #pragma unroll
@@ -191,10 +213,12 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, boo
         r2[k] = x[k].x * x[k].x + x[k].y * x[k].y + x[k].z * x[k].z;
     }
     if (!(r2[0] > 0.f && r2[1] > 0.f && r2[2] > 0.f)) return CULL_DEGENERATE;   // o is a vertex: Vol = 0
+    float xn[3];   // |x_k|
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         inv[k] = rsqrtf(r2[k]);
         s[k] = x[k].z * inv[k];
+        xn[k] = r2[k] * inv[k];
     }
     float slo = fminf(s[0], fminf(s[1], s[2])), shi = fmaxf(s[0], fmaxf(s[1], s[2]));
     // pole containment: does the spin axis pass through T?  (2-D winding in the x_f x_r plane)
@@ -203,14 +227,14 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, boo
     for (int k = 0; k < 3; ++k) {
         const int k1 = (k + 1) % 3;
         float w = x[k].x * x[k1].y - x[k].y * x[k1].x;
-        float eps = 8.f * kU * sqrtf(r2[k] * r2[k1]);
+        float eps = 9.f * kU * xn[k] * xn[k1];
         pos |= (w > eps);
         neg |= (w < -eps);
         near_axis |= (x[k].x * x[k].x + x[k].y * x[k].y) < kNearAxis2 * r2[k];
     }
     // The axis can only meet T if T's horizontal projection straddles it on both coordinates
     // (this rejects degenerate, e.g. radial vertical, projections whose windings all round to ~0).
-    const float tolb = 16.f * kU * sqrtf(fmaxf(r2[0], fmaxf(r2[1], r2[2])));
+    const float tolb = 17.f * kU * fmaxf(xn[0], fmaxf(xn[1], xn[2]));
     const bool straddle = fminf(x[0].x, fminf(x[1].x, x[2].x)) <= tolb && fmaxf(x[0].x, fmaxf(x[1].x, x[2].x)) >= -tolb &&
                           fminf(x[0].y, fminf(x[1].y, x[2].y)) <= tolb && fmaxf(x[0].y, fmaxf(x[1].y, x[2].y)) >= -tolb;
     const bool pole = straddle && !(pos && neg);
@@ -245,8 +269,8 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, boo
         }
     }
     const float pad = kPadS + pad_e + (longedge ? 1e-5f : 0.f);
-    R.c_from = lower_bound_f(sinTab, E.gamma, slo - pad);
-    R.c_to = upper_bound_f(sinTab, E.gamma, shi + pad) - 1;
+    R.c_from = first_channel_ge(sinTab, E.gamma, lut, slo - pad);
+    R.c_to = min(first_channel_gt(sinTab, E.gamma, lut, shi + pad), E.gamma) - 1;
     if (R.c_from > R.c_to) return CULL_CHANNEL;
     // A4: azimuth arc -> ray index range
     const bool full = pole || near_axis;
@@ -304,17 +328,6 @@ __device__ __forceinline__ long long rect_items(const Rect &R, const EmDev &E) {
     int plo = max(0, min(R.c_to, E.pole_lo - 1) - R.c_from + 1);
     int phi = max(0, R.c_to - max(R.c_from, E.gamma - E.pole_hi) + 1);
     return (long long)(plo + phi) * E.chi + (rows - plo - phi) * R.r_len;
-}
-
-// First channel j with sin_j >= x: LUT start (an under-estimate) + short linear advance over
-// the sentinel-terminated table (sinT[gamma] = +inf), or a binary search without a LUT.
-__device__ __forceinline__ int first_channel_ge(const float *sinT, int gamma, const unsigned char *lut, float x) {
-    if (!lut) return lower_bound_f(sinT, gamma, x);
-    int b = (int)((x + 1.f) * (0.5f * kLutBins));
-    b = min(max(b, 0), kLutBins - 1);
-    int j = lut[b];
-    while (sinT[j] < x) ++j;
-    return j;
 }
 
 // K2 phase A: cheap conservative elevation pre-test of one (triangle, emitter) pair.
