@@ -401,35 +401,39 @@ __device__ __forceinline__ bool make_setup(const f3 v[3], f3 o, int faces, Setup
         n[k] = crossf(aP, e);
         B[k] = __fmul_rn(__fmul_rn(16.f * kU, sqrtf(dotf(aP, aP))), sqrtf(dotf(e, e)));
     }
-    f3 e1 = subf(v[1], v[0]), e2 = subf(v[2], v[0]);
-    f3 N = crossf(e1, e2);
-    f3 a0 = subf(v[0], o);
-    float h = dotf(N, a0);
-    float nE = __fmul_rn(sqrtf(dotf(e1, e1)), sqrtf(dotf(e2, e2)));
-    float nN = sqrtf(dotf(N, N));
-    float na0 = sqrtf(dotf(a0, a0));
-    float Bh = __fmul_rn(__fadd_rn(__fmul_rn(8.f * kU, nE), __fmul_rn(6.f * kU, nN)), na0);
-    float s;
-    bool force64 = false;
-    if (!(fabsf(h) > 2.f * Bh)) {
-        double h64 = exact_vol(v, o);
-        ++setup64;
-        if (!(h64 > 0.0 || h64 < 0.0)) return false;
-        s = h64 > 0.0 ? 1.f : -1.f;
-        force64 = true;
-    } else {
-        s = h > 0.f ? 1.f : -1.f;
-    }
+    // plane (N, h) in fp64 from the exact fp64 edges, rounded: t = h / d.N is then certified to
+    // 4.5e-6 for all but |cos(view)| < ~0.05.
+    const d3 V0 = tod(v[0]);
+    const d3 E1 = subd(tod(v[1]), V0), E2 = subd(tod(v[2]), V0);
+    const d3 N64 = crossd(E1, E2);
+    const d3 A0 = subd(V0, tod(o));
+    const double h64 = dotd(N64, A0);
+    if (!(h64 > 0.0 || h64 < 0.0)) return false;   // origin in the plane / degenerate: no hits
+    const float s = h64 > 0.0 ? 1.f : -1.f;
     if ((faces == 1 && s < 0.f) || (faces == 2 && s > 0.f)) return false;
+    const f3 N = {(float)N64.x, (float)N64.y, (float)N64.z};
+    const float habs = (float)fabs(h64);
+    // generous bound of the fp64 error of h64 (2^-48 relative to its L1 magnitudes)
+    // (explicit _rn intrinsics: thresholds must be bit-identical in every kernel that inlines this)
+    const float sE1 = __fadd_rn(__fadd_rn(fabsf((float)E1.x), fabsf((float)E1.y)), fabsf((float)E1.z));
+    const float sE2 = __fadd_rn(__fadd_rn(fabsf((float)E2.x), fabsf((float)E2.y)), fabsf((float)E2.z));
+    const float sN = __fadd_rn(__fadd_rn(fabsf(N.x), fabsf(N.y)), fabsf(N.z));
+    const float l1 = __fadd_rn(__fmul_rn(sE1, sE2), sN);
+    const float la = __fadd_rn(__fadd_rn(fabsf((float)A0.x), fabsf((float)A0.y)), fabsf((float)A0.z));
+    const float err64 = __fmul_rn(__fmul_rn(3.64e-15f, l1), la);
+    const bool sign_ok = habs > 2.f * err64;
     S.n0 = scalef(n[0], s * sg[0]);
     S.n1 = scalef(n[1], s * sg[1]);
     S.n2 = scalef(n[2], s * sg[2]);
-    S.B0 = B[0]; S.B1 = B[1]; S.B2 = B[2];
+    S.B0 = sign_ok ? B[0] : CUDART_INF_F;   // unsure side of the plane: every candidate -> fp64
+    S.B1 = sign_ok ? B[1] : CUDART_INF_F;
+    S.B2 = sign_ok ? B[2] : CUDART_INF_F;
     S.N = scalef(N, s);
-    S.habs = fabsf(h);
-    const float rh = __fdiv_rn(Bh, fabsf(h));
-    const float Bn = __fadd_rn(__fmul_rn(8.f * kU, nE), __fmul_rn(4.f * kU, nN));
-    S.TN = (force64 || !(rh < 2e-6f)) ? CUDART_INF_F : __fdiv_rn(Bn, __fsub_rn(kTRel - 2.f * kU, rh));
+    S.habs = habs;
+    const float rh = __fadd_rn(1.01f * kU, __fmul_rn(__fdiv_rn(err64, habs), 1.01f));
+    const float Bn = __fmul_rn(3.1f * kU, sqrtf(dotf(N, N)));
+    (void)setup64;
+    S.TN = (!sign_ok || !(rh < 2e-6f)) ? CUDART_INF_F : __fmul_rn(__fdiv_rn(Bn, __fsub_rn(kTRel - 3.f * kU, rh)), 1.0001f);
     return true;
 }
 
