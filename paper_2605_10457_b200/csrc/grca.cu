@@ -62,6 +62,8 @@ struct KParams {
     unsigned short *surv;        // per tile: K2_THREADS * n_em entries (local_tri << 8 | emitter)
     int *tile_count;
     unsigned long long *desc;    // per survivor entry: small-rectangle descriptor (0 = none)
+    unsigned *rounds;            // work units of 32 survivor entries: tile << 6 | round
+    unsigned *n_rounds;
 };
 
 // slot fields (SoA per warp in shared memory) for the inline small-pair expansion
@@ -99,7 +101,7 @@ __global__ void k_init(unsigned long long *hits, unsigned *allhits, long long n,
     if (allhits)
         for (long long i = tid; i < n; i += stride) allhits[i] = 0u;
     if (tid < ST_COUNT) stats[tid] = 0ull;
-    if (tid < 4) ctrl[tid] = 0u;
+    if (tid < 8) ctrl[tid] = 0u;
 }
 
 // ------------------------------------------------------- K2 cull (phase A) --
@@ -171,7 +173,14 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
         const int n = qn;
         unsigned short *dst = P.surv + tile * (long long)K2_THREADS * P.n_em;
         for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = sQ[i];
-        if (threadIdx.x == 0) P.tile_count[tile] = n;
+        if (threadIdx.x == 0) {
+            P.tile_count[tile] = n;
+            const int r = (n + 31) >> 5;   // work units of 32 survivors for K2b / K4s
+            if (r) {
+                const unsigned base = atomicAdd(P.n_rounds, (unsigned)r);
+                for (int k = 0; k < r; ++k) P.rounds[base + k] = ((unsigned)tile << 6) | (unsigned)k;
+            }
+        }
         __syncthreads();
     }
     cnt[ST_PAIRS] = c_pairs;
@@ -214,14 +223,17 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
     unsigned setup64 = 0;
-    const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
-    const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long tile = wid; tile < ntiles; tile += nwarps) {
+    // work = rounds of 32 survivor entries, interleaved over all warps (balanced: no tile tails)
+    const unsigned nr = *P.n_rounds;
+    const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned w = wid; w < nr; w += nwarps) {
+        const unsigned ru = P.rounds[w];
+        const long long tile = ru >> 6;
         const int n = P.tile_count[tile];
         const long long region = tile * (long long)K2_THREADS * P.n_em;
-        for (int b0 = 0; b0 < n; b0 += 32) {
-            const int idx = b0 + lane;
+        {
+            const int idx = (int)(ru & 63u) * 32 + lane;
             const bool act = idx < n;
             int e = 0, st = -1;
             long long t = 0;
@@ -297,14 +309,16 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const KParams P) {
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
     unsigned setup64 = 0;
-    const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
-    const long long wid = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    for (long long tile = wid; tile < ntiles; tile += nwarps) {
+    const unsigned nr = *P.n_rounds;
+    const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned w = wid; w < nr; w += nwarps) {
+        const unsigned ru = P.rounds[w];
+        const long long tile = ru >> 6;
         const int n = P.tile_count[tile];
         const long long region = tile * (long long)K2_THREADS * P.n_em;
-        for (int b0 = 0; b0 < n; b0 += 32) {
-            const int idx = b0 + lane;
+        {
+            const int idx = (int)(ru & 63u) * 32 + lane;
             int my = 0;
             if (idx < n) {
                 const unsigned long long desc = P.desc[region + idx];
@@ -629,6 +643,7 @@ struct grca_ctx {
     unsigned short *d_surv = nullptr;  // K2 survivors, per tile K2_THREADS * n_em entries
     int *d_tile_count = nullptr;
     unsigned long long *d_desc = nullptr;
+    unsigned *d_rounds = nullptr;
     long long surv_cap_tiles = 0;
     int surv_n_em = 0;
     int4 *d_large = nullptr;
@@ -687,6 +702,7 @@ void free_all(grca_t h) {
     cudaFree(h->d_surv);
     cudaFree(h->d_tile_count);
     cudaFree(h->d_desc);
+    cudaFree(h->d_rounds);
     cudaFree(h->d_large);
     cudaFree(h->d_chunks);
     cudaFree(h->d_ctrl);
@@ -713,6 +729,8 @@ KParams params(grca_t h) {
     P.cap_large = h->cap_large;
     P.chunks = h->d_chunks;
     P.n_chunks = h->d_ctrl + 1;
+    P.n_rounds = h->d_ctrl + 2;
+    P.rounds = h->d_rounds;
     P.cap_chunks = h->cap_chunks;
     P.stats = h->d_stats;
     P.faces = h->ci.faces;
@@ -782,7 +800,7 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     alloc((void **)&h->d_lut, sizeof(unsigned char) * kLutMaxEm * kLutBins);
     alloc((void **)&h->d_large, sizeof(int4) * h->cap_large);
     alloc((void **)&h->d_chunks, sizeof(int4) * h->cap_chunks);
-    alloc((void **)&h->d_ctrl, sizeof(unsigned) * 4);
+    alloc((void **)&h->d_ctrl, sizeof(unsigned) * 8);
     alloc((void **)&h->d_stats, sizeof(unsigned long long) * 32);
     if (!ok) {
         g_create_err = "device allocation failed";
@@ -797,7 +815,7 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
             for (int k = 0; k < kEv; ++k)
                 if (cudaEventCreate(&h->ev[r][k]) != cudaSuccess) h->ev_ok = false;
     }
-    cudaMemsetAsync(h->d_ctrl, 0, sizeof(unsigned) * 4, h->stream);
+    cudaMemsetAsync(h->d_ctrl, 0, sizeof(unsigned) * 8, h->stream);
     cudaMemsetAsync(h->d_stats, 0, sizeof(unsigned long long) * 32, h->stream);
     // occupancy of the persistent kernels (K2 smem depends on emitters: use the max)
     cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2_smem_bytes(kMaxEmitters, kMaxSin, false));
@@ -977,12 +995,15 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
         cudaFree(h->d_surv);
         cudaFree(h->d_tile_count);
         cudaFree(h->d_desc);
+        cudaFree(h->d_rounds);
+        h->d_rounds = nullptr;
         h->d_surv = nullptr;
         h->d_tile_count = nullptr;
         h->d_desc = nullptr;
         if (cudaMalloc((void **)&h->d_surv, sizeof(unsigned short) * tiles * K2_THREADS * n_emitters) != cudaSuccess ||
             cudaMalloc((void **)&h->d_tile_count, sizeof(int) * tiles) != cudaSuccess ||
-            cudaMalloc((void **)&h->d_desc, sizeof(unsigned long long) * tiles * K2_THREADS * n_emitters) != cudaSuccess) {
+            cudaMalloc((void **)&h->d_desc, sizeof(unsigned long long) * tiles * K2_THREADS * n_emitters) != cudaSuccess ||
+            cudaMalloc((void **)&h->d_rounds, sizeof(unsigned) * tiles * ((K2_THREADS * n_emitters + 31) / 32)) != cudaSuccess) {
             cudaGetLastError();
             h->surv_n_em = 0;
             return fail(h, GRCA_E_OOM, "survivor buffer allocation failed");
@@ -1060,13 +1081,13 @@ static grca_status launch_packed(grca_t h) {
     if (prof) CK(cudaEventRecord(h->ev[slot][2], h->stream));
     const long long tiles = (h->n_tri + K2_THREADS - 1) / K2_THREADS;
     if (h->n_tri > 0) {   // K2b: warp per tile
-        const long long grid = std::min<long long>((tiles + 7) / 8, (long long)h->num_sms * h->k2b_blocks_per_sm);
+        const long long grid = (long long)h->num_sms * h->k2b_blocks_per_sm;
         k_refine<<<(unsigned)grid, K2_THREADS, h->k2b_smem, h->stream>>>(P);
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][3], h->stream));
     if (h->n_tri > 0) {   // K4s: warp per tile
-        const long long grid = std::min<long long>((tiles + 7) / 8, (long long)h->num_sms * h->k4s_blocks_per_sm);
+        const long long grid = (long long)h->num_sms * h->k4s_blocks_per_sm;
         k_small<<<(unsigned)grid, K2_THREADS, h->k4s_smem, h->stream>>>(P);
         CK(cudaGetLastError());
     }
