@@ -189,6 +189,101 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
     block_flush(acc, P.stats, cnt);
 }
 
+// ---------------------------------------- K2 cull, fixed emitter count (hot) --
+// Same test as k_cull, specialised for NE <= kFixedEm emitters: the emitter loop is unrolled and the
+// EmLite records are a kernel parameter (constant bank), so their fields are direct FFMA/FADD
+// operands; survivors are compacted once per tile with a block-wide scan of per-thread emitter
+// masks (no per-emitter ballots or shared atomics).
+constexpr int kFixedEm = 8;
+struct EmLitePack {
+    EmLite e[kFixedEm];
+};
+
+template <int NE>
+__global__ void __launch_bounds__(K2_THREADS) k_cull_fixed(const KParams P, const EmLitePack EL) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *sSin = reinterpret_cast<float *>(smem);
+    unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
+    __shared__ int wsum[K2_THREADS / 32];
+    __shared__ unsigned long long acc[ST_COUNT];
+    for (int i = threadIdx.x; i < P.n_sin; i += blockDim.x) sSin[i] = P.sin[i];
+    if (P.lut)
+        for (int i = threadIdx.x; i < NE * kLutBins; i += blockDim.x) sLut[i] = P.lut[i];
+    if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned c_pairs = 0, c_range = 0, c_chan = 0;
+    const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long t = tile * K2_THREADS + threadIdx.x;
+        unsigned keep = 0u, rng = 0u;
+        if (t < P.n_tri) {
+            f3 v[3];
+            load_tri(P.tri, t, v);   // A1 (fused K1)
+            const float l0 = (v[1].x - v[0].x) * (v[1].x - v[0].x) + (v[1].y - v[0].y) * (v[1].y - v[0].y) +
+                             (v[1].z - v[0].z) * (v[1].z - v[0].z);
+            const float l1 = (v[2].x - v[1].x) * (v[2].x - v[1].x) + (v[2].y - v[1].y) * (v[2].y - v[1].y) +
+                             (v[2].z - v[1].z) * (v[2].z - v[1].z);
+            const float l2 = (v[0].x - v[2].x) * (v[0].x - v[2].x) + (v[0].y - v[2].y) * (v[0].y - v[2].y) +
+                             (v[0].z - v[2].z) * (v[0].z - v[2].z);
+            const float m2 = fmaxf(l0, fmaxf(l1, l2));
+            const float emax = m2 * rsqrtf(m2) * (1.f + 1e-5f);   // triangle diameter (0 if degenerate)
+            c_pairs += NE;
+            unsigned chan = 0u;
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                const int st = P.nocull ? CULL_KEEP
+                                        : quick_cull(v, emax, EL.e[e], sSin + EL.e[e].sin_base,
+                                                     P.lut ? sLut + e * kLutBins : nullptr);
+                keep |= (st == CULL_KEEP ? 1u : 0u) << e;
+                rng |= (st == CULL_RANGE ? 1u : 0u) << e;
+                chan += (st == CULL_CHANNEL);
+            }
+            c_chan += chan;
+        }
+        const int cntk = __popc(keep);
+        c_range += __popc(rng);
+        // block-wide exclusive scan of the per-thread survivor counts
+        int incl = cntk;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[wib] = incl;
+        __syncthreads();
+        int wbase = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < K2_THREADS / 32; ++w) {
+            const int x = wsum[w];
+            wbase += (w < wib) ? x : 0;
+            total += x;
+        }
+        unsigned short *dst = P.surv + tile * (long long)K2_THREADS * P.n_em + wbase + incl - cntk;
+        while (keep) {
+            const int e = __ffs(keep) - 1;
+            keep &= keep - 1u;
+            *dst++ = (unsigned short)((threadIdx.x << 8) | e);
+        }
+        if (threadIdx.x == 0) {
+            P.tile_count[tile] = total;
+            const int r = (total + 31) >> 5;   // work units of 32 survivors for K2b / K4s
+            if (r) {
+                const unsigned base = atomicAdd(P.n_rounds, (unsigned)r);
+                for (int k = 0; k < r; ++k) P.rounds[base + k] = ((unsigned)tile << 6) | (unsigned)k;
+            }
+        }
+        __syncthreads();   // wsum reuse
+    }
+    unsigned long long cnt[ST_COUNT];
+#pragma unroll
+    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
+    cnt[ST_PAIRS] = c_pairs;
+    cnt[ST_RANGE] = c_range;
+    cnt[ST_CHANNEL] = c_chan;
+    block_flush(acc, P.stats, cnt);
+}
+
 // ------------------------------------------------------------- K2b refine --
 // Dense over the survivors of K2 (one warp per tile): exact conservative rectangle (cull_pair).
 // Small rectangles get a 64-bit descriptor at the survivor's own index (no atomics); large ones
@@ -646,6 +741,8 @@ struct grca_ctx {
     unsigned *d_rounds = nullptr;
     long long surv_cap_tiles = 0;
     int surv_n_em = 0;
+    EmLitePack lite_pack{};
+    size_t k2f_smem = 0;
     int4 *d_large = nullptr;
     int4 *d_chunks = nullptr;
     unsigned *d_ctrl = nullptr;
@@ -746,6 +843,19 @@ KParams params(grca_t h) {
     return P;
 }
 }  // namespace
+
+static const void *k2_fixed_fn(int ne) {
+    switch (ne) {
+        case 1: return (const void *)k_cull_fixed<1>;
+        case 2: return (const void *)k_cull_fixed<2>;
+        case 3: return (const void *)k_cull_fixed<3>;
+        case 4: return (const void *)k_cull_fixed<4>;
+        case 5: return (const void *)k_cull_fixed<5>;
+        case 6: return (const void *)k_cull_fixed<6>;
+        case 7: return (const void *)k_cull_fixed<7>;
+        default: return (const void *)k_cull_fixed<8>;
+    }
+}
 
 static size_t k2_smem_bytes(int n_em, int n_sin, bool lut) {
     return sizeof(EmLite) * n_em + sizeof(float) * ((n_sin + 3) & ~3) +
@@ -1023,10 +1133,18 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     h->offsets = offs;
     // dynamic smem for these emitters; occupancy of the persistent kernels
     h->k2_smem = k2_smem_bytes(n_emitters, h->n_sin, use_lut);
+    memset(&h->lite_pack, 0, sizeof(h->lite_pack));
+    for (int n = 0; n < n_emitters && n < kFixedEm; ++n) h->lite_pack.e[n] = lites[n];
+    h->k2f_smem = sizeof(float) * ((h->n_sin + 3) & ~3) + (use_lut ? (size_t)n_emitters * kLutBins : 0);
     h->k2b_smem = k2b_smem_bytes(n_emitters, h->n_sin, use_lut);
     h->k4s_smem = k4s_smem_bytes(n_emitters);
     int b2 = 0, b2b = 0, b4s = 0, b4 = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_cull, K2_THREADS, h->k2_smem));
+    if (n_emitters <= kFixedEm) {
+        const void *fn = k2_fixed_fn(n_emitters);
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, fn, K2_THREADS, h->k2f_smem));
+    } else {
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_cull, K2_THREADS, h->k2_smem));
+    }
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2b, k_refine, K2_THREADS, h->k2b_smem));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4s, k_small, K2_THREADS, h->k4s_smem));
     h->k4s_blocks_per_sm = std::max(1, b4s);
@@ -1075,7 +1193,13 @@ static grca_status launch_packed(grca_t h) {
     if (h->n_tri > 0) {   // K2
         const long long tiles = (h->n_tri + K2_THREADS - 1) / K2_THREADS;
         const long long grid = std::min<long long>(tiles, (long long)h->num_sms * h->k2_blocks_per_sm);
-        k_cull<<<(unsigned)grid, K2_THREADS, h->k2_smem, h->stream>>>(P);
+        if (h->n_em <= kFixedEm) {
+            void *args[] = {(void *)&P, (void *)&h->lite_pack};
+            CK(cudaLaunchKernel(k2_fixed_fn(h->n_em), dim3((unsigned)grid), dim3(K2_THREADS), args, h->k2f_smem,
+                                h->stream));
+        } else {
+            k_cull<<<(unsigned)grid, K2_THREADS, h->k2_smem, h->stream>>>(P);
+        }
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][2], h->stream));

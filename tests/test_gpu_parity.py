@@ -336,3 +336,12 @@ def test_c4_full_size_sampled():
     rep, _ = check(w["emitters"], w["tris"], dist, tri, rays=rays)
     assert st["pairs"] == len(w["tris"]) * 8
     assert rep["oracle_hits"] > 20
+
+
+@pytest.mark.parametrize("n_em", [9, 17])
+def test_many_emitters_generic_paths(n_em):
+    """More emitters than the unrolled K2 handles (9: generic kernel + LUT; 17: no LUT, binary search)."""
+    ems, tris = sg.random_scene(40 + n_em, n_tris=400, n_emitters=n_em, gamma=10, chi=60, extent=7.0)
+    dist, tri, st, _ = run(ems, tris)
+    check(ems, tris, dist, tri)
+    assert st["pairs"] == len(tris) * n_em
