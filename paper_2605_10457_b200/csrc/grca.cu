@@ -1019,14 +1019,15 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
             const double p = (double)E.channel_elev_rad[j];
             sins.push_back((float)sin(p));
         }
-        sins.push_back(INFINITY);   // sentinel: sinT[gamma] = +inf
+        sins.push_back(INFINITY);   // sentinels: sinT[gamma] = sinT[gamma + 1] = +inf
+        sins.push_back(INFINITY);
         while (plo < E.n_channels && cos((double)E.channel_elev_rad[plo]) < 0.01) ++plo;
         while (phi < E.n_channels - plo && cos((double)E.channel_elev_rad[E.n_channels - 1 - phi]) < 0.01) ++phi;
         D.pole_lo = plo;
         D.pole_hi = phi;
         offs[n + 1] = offs[n] + (long long)E.n_channels * E.rays_per_channel;
     }
-    if ((int)sins.size() > kMaxSin) return fail(h, GRCA_E_INVALID, "sum of (n_channels + 1) over emitters > 4096");
+    if ((int)sins.size() > kMaxSin) return fail(h, GRCA_E_INVALID, "sum of (n_channels + 2) over emitters > 4096");
     if (offs[n_emitters] > h->ci.max_rays) return fail(h, GRCA_E_CAPACITY, "sum gamma*chi exceeds max_rays");
     // A0: the fp32 ray table, built in fp64 on the host (Eq. ray_dir)
     std::vector<float4> tab((size_t)offs[n_emitters]);

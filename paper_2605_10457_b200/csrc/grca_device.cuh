@@ -355,19 +355,34 @@ __device__ __forceinline__ int quick_cull(const f3 v[3], float emax, const EmLit
         }
     }
     const float rmax = fmaxf(r[0], fmaxf(r[1], r[2]));
+    // branch-free: every pair evaluates the whole test (early returns only cost reconvergence)
     const float rlb = rmax - emax;
-    if (rlb > L.lim) return CULL_RANGE;
-    if (!(rlb > 2.f * emax)) return CULL_KEEP;   // near (or degenerate / non-finite): exact path
-    const float q = __fdividef(emax, rlb);
+    const bool range = rlb > L.lim;
+    const bool near = !(rlb > 2.f * emax);   // near (or degenerate / non-finite): exact path in K2b
+    const float q = emax * __frcp_rn(fmaxf(rlb, 1e-30f));
     const float q2 = q * q;
     const float smax = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));
-    if (smax >= 1.f - 0.51f * q2 - 1e-5f) return CULL_KEEP;   // a pole may lie inside T
+    const bool pole = smax >= 1.f - 0.51f * q2 - 1e-5f;   // a pole may lie inside T
     const float pad = L.pad0 + 0.13f * q2;
     const float lo = fminf(s[0], fminf(s[1], s[2])) - pad;
     const float hi = fmaxf(s[0], fmaxf(s[1], s[2])) + pad;
-    const int j = first_channel_ge(sinT, L.gamma, lut, lo);
-    if (sinT[j] > hi) return CULL_CHANNEL;   // sinT[gamma] = +inf sentinel
-    return CULL_KEEP;
+    float vj;   // sin of the first channel >= lo
+    if (lut) {
+        int b = (int)((lo + 1.f) * (0.5f * kLutBins));
+        b = min(max(b, 0), kLutBins - 1);
+        int j = lut[b];
+        const float v0 = sinT[j], v1 = sinT[j + 1];   // two +inf sentinels: j + 1 <= gamma + 1
+        vj = v0 >= lo ? v0 : v1;
+        if (v1 < lo) {   // rare: > 2 channels in one bin (near the poles)
+            j += 2;
+            while (sinT[j] < lo) ++j;
+            vj = sinT[j];
+        }
+    } else {
+        vj = sinT[lower_bound_f(sinT, L.gamma, lo)];
+    }
+    const bool keep = near || pole || vj <= hi;
+    return range ? CULL_RANGE : (keep ? CULL_KEEP : CULL_CHANNEL);
 }
 
 // --------------------------------------------------- A6 setup + certified test --
