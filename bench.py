@@ -29,7 +29,6 @@ sys.path.insert(0, ROOT)
 
 import scenegen as sg  # noqa: E402
 
-BLOCK = 4096   # triangle block for block-interleaved sharding
 N_FRAMES = 4   # distinct resident frames cycled through (each > L2)
 
 
@@ -88,23 +87,25 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- scene --
-def shard_mask(n: int, rank: int, world: int) -> np.ndarray:
-    """Block-interleaved triangle ownership: block b of BLOCK triangles -> rank b mod P."""
-    return ((np.arange(n) // BLOCK) % world) == rank
-
-
 class Scene:
     """Resident C-config frames on the GPU (harness: input generation, not the hot path)."""
 
-    def __init__(self, config: str, rank: int, world: int, device, deformation: str = "ND"):
+    def __init__(self, config: str, rank: int, world: int, device, deformation: str = "ND", shard: str = "triangles"):
         import torch
+
+        from paper_2605_10457_b200 import dist as D
 
         w = sg.workload(config, frame=0, deformation=deformation)
         self.w = w
         self.emitters = w["emitters"]
         n_static, n_dyn = w["n_static"], w["n_dynamic"]
         self.n_tri_global = n_static + n_dyn
-        own = shard_mask(self.n_tri_global, rank, world)
+        own = np.zeros(self.n_tri_global, dtype=bool)
+        if shard == "triangles":
+            own[D.shard_triangles(self.n_tri_global, rank, world)] = True
+        else:   # sensor sharding: every rank holds all triangles, casts its own emitters
+            own[:] = True
+            self.emitters = [self.emitters[n] for n in D.shard_emitters(len(self.emitters), rank, world)]
         self.own_static = np.nonzero(own[:n_static])[0]
         self.own_dyn = np.nonzero(own[n_static:])[0]
         self.ids = torch.as_tensor(np.concatenate([self.own_static, n_static + self.own_dyn]).astype(np.int32),
@@ -173,6 +174,71 @@ def time_oracle(emitters, tris, target_s: float = 12.0, max_rays: int = 4096):
             "tests_per_s": n2 * len(tris) / dt, "frame_ms_extrapolated": 1e3 * dt * sg.n_rays_total(emitters) / n2}
 
 
+KERNELS = ["K0_init", "K2_cull", "K2b_refine", "K4s_small", "K3_bin", "K4_large", "K5_unpack"]
+NCU_NAME = {"K2_cull": "k_cull_fixed", "K2b_refine": "k_refine", "K4s_small": "k_small", "K4_large": "k_isect",
+            "K0_init": "k_init", "K3_bin": "k_bin", "K5_unpack": "k_unpack"}
+# algorithmic work per unit: fp32 ALU operations or HBM bytes
+ALU_PER_PAIR_K2 = 50        # elevation pre-test of one (triangle, emitter) pair
+ALU_PER_SURV_K2B = 400      # exact bounds (elevation, pole, azimuth arc, ray range) of one survivor
+ALU_PER_ITEM = 25           # certified edge-function test of one (triangle, ray) candidate
+ALU_PER_SETUP = 150         # per-pair certified setup (3 edge normals + bounds, fp64 plane)
+
+
+def ncu_traffic():
+    """DRAM bytes per launch from the latest committed `ncu --set full` capture (profiles/)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
+        return {}, None
+    d = json.load(open(files[-1]))
+    out = {}
+    for k, v in d.get("per_kernel", {}).items():
+        for ours, nm in NCU_NAME.items():
+            if nm in k:
+                out[ours] = v["dram_bytes"]
+    return out, os.path.basename(files[-1])
+
+
+def kernel_rooflines(kernel_ms, st, n_rays, n_tri, n_em, clk, device):
+    import torch
+
+    pk = peaks()
+    n_sm = torch.cuda.get_device_properties(device).multi_processor_count
+    mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
+    alu_peak = n_sm * 128 * mhz * 1e6 / 1e12          # fp32 lane-ops/s (4 SMSP x 32 lanes per SM)
+    traffic, src = ncu_traffic()
+    small_items = st["rtic_small"]
+    large_items = st["rtic_tested"] - small_items
+    work = {
+        "K0_init": ("hbm", 8 * n_rays),
+        "K2_cull": ("alu", ALU_PER_PAIR_K2 * st["pairs"]),
+        "K2b_refine": ("alu", ALU_PER_SURV_K2B * st["prefilter_survivors"]),
+        "K4s_small": ("alu", ALU_PER_ITEM * small_items + ALU_PER_SETUP * st["small_pairs"]),
+        "K3_bin": ("hbm", 32 * max(1, st["large_pairs"])),
+        "K4_large": ("alu", ALU_PER_ITEM * large_items + ALU_PER_SETUP * st["chunks"]),
+        "K5_unpack": ("hbm", 16 * n_rays),
+    }
+    out = {}
+    for k, (bound, amount) in work.items():
+        t = max(kernel_ms[k], 1e-9) / 1e3
+        if bound == "hbm":
+            ach, peak, unit = amount / t / 1e9, pk["hbm_gbs"], "GB/s"
+        else:
+            ach, peak, unit = amount / t / 1e12, alu_peak, "Tops/s"
+        tr = traffic.get(k)
+        out[k] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                  "traffic": tr, "algorithmic_per_launch": amount,
+                  "peak_src": (pk["src"] + " (MEASURED_PEAKS.json hbm_gbs)") if bound == "hbm" else
+                  f"derived: {n_sm} SMs x 128 fp32 lanes x {mhz:.0f} MHz (median SM clock under load)",
+                  "traffic_src": src}
+    # K2 also streams the triangle soup once: report its HBM fraction beside the ALU one
+    t2 = max(kernel_ms["K2_cull"], 1e-9) / 1e3
+    out["K2_cull"]["hbm_achieved_gbs"] = 48 * n_tri / t2 / 1e9
+    out["K2_cull"]["hbm_frac"] = out["K2_cull"]["hbm_achieved_gbs"] / pk["hbm_gbs"]
+    return out
+
+
 # ------------------------------------------------------------------ main --
 def main():
     ap = argparse.ArgumentParser()
@@ -185,6 +251,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--small-max", type=int, default=0)
+    ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters"])
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to exercise the N>1 logic with several ranks on one GPU")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -228,31 +297,44 @@ def main():
     import torch.distributed as dist
 
     from paper_2605_10457_b200 import Grca
+    from paper_2605_10457_b200 import dist as D
     from paper_2605_10457_b200 import grca as G
 
+    dev_index = local_rank if args.backend == "nccl" else local_rank % max(1, torch.cuda.device_count())
     if world > 1:
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-    device = torch.device(f"cuda:{local_rank}")
+        torch.cuda.set_device(dev_index)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev_index}"))
+        else:
+            dist.init_process_group("gloo")
+    device = torch.device(f"cuda:{dev_index}")
     torch.cuda.set_device(device)
+    n_em_total = len(sg.workload(args.config)["emitters"]) if args.config == "C1" else sg.WORKLOADS[args.config][0]
+    shard = args.shard if args.shard != "auto" else (D.choose_mode(n_em_total, world) if world > 1 else "triangles")
 
-    scene = Scene(args.config, rank, world, device, args.deformation)
+    scene = Scene(args.config, rank, world, device, args.deformation, shard=shard)
     ems = scene.emitters
     n_rays = sg.n_rays_total(ems)
-    g = Grca(device=local_rank, max_triangles=scene.n_tri, max_rays=n_rays, debug_flags=G.PROFILE_KERNELS,
+    n_rays_job = sg.n_rays_total(scene.w["emitters"])
+    g = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays, debug_flags=G.PROFILE_KERNELS,
              small_max=args.small_max, nranks=world, rank=rank)
     g.set_emitters(ems)
     dist_out = torch.empty(n_rays, dtype=torch.float32, device=device)
     tri_out = torch.empty(n_rays, dtype=torch.int32, device=device)
 
+    merge = world > 1 and shard == "triangles"
+
+    def cast_once():
+        if merge:   # triangle shards: exact merge = all-reduce(MIN) of the packed (t, id) keys
+            g.cast_packed()
+            D.merge_packed(g.hits_packed())
+            g.unpack(dist_out, tri_out)
+        else:       # single GPU, or sensor shards (disjoint ray slices, no reduction)
+            g.cast(dist_out, tri_out)
+
     def step(k):
         g.update_triangles(scene.frames[k % N_FRAMES], tri_ids=scene.ids)
-        if world > 1:
-            g.cast_packed()
-            dist.all_reduce(g.hits_packed(), op=dist.ReduceOp.MIN)   # exact merge: min over (t, id) keys
-            g.unpack(dist_out, tri_out)
-        else:
-            g.cast(dist_out, tri_out)
+        cast_once()
 
     stream = torch.cuda.current_stream(device)
     for k in range(args.warmup):
@@ -285,7 +367,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    rays_s = n_rays * args.steps / (ms / 1e3)
+    rays_s = n_rays_job * args.steps / (ms / 1e3)   # whole job: every rank's rays of the frame
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
@@ -302,12 +384,7 @@ def main():
         for k in range(k_e2e):
             dev_buf[3 * scene.n_static_local:].copy_(host_dyn[k % N_FRAMES], non_blocking=True)
             g.update_triangles(dev_buf, tri_ids=scene.ids)
-            if world > 1:
-                g.cast_packed()
-                dist.all_reduce(g.hits_packed(), op=dist.ReduceOp.MIN)
-                g.unpack(dist_out, tri_out)
-            else:
-                g.cast(dist_out, tri_out)
+            cast_once()
             host_dist.copy_(dist_out, non_blocking=True)
             host_tri.copy_(tri_out, non_blocking=True)
         f1.record(stream)
@@ -317,26 +394,16 @@ def main():
             t = torch.tensor([ems_e2e], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems_e2e = float(t.item())
-        e2e = {"value": n_rays * k_e2e / (ems_e2e / 1e3), "unit": "rays/s", "ms_per_step": ems_e2e / k_e2e,
+        e2e = {"value": n_rays_job * k_e2e / (ems_e2e / 1e3), "unit": "rays/s", "ms_per_step": ems_e2e / k_e2e,
                "h2d_bytes_per_step": int(n_dyn_vals * 16), "d2h_bytes_per_step": int(n_rays * 8), "steps": k_e2e,
                "what": "pinned H2D of this frame's dynamic vertices + grca_cast + D2H of (dist, id) per ray"}
 
-    # ---- roofline of the dominant kernel (per-kernel CUDA events on the launch stream)
-    pk = peaks()
-    names = ["K0_init", "K2_cull", "K2b_refine", "K4s_small", "K3_bin", "K4_large", "K5_unpack"]
-    kernel_ms = {n: kms[i] for i, n in enumerate(names)}
-    tri_bytes = 48 * scene.n_tri   # algorithmic: 3 float4 vertices per triangle (non-indexed)
-    dom = max(names, key=lambda n: kernel_ms[n])
-    alg = {
-        "K0_init": 8 * n_rays, "K2_cull": tri_bytes, "K2b_refine": 50 * max(1, stats["survivors"]),
-        "K4s_small": 16 * max(1, stats["rtic_tested"]), "K3_bin": 16 * max(1, stats["large_pairs"]),
-        "K4_large": 16 * max(1, stats["rtic_tested"]), "K5_unpack": 16 * n_rays,
-    }
-    ach = alg[dom] / (kernel_ms[dom] / 1e3) / 1e9
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / pk["hbm_gbs"], "traffic": None, "peak_src": pk["src"],
-                "algorithmic_bytes_per_launch": alg[dom],
-                "note": "K2 algorithmic bytes = 48 B/triangle vertex read (fused K1 load); see DESIGN.md"}
+    # ---- per-kernel roofline (per-kernel CUDA events on the launch stream, last <= 64 steps)
+    kernel_ms = {n: kms[i] for i, n in enumerate(KERNELS)}
+    roof = kernel_rooflines(kernel_ms, stats, n_rays, scene.n_tri, len(ems), clk, device)
+    dom = max(roof, key=lambda n: kernel_ms[n])
+    roofline = dict(roof[dom])
+    roofline["kernel"] = dom
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -350,16 +417,21 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": args.config, "emitters": len(ems), "rays_per_frame": n_rays,
+            "config": {"workload": args.config, "emitters": len(scene.w["emitters"]), "rays_per_frame": n_rays_job,
                        "triangles": scene.n_tri_global, "dynamic_triangles": int(scene.w["n_dynamic"]),
                        "deformation": args.deformation, "max_range_m": float(ems[0].max_range),
-                       "sharding": f"triangles block-interleaved ({BLOCK}) x {world}" if world > 1 else "none",
+                       "sharding": ("none" if world == 1 else
+                                    f"triangles block-interleaved ({D.BLOCK}) + all-reduce(MIN) x {world}"
+                                    if shard == "triangles" else f"emitters (n mod P) x {world}, no reduction"),
                        "l2": "inputs > L2: 4 resident ~1 GB frame buffers cycled"},
             "frame_ms": ms_step, "rtic_culled_frac": culled,
             "rtic_tested_per_frame": stats["rtic_tested"], "rtic_brute_per_frame": stats["rtic_brute"],
             "rtic_per_s": stats["rtic_tested"] / (ms_step / 1e3),
-            "rtic_effective_per_s": stats["rtic_brute"] / (ms_step / 1e3),
-            "kernel_ms": kernel_ms, "stats": {k: stats[k] for k in (
+            "rtic_effective_per_s": n_rays_job * scene.n_tri_global / (ms_step / 1e3),
+            "stats_scope": "rank 0" if world > 1 else "job",
+            "kernel_ms": kernel_ms, "kernel_roofline": {k: {kk: v[kk] for kk in ("bound", "achieved", "unit", "frac")}
+                                                          for k, v in roof.items()},
+            "stats": {k: stats[k] for k in ("prefilter_survivors", "rtic_small",
                 "pairs", "range_culled", "channel_culled", "azimuth_culled", "survivors", "small_pairs", "large_pairs",
                 "chunks", "fp64_fallbacks", "hits_recorded", "overflow")},
             "roofline": roofline, "gpu_launches": 7 * args.steps, "clocks": clk,

@@ -104,6 +104,8 @@ typedef struct {
     int64_t fp64_fallbacks;  /* candidates decided by the fp64 path */
     int64_t hits_recorded;   /* accepted intersections (before the closest-hit min) */
     int64_t overflow_inline; /* large pairs processed inline because the list was full */
+    int64_t prefilter_survivors; /* pairs passed by the K2 elevation pre-test to K2b */
+    int64_t rtic_small;      /* part of rtic_tested done by K4s (small rectangles) */
     int32_t overflow;        /* 1 if any capacity fallback happened */
     float ms_total;          /* device time of the last cast if GRCA_PROFILE_KERNELS */
     float ms_k[8];           /* per kernel: K0 init, K2 cull, K2b refine, K4s small, K3 bin, K4 large, K5 unpack */

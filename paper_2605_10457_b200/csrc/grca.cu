@@ -36,7 +36,7 @@ constexpr int kLutMaxEm = 16;   // channel LUTs staged in smem for up to 16 emit
 enum Stat {
     ST_PAIRS = 0, ST_RANGE, ST_CHANNEL, ST_AZIMUTH, ST_SURV, ST_SMALL, ST_LARGE, ST_ITEMS_SMALL,
     ST_ITEMS_LARGE, ST_FP64, ST_HITS, ST_CHUNKS, ST_OVF_LARGE, ST_OVF_CHUNK, ST_SETUP64, ST_DEGEN,
-    ST_COUNT
+    ST_K2SURV, ST_COUNT
 };
 
 struct KParams {
@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
     unsigned long long cnt[ST_COUNT];
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
-    unsigned c_pairs = 0, c_range = 0, c_chan = 0;
+    unsigned c_pairs = 0, c_range = 0, c_chan = 0, c_surv = 0;
     const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         if (threadIdx.x == 0) qn = 0;
@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
                                            P.lut ? sLut + sL[e].lut_base : nullptr);
                 c_range += (st == CULL_RANGE);
                 c_chan += (st == CULL_CHANNEL);
+                c_surv += (st == CULL_KEEP);
             }
             const bool keep = st == CULL_KEEP;
             const unsigned m = __ballot_sync(FULL, keep);
@@ -186,6 +187,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
     cnt[ST_PAIRS] = c_pairs;
     cnt[ST_RANGE] = c_range;
     cnt[ST_CHANNEL] = c_chan;
+    cnt[ST_K2SURV] = c_surv;
     block_flush(acc, P.stats, cnt);
 }
 
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull_fixed(const KParams P, cons
     if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
     __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned c_pairs = 0, c_range = 0, c_chan = 0;
+    unsigned c_pairs = 0, c_range = 0, c_chan = 0, c_surv = 0;
     const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long t = tile * K2_THREADS + threadIdx.x;
@@ -243,6 +245,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull_fixed(const KParams P, cons
         }
         const int cntk = __popc(keep);
         c_range += __popc(rng);
+        c_surv += cntk;
         // block-wide exclusive scan of the per-thread survivor counts
         int incl = cntk;
 #pragma unroll
@@ -281,6 +284,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull_fixed(const KParams P, cons
     cnt[ST_PAIRS] = c_pairs;
     cnt[ST_RANGE] = c_range;
     cnt[ST_CHANNEL] = c_chan;
+    cnt[ST_K2SURV] = c_surv;
     block_flush(acc, P.stats, cnt);
 }
 
@@ -1264,6 +1268,8 @@ static grca_status fill_stats(grca_t h, grca_stats *s) {
     s->fp64_fallbacks = (int64_t)st[ST_FP64];
     s->hits_recorded = (int64_t)st[ST_HITS];
     s->overflow_inline = (int64_t)(st[ST_OVF_LARGE] + st[ST_OVF_CHUNK]);
+    s->prefilter_survivors = (int64_t)st[ST_K2SURV];
+    s->rtic_small = (int64_t)st[ST_ITEMS_SMALL];
     s->overflow = s->overflow_inline > 0;
     if (h->ev_ok && h->n_casts > 0) {
         const int slot = (int)((h->n_casts - 1) % kRing);

@@ -359,7 +359,7 @@ __device__ __forceinline__ int quick_cull(const f3 v[3], float emax, const EmLit
     const float rlb = rmax - emax;
     const bool range = rlb > L.lim;
     const bool near = !(rlb > 2.f * emax);   // near (or degenerate / non-finite): exact path in K2b
-    const float q = emax * __frcp_rn(fmaxf(rlb, 1e-30f));
+    const float q = __fdividef(emax, rlb);   // garbage when rlb <= 0, but then near = true
     const float q2 = q * q;
     const float smax = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));
     const bool pole = smax >= 1.f - 0.51f * q2 - 1e-5f;   // a pole may lie inside T

@@ -1,0 +1,102 @@
+"""Multi-GPU partitioning and merge for the GRCA hot path.
+
+One process per GPU, torch.distributed for the plumbing (NCCL on B200, gloo in CPU tests).
+
+* Triangle sharding (default): triangles are independent units and the per-ray closest hit is a
+  min over triangles (an associative, commutative lattice), so any partition of the triangles
+  merges exactly by an element-wise min of the per-shard packed hit buffers.  Blocks of BLOCK
+  consecutive triangles go to rank b mod P (heavy objects spread over ranks); global ids travel
+  with the triangles.  The one exchange step is an in-place all-reduce(MIN) of the packed
+  buffer (int64 view of (fp32 t bits << 32 | id): non-negative, so signed min == unsigned min).
+* Sensor (emitter) sharding when Omega >= P: emitter n -> rank n mod P; every rank casts all
+  triangles for its emitters; outputs are disjoint ray slices (no reduction for the cast; an
+  optional all-gather assembles the full layout).
+
+Nothing here computes any part of the method: it only partitions inputs and moves results.
+"""
+from __future__ import annotations
+
+from typing import List, Sequence
+
+import numpy as np
+
+BLOCK = 4096
+MISS_KEY = 0x7F800000FFFFFFFF
+
+
+def shard_triangles(n_tri: int, rank: int, world: int, block: int = BLOCK) -> np.ndarray:
+    """Global indices of the triangles owned by `rank` (block-interleaved)."""
+    idx = np.arange(int(n_tri), dtype=np.int64)
+    return idx[((idx // block) % world) == rank]
+
+
+def shard_emitters(n_emitters: int, rank: int, world: int) -> List[int]:
+    """Emitter indices owned by `rank` under sensor sharding (emitter n -> rank n mod P)."""
+    return [n for n in range(int(n_emitters)) if n % world == rank]
+
+
+def choose_mode(n_emitters: int, world: int) -> str:
+    """'emitters' when every rank gets the same number of emitters (Omega >= P, P | Omega), else
+    'triangles' (sensor sharding needs no reduction but re-reads all triangles)."""
+    if world > 1 and n_emitters >= world and n_emitters % world == 0:
+        return "emitters"
+    return "triangles"
+
+
+def merge_packed(hits, group=None):
+    """In-place exact merge of per-shard packed hit buffers: all-reduce(MIN) over ranks.
+
+    `hits` is an int64 tensor (CUDA with NCCL, CPU with gloo); returns it."""
+    import torch
+    import torch.distributed as dist
+
+    assert hits.dtype == torch.int64
+    dist.all_reduce(hits, op=dist.ReduceOp.MIN, group=group)
+    return hits
+
+
+def gather_emitter_slices(dist_slice, tri_slice, rank_emitters_rays: Sequence[Sequence[int]], offsets, group=None):
+    """Assemble the full (dist, tri) layout from per-rank emitter slices (sensor sharding).
+
+    rank_emitters_rays[r] lists the emitters of rank r; offsets are the global O_n (n_em + 1).
+    Each rank passes its concatenated slices (in its emitter order)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    n_total = int(offsets[-1])
+    sizes = [sum(int(offsets[n + 1] - offsets[n]) for n in rank_emitters_rays[r]) for r in range(world)]
+    mx = max(sizes)
+    pad_d = torch.full((mx,), float("inf"), dtype=dist_slice.dtype, device=dist_slice.device)
+    pad_t = torch.full((mx,), -1, dtype=tri_slice.dtype, device=tri_slice.device)
+    pad_d[: dist_slice.numel()] = dist_slice
+    pad_t[: tri_slice.numel()] = tri_slice
+    gd = [torch.empty_like(pad_d) for _ in range(world)]
+    gt = [torch.empty_like(pad_t) for _ in range(world)]
+    dist.all_gather(gd, pad_d, group=group)
+    dist.all_gather(gt, pad_t, group=group)
+    out_d = torch.empty(n_total, dtype=dist_slice.dtype, device=dist_slice.device)
+    out_t = torch.empty(n_total, dtype=tri_slice.dtype, device=tri_slice.device)
+    for r in range(world):
+        pos = 0
+        for n in rank_emitters_rays[r]:
+            a, b = int(offsets[n]), int(offsets[n + 1])
+            out_d[a:b] = gd[r][pos: pos + (b - a)]
+            out_t[a:b] = gt[r][pos: pos + (b - a)]
+            pos += b - a
+    return out_d, out_t
+
+
+class ShardedCaster:
+    """Triangle-sharded cast over a process group: each rank holds its shard's vertices (and
+    their global ids); `cast()` runs K0..K4 locally, merges with all-reduce(MIN) and unpacks."""
+
+    def __init__(self, grca, group=None):
+        self.g = grca
+        self.group = group
+
+    def cast(self, out_dist, out_tri):
+        self.g.cast_packed()
+        merge_packed(self.g.hits_packed(), self.group)
+        self.g.unpack(out_dist, out_tri)
+        return out_dist, out_tri
