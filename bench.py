@@ -175,7 +175,8 @@ def time_oracle(emitters, tris, target_s: float = 12.0, max_rays: int = 4096):
 
 
 KERNELS = ["K0_init", "K2_cull", "K2b_refine", "K4s_small", "K3_bin", "K4_large", "K5_unpack"]
-NCU_NAME = {"K2_cull": "k_cull_fixed", "K2b_refine": "k_refine", "K4s_small": "k_small", "K4_large": "k_isect",
+# (fused default: "K4s_small" is the fused K2b+K4s kernel k_refine_small and "K2b_refine" is ~0)
+NCU_NAME = {"K2_cull": "k_cull_fixed", "K2b_refine": "k_refine(", "K4s_small": "k_refine_small", "K4_large": "k_isect",
             "K0_init": "k_init", "K3_bin": "k_bin", "K5_unpack": "k_unpack"}
 # algorithmic work per unit: fp32 ALU operations or HBM bytes
 ALU_PER_PAIR_K2 = 50        # elevation pre-test of one (triangle, emitter) pair
@@ -251,6 +252,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--small-max", type=int, default=0)
+    ap.add_argument("--split-refine", action="store_true", help="K2b and K4s as two kernels (A/B)")
     ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters"])
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 logic with several ranks on one GPU")
@@ -316,7 +318,7 @@ def main():
     ems = scene.emitters
     n_rays = sg.n_rays_total(ems)
     n_rays_job = sg.n_rays_total(scene.w["emitters"])
-    g = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays, debug_flags=G.PROFILE_KERNELS,
+    g = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays, debug_flags=G.PROFILE_KERNELS | (G.DEBUG_SPLIT_REFINE if args.split_refine else 0),
              small_max=args.small_max, nranks=world, rank=rank)
     g.set_emitters(ems)
     dist_out = torch.empty(n_rays, dtype=torch.float32, device=device)

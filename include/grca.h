@@ -58,7 +58,9 @@ enum {
     GRCA_DEBUG_COUNT_ALL_HITS = 1u, /* per-ray count of every accepted hit (all-hits invariant) */
     GRCA_DEBUG_NO_CULL = 2u,        /* every (tri, emitter) pair tests the full ray grid */
     GRCA_PROFILE_KERNELS = 4u,      /* CUDA events around each kernel; see grca_kernel_times */
-    GRCA_DEBUG_FORCE_FP64 = 8u      /* every candidate takes the fp64 path (precision check) */
+    GRCA_DEBUG_FORCE_FP64 = 8u,     /* every candidate takes the fp64 path (precision check) */
+    GRCA_DEBUG_SPLIT_REFINE = 16u   /* run K2b (bounds) and K4s (small work) as two kernels instead of
+                                       the fused refine+small kernel (A/B measurement, same results) */
 };
 
 typedef struct {
@@ -108,7 +110,8 @@ typedef struct {
     int64_t rtic_small;      /* part of rtic_tested done by K4s (small rectangles) */
     int32_t overflow;        /* 1 if any capacity fallback happened */
     float ms_total;          /* device time of the last cast if GRCA_PROFILE_KERNELS */
-    float ms_k[8];           /* per kernel: K0 init, K2 cull, K2b refine, K4s small, K3 bin, K4 large, K5 unpack */
+    float ms_k[8];           /* per kernel: K0 init, K2 cull, K2b refine (split mode only), K2b+K4s
+                                refine+small (K4s in split mode), K3 bin, K4 large, K5 unpack */
 } grca_stats;
 
 /* Create a handle bound to ci->device.  Allocates all device scratch.

@@ -516,6 +516,168 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const KParams P) {
     block_flush(acc, P.stats, cnt);
 }
 
+// ----------------------------------------- K2b+K4s fused: refine + small work --
+// One warp per 32-survivor round (interleaved over all warps): lane-per-survivor exact rectangle
+// (cull_pair), certified setup of small rectangles into shared-memory float4 slots, then the
+// warp expands all items of its small rectangles with a prefix scan (A5) and tests them 32 at a
+// time (A6).  Large rectangles go to the large list (K3/K4).  One vertex fetch per survivor.
+__global__ void __launch_bounds__(K2_THREADS) k_refine_small(const KParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float4 *sSlot = reinterpret_cast<float4 *>(smem);   // [warp][6][32]
+    int *sExcl = reinterpret_cast<int *>(sSlot + (K2_THREADS / 32) * 6 * 32);   // [warp][32]
+    EmDev *sE = reinterpret_cast<EmDev *>(sExcl + K2_THREADS);
+    float *sSin = reinterpret_cast<float *>(sE + P.n_em);
+    unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
+    __shared__ unsigned long long acc[ST_COUNT];
+    {
+        const int nw = P.n_em * (int)(sizeof(EmDev) / 4);
+        const int *src = reinterpret_cast<const int *>(P.em);
+        int *dst = reinterpret_cast<int *>(sE);
+        for (int i = threadIdx.x; i < nw; i += blockDim.x) dst[i] = src[i];
+        for (int i = threadIdx.x; i < P.n_sin; i += blockDim.x) sSin[i] = P.sin[i];
+        if (P.lut)
+            for (int i = threadIdx.x; i < P.n_em * kLutBins; i += blockDim.x) sLut[i] = P.lut[i];
+        if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    float4 *slot = sSlot + wib * 6 * 32;
+    int *excl = sExcl + wib * 32;
+    unsigned long long cnt[ST_COUNT];
+#pragma unroll
+    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
+    unsigned setup64 = 0;
+    const unsigned nr = *P.n_rounds;
+    const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned w = wid; w < nr; w += nwarps) {
+        const unsigned ru = P.rounds[w];
+        const long long tile = ru >> 6;
+        const int n = P.tile_count[tile];
+        const long long region = tile * (long long)K2_THREADS * P.n_em;
+        const int idx = (int)(ru & 63u) * 32 + lane;
+        int my = 0, e = 0;
+        long long t = 0;
+        Rect R;
+        bool large = false;
+        if (idx < n) {
+            const unsigned ent = P.surv[region + idx];
+            e = ent & 255;
+            t = tile * K2_THREADS + (ent >> 8);
+            f3 v[3];
+            load_tri(P.tri, t, v);
+            const EmDev &E = sE[e];
+            const int st = cull_pair(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
+                                     P.nocull != 0, R);
+            if (st == CULL_KEEP) {
+                cnt[ST_SURV]++;
+                const long long items = rect_items(R, E);
+                if (items <= P.small_max && !R.pole_rows) {
+                    Setup S;
+                    if (make_setup(v, em_o(E), P.faces, S, setup64)) {
+                        my = (int)items;
+                        cnt[ST_SMALL]++;
+                        cnt[ST_ITEMS_SMALL] += (unsigned long long)my;
+                        slot[0 * 32 + lane] = make_float4(S.n0.x, S.n0.y, S.n0.z, S.B0);
+                        slot[1 * 32 + lane] = make_float4(S.n1.x, S.n1.y, S.n1.z, S.B1);
+                        slot[2 * 32 + lane] = make_float4(S.n2.x, S.n2.y, S.n2.z, S.B2);
+                        slot[3 * 32 + lane] = make_float4(S.N.x, S.N.y, S.N.z, S.habs);
+                        slot[4 * 32 + lane] = make_float4(S.TN, __uint_as_float(tri_id(P.tri, t)),
+                                                          __int_as_float((int)t), __int_as_float(e));
+                        slot[5 * 32 + lane] = make_float4(__int_as_float(R.c_from), __int_as_float(R.r_lo),
+                                                          __int_as_float(R.r_len), 1.f / (float)R.r_len);
+                    } else {
+                        cnt[ST_DEGEN]++;
+                    }
+                } else {
+                    large = true;
+                }
+            } else if (st == CULL_RANGE) cnt[ST_RANGE]++;
+            else if (st == CULL_CHANNEL) cnt[ST_CHANNEL]++;
+            else if (st == CULL_AZIMUTH) cnt[ST_AZIMUTH]++;
+            else cnt[ST_DEGEN]++;
+        }
+        const unsigned lm = __ballot_sync(FULL, large);
+        if (lm) {
+            const int leader = __ffs(lm) - 1;
+            unsigned base = 0;
+            if (lane == leader) base = atomicAdd(P.n_large, (unsigned)__popc(lm));
+            base = __shfl_sync(FULL, base, leader);
+            if (large) {
+                const long long pos = (long long)base + __popc(lm & ((1u << lane) - 1u));
+                if (pos < P.cap_large) {
+                    P.large[pos] = make_int4((int)t, e | (R.c_from << 8), R.c_to,
+                                             (int)((unsigned)R.r_lo | ((unsigned)R.r_len << 16)));
+                    cnt[ST_LARGE]++;
+                } else {   // capacity fallback: intersect here (slow, never dropped)
+                    cnt[ST_OVF_LARGE]++;
+                    if (R.pole_rows) { R.r_lo = 0; R.r_len = sE[e].chi; }
+                    intersect_rect_serial(P, sE[e], t, R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len, cnt, setup64);
+                }
+            }
+        }
+        // A5: warp-level prefix-scan work expansion
+        int incl = my;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        excl[lane] = incl - my;
+        const int total = __shfl_sync(FULL, incl, 31);
+        __syncwarp();
+        for (int b = 0; b < total; b += 32) {
+            const int qi = b + lane;
+            int ow = 0;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) {
+                const int vv = __shfl_sync(FULL, incl, ow + s - 1);
+                if (vv <= qi) ow += s;
+            }
+            if (qi < total) {
+                const float4 r4 = slot[4 * 32 + ow], r5 = slot[5 * 32 + ow];
+                const EmDev &EO = sE[__float_as_int(r4.w)];
+                const int local = qi - excl[ow];
+                const int len = __float_as_int(r5.z);
+                int row = (int)(((float)local + 0.5f) * r5.w);
+                int col = local - row * len;
+                if (col < 0) { --row; col += len; }
+                if (col >= len) { ++row; col -= len; }
+                const int j = __float_as_int(r5.x) + row;
+                int i = __float_as_int(r5.y) + col;
+                if (i >= EO.chi) i -= EO.chi;
+                const int g = EO.ray_base + j * EO.chi + i;
+                const float4 d = __ldg(P.raytab + g);
+                const float4 r0 = slot[0 * 32 + ow], r1 = slot[1 * 32 + ow], r2 = slot[2 * 32 + ow],
+                             r3 = slot[3 * 32 + ow];
+                Setup Q;
+                Q.n0 = {r0.x, r0.y, r0.z};
+                Q.n1 = {r1.x, r1.y, r1.z};
+                Q.n2 = {r2.x, r2.y, r2.z};
+                Q.B0 = r0.w; Q.B1 = r1.w; Q.B2 = r2.w;
+                Q.N = {r3.x, r3.y, r3.z};
+                Q.habs = r3.w;
+                Q.TN = r4.x;
+                float th = 0.f;
+                int r = P.force64 ? 2 : test_fast(d, Q, EO.dmax_lo, EO.dmax_hi, th);
+                if (r == 2) {
+                    cnt[ST_FP64]++;
+                    f3 wv[3];
+                    load_tri(P.tri, (long long)__float_as_int(r4.z), wv);
+                    r = test_exact(wv, em_o(EO), d, EO.dmax, P.faces, th);
+                }
+                if (r == 1) {
+                    cnt[ST_HITS]++;
+                    record_hit(P.hits, P.allhits, g, th, __float_as_uint(r4.y));
+                }
+            }
+        }
+        __syncwarp();
+    }
+    cnt[ST_SETUP64] = setup64;
+    block_flush(acc, P.stats, cnt);
+}
+
 // ------------------------------------------------------------------ K3 bin --
 // Row groups of a large rectangle: pole rows (channels with cos(phi) < 0.01) take all chi
 // rays; the rest take [r_lo, r_lo + r_len).  Each group becomes chunks of <= kChunkItems
@@ -723,8 +885,8 @@ struct grca_ctx {
     grca_create_info ci{};
     std::string err;
     int num_sms = 148;
-    int k2_blocks_per_sm = 1, k2b_blocks_per_sm = 1, k4s_blocks_per_sm = 1, k4_blocks_per_sm = 1;
-    size_t k2_smem = 0, k2b_smem = 0, k4s_smem = 0;
+    int k2_blocks_per_sm = 1, k2b_blocks_per_sm = 1, k4s_blocks_per_sm = 1, k4_blocks_per_sm = 1, kf_blocks_per_sm = 1;
+    size_t k2_smem = 0, k2b_smem = 0, k4s_smem = 0, kf_smem = 0;
     // emitters
     int n_em = 0;
     int n_sin = 0;
@@ -869,6 +1031,10 @@ static size_t k2b_smem_bytes(int n_em, int n_sin, bool lut) {
     return sizeof(EmDev) * n_em + sizeof(float) * ((n_sin + 3) & ~3) + (lut ? (size_t)n_em * kLutBins : 0);
 }
 static size_t k4s_smem_bytes(int n_em) { return sizeof(EmDev) * n_em + sizeof(float) * NF * K2_THREADS; }
+static size_t kfused_smem_bytes(int n_em, int n_sin, bool lut) {
+    return sizeof(float4) * (K2_THREADS / 32) * 6 * 32 + sizeof(int) * K2_THREADS + sizeof(EmDev) * n_em +
+           sizeof(float) * ((n_sin + 3) & ~3) + (lut ? (size_t)n_em * kLutBins : 0);
+}
 
 extern "C" {
 
@@ -935,6 +1101,8 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2b_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k4s_smem_bytes(kMaxEmitters));
+    cudaFuncSetAttribute(k_refine_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kfused_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_isect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(EmDev) * kMaxEmitters));
     cudaStreamSynchronize(h->stream);
     if (cudaGetLastError() != cudaSuccess) {
@@ -1143,6 +1311,7 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     h->k2f_smem = sizeof(float) * ((h->n_sin + 3) & ~3) + (use_lut ? (size_t)n_emitters * kLutBins : 0);
     h->k2b_smem = k2b_smem_bytes(n_emitters, h->n_sin, use_lut);
     h->k4s_smem = k4s_smem_bytes(n_emitters);
+    h->kf_smem = kfused_smem_bytes(n_emitters, h->n_sin, use_lut);
     int b2 = 0, b2b = 0, b4s = 0, b4 = 0;
     if (n_emitters <= kFixedEm) {
         const void *fn = k2_fixed_fn(n_emitters);
@@ -1153,6 +1322,9 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2b, k_refine, K2_THREADS, h->k2b_smem));
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4s, k_small, K2_THREADS, h->k4s_smem));
     h->k4s_blocks_per_sm = std::max(1, b4s);
+    int bf = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_refine_small, K2_THREADS, h->kf_smem));
+    h->kf_blocks_per_sm = std::max(1, bf);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_isect, K4_THREADS, sizeof(EmDev) * n_emitters));
     h->k2_blocks_per_sm = std::max(1, b2);
     h->k2b_blocks_per_sm = std::max(1, b2b);
@@ -1209,15 +1381,21 @@ static grca_status launch_packed(grca_t h) {
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][2], h->stream));
     const long long tiles = (h->n_tri + K2_THREADS - 1) / K2_THREADS;
-    if (h->n_tri > 0) {   // K2b: warp per tile
+    const bool split = (h->ci.debug_flags & GRCA_DEBUG_SPLIT_REFINE) != 0;
+    if (h->n_tri > 0 && split) {   // K2b (bounds only), rounds interleaved over warps
         const long long grid = (long long)h->num_sms * h->k2b_blocks_per_sm;
         k_refine<<<(unsigned)grid, K2_THREADS, h->k2b_smem, h->stream>>>(P);
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][3], h->stream));
-    if (h->n_tri > 0) {   // K4s: warp per tile
-        const long long grid = (long long)h->num_sms * h->k4s_blocks_per_sm;
-        k_small<<<(unsigned)grid, K2_THREADS, h->k4s_smem, h->stream>>>(P);
+    if (h->n_tri > 0) {   // K4s (split) or fused K2b+K4s
+        if (split) {
+            const long long grid = (long long)h->num_sms * h->k4s_blocks_per_sm;
+            k_small<<<(unsigned)grid, K2_THREADS, h->k4s_smem, h->stream>>>(P);
+        } else {
+            const long long grid = (long long)h->num_sms * h->kf_blocks_per_sm;
+            k_refine_small<<<(unsigned)grid, K2_THREADS, h->kf_smem, h->stream>>>(P);
+        }
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][4], h->stream));

@@ -500,8 +500,7 @@ __device__ __noinline__ int test_exact(const f3 v[3], f3 o, float4 d4, double dm
 __device__ __forceinline__ void record_hit(unsigned long long *hits, unsigned *allhits, int g, float t, uint32_t id) {
     const unsigned long long key = ((unsigned long long)__float_as_uint(t) << 32) | id;
     if (allhits) atomicAdd(allhits + g, 1u);
-    const unsigned long long cur = __ldcg(hits + g);
-    if (key < cur) atomicMin(hits + g, key);
+    atomicMin(hits + g, key);   // result unused -> RED.MIN: fire-and-forget, no L2 round trip
 }
 
 }  // namespace grca

@@ -345,3 +345,14 @@ def test_many_emitters_generic_paths(n_em):
     dist, tri, st, _ = run(ems, tris)
     check(ems, tris, dist, tri)
     assert st["pairs"] == len(tris) * n_em
+
+
+def test_split_refine_path_identical():
+    """The two-kernel (K2b bounds + K4s small) path gives bit-identical results to the fused one."""
+    ems, tris = sg.random_scene(55, n_tris=1500, n_emitters=3, gamma=14, chi=220, extent=9.0)
+    a = run(ems, tris)
+    b = run(ems, tris, flags=G.DEBUG_SPLIT_REFINE)
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
+    for k in ("survivors", "small_pairs", "large_pairs", "rtic_tested", "hits_recorded"):
+        assert a[2][k] == b[2][k], k
+    check(ems, tris, a[0], a[1])
