@@ -626,30 +626,46 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine_small(const KParams P) {
         excl[lane] = incl - my;
         const int total = __shfl_sync(FULL, incl, 31);
         __syncwarp();
-        for (int b = 0; b < total; b += 32) {
-            const int qi = b + lane;
-            int ow = 0;
+        // KU candidates per lane in flight: resolve owners and ray indices, issue all ray loads,
+        // then test (memory-level parallelism for the L2-resident ray table)
+        constexpr int KU = 4;
+        for (int b = 0; b < total; b += 32 * KU) {
+            int owv[KU], gv[KU];
+            float4 dv[KU];
 #pragma unroll
-            for (int s = 16; s > 0; s >>= 1) {
-                const int vv = __shfl_sync(FULL, incl, ow + s - 1);
-                if (vv <= qi) ow += s;
+            for (int u = 0; u < KU; ++u) {
+                const int qi = b + u * 32 + lane;
+                int ow = 0;
+#pragma unroll
+                for (int s = 16; s > 0; s >>= 1) {
+                    const int vv = __shfl_sync(FULL, incl, ow + s - 1);
+                    if (vv <= qi) ow += s;
+                }
+                owv[u] = ow;
+                gv[u] = -1;
+                if (qi < total) {
+                    const float4 r5 = slot[5 * 32 + ow];
+                    const EmDev &EO = sE[__float_as_int(slot[4 * 32 + ow].w)];
+                    const int local = qi - excl[ow];
+                    const int len = __float_as_int(r5.z);
+                    int row = (int)(((float)local + 0.5f) * r5.w);
+                    int col = local - row * len;
+                    if (col < 0) { --row; col += len; }
+                    if (col >= len) { ++row; col -= len; }
+                    const int j = __float_as_int(r5.x) + row;
+                    int i = __float_as_int(r5.y) + col;
+                    if (i >= EO.chi) i -= EO.chi;
+                    gv[u] = EO.ray_base + j * EO.chi + i;
+                    dv[u] = __ldg(P.raytab + gv[u]);
+                }
             }
-            if (qi < total) {
-                const float4 r4 = slot[4 * 32 + ow], r5 = slot[5 * 32 + ow];
-                const EmDev &EO = sE[__float_as_int(r4.w)];
-                const int local = qi - excl[ow];
-                const int len = __float_as_int(r5.z);
-                int row = (int)(((float)local + 0.5f) * r5.w);
-                int col = local - row * len;
-                if (col < 0) { --row; col += len; }
-                if (col >= len) { ++row; col -= len; }
-                const int j = __float_as_int(r5.x) + row;
-                int i = __float_as_int(r5.y) + col;
-                if (i >= EO.chi) i -= EO.chi;
-                const int g = EO.ray_base + j * EO.chi + i;
-                const float4 d = __ldg(P.raytab + g);
+#pragma unroll
+            for (int u = 0; u < KU; ++u) {
+                if (gv[u] < 0) continue;
+                const int ow = owv[u];
                 const float4 r0 = slot[0 * 32 + ow], r1 = slot[1 * 32 + ow], r2 = slot[2 * 32 + ow],
-                             r3 = slot[3 * 32 + ow];
+                             r3 = slot[3 * 32 + ow], r4 = slot[4 * 32 + ow];
+                const EmDev &EO = sE[__float_as_int(r4.w)];
                 Setup Q;
                 Q.n0 = {r0.x, r0.y, r0.z};
                 Q.n1 = {r1.x, r1.y, r1.z};
@@ -659,16 +675,16 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine_small(const KParams P) {
                 Q.habs = r3.w;
                 Q.TN = r4.x;
                 float th = 0.f;
-                int r = P.force64 ? 2 : test_fast(d, Q, EO.dmax_lo, EO.dmax_hi, th);
+                int r = P.force64 ? 2 : test_fast(dv[u], Q, EO.dmax_lo, EO.dmax_hi, th);
                 if (r == 2) {
                     cnt[ST_FP64]++;
                     f3 wv[3];
                     load_tri(P.tri, (long long)__float_as_int(r4.z), wv);
-                    r = test_exact(wv, em_o(EO), d, EO.dmax, P.faces, th);
+                    r = test_exact(wv, em_o(EO), dv[u], EO.dmax, P.faces, th);
                 }
                 if (r == 1) {
                     cnt[ST_HITS]++;
-                    record_hit(P.hits, P.allhits, g, th, __float_as_uint(r4.y));
+                    record_hit(P.hits, P.allhits, gv[u], th, __float_as_uint(r4.y));
                 }
             }
         }
