@@ -173,6 +173,10 @@ grca_status grca_debug_all_hits(grca_t h, const uint32_t **d_counts);
  * int32[4] {tri, emitter | c_from << 8, c_to, r_lo | r_len << 16}; *n_out = entries appended. */
 grca_status grca_debug_large_list(grca_t h, int32_t *h_out, int64_t cap, int64_t *n_out);
 
+/* Test-only, host: the azimuth approximation used by the cull (|error| <= 2.0e-6 rad),
+ * evaluated with the same code on the host for n (y, x) pairs. */
+grca_status grca_debug_fast_atan2(const float *h_y, const float *h_x, float *h_out, int64_t n);
+
 /* n_rays_total and ray_offsets[n_emitters + 1] (O_n) of the current emitters. */
 grca_status grca_get_layout(grca_t h, int64_t *n_rays_total, int64_t *ray_offsets);
 

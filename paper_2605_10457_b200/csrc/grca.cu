@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine_small(const KParams P) {
         __syncwarp();
         // KU candidates per lane in flight: resolve owners and ray indices, issue all ray loads,
         // then test (memory-level parallelism for the L2-resident ray table)
-        constexpr int KU = 4;
+        constexpr int KU = 1;
         for (int b = 0; b < total; b += 32 * KU) {
             int owv[KU], gv[KU];
             float4 dv[KU];
@@ -1396,7 +1396,6 @@ static grca_status launch_packed(grca_t h) {
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][2], h->stream));
-    const long long tiles = (h->n_tri + K2_THREADS - 1) / K2_THREADS;
     const bool split = (h->ci.debug_flags & GRCA_DEBUG_SPLIT_REFINE) != 0;
     if (h->n_tri > 0 && split) {   // K2b (bounds only), rounds interleaved over warps
         const long long grid = (long long)h->num_sms * h->k2b_blocks_per_sm;
@@ -1551,6 +1550,12 @@ grca_status grca_debug_large_list(grca_t h, int32_t *h_out, int64_t cap, int64_t
     const long long m = std::min<long long>(std::min<long long>(n, h->cap_large), cap);
     if (h_out && m > 0) CK(cudaMemcpy(h_out, h->d_large, sizeof(int4) * m, cudaMemcpyDeviceToHost));
     *n_out = n;
+    return GRCA_OK;
+}
+
+grca_status grca_debug_fast_atan2(const float *h_y, const float *h_x, float *h_out, int64_t n) {
+    if ((!h_y || !h_x || !h_out) && n > 0) return GRCA_E_INVALID;
+    for (int64_t i = 0; i < n; ++i) h_out[i] = fast_atan2(h_y[i], h_x[i]);
     return GRCA_OK;
 }
 

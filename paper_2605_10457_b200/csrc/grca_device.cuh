@@ -81,9 +81,34 @@ __device__ __forceinline__ d3 crossd(d3 a, d3 b) {
 }
 // Lexicographic order of fp32 points: the canonical edge direction (watertightness).
 __device__ __forceinline__ bool lexless(f3 p, f3 q) {
-    return p.x < q.x || (p.x == q.x && (p.y < q.y || (p.y == q.y && p.z < q.z)));
+    const bool lx = p.x < q.x, ex = p.x == q.x, ly = p.y < q.y, ey = p.y == q.y, lz = p.z < q.z;
+    return lx | (ex & (ly | (ey & lz)));
 }
 __device__ __forceinline__ bool finite3(f3 a) { return isfinite(a.x) && isfinite(a.y) && isfinite(a.z); }
+
+// atan2 with |error| <= 2.0e-6 rad (odd degree-11 least-max polynomial on [0, 1] after octant
+// reduction; bound checked on 2M points by tests/test_abi_cpu.py through grca_debug_fast_atan2).
+// Used for vertex azimuths, whose cull pad (kPadTheta = 5e-5) budgets 2.5e-6 for it.
+__host__ __device__ __forceinline__ float fast_atan2(float y, float x) {
+    const float ax = fabsf(x), ay = fabsf(y);
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+#ifdef __CUDA_ARCH__
+    const float z = mx > 0.f ? __fdividef(mn, mx) : 0.f;
+#else
+    const float z = mx > 0.f ? mn / mx : 0.f;
+#endif
+    const float z2 = z * z;
+    float p = -0.011710336431860924f;
+    p = p * z2 + 0.05262540653347969f;
+    p = p * z2 - 0.11640699207782745f;
+    p = p * z2 + 0.1935330331325531f;
+    p = p * z2 - 0.3326217532157898f;
+    p = p * z2 + 0.999977171421051f;
+    float a = p * z;
+    if (ay > ax) a = 1.5707963267948966f - a;
+    if (x < 0.f) a = 3.141592653589793f - a;
+    return copysignf(a, y);
+}
 
 // ----------------------------------------------------------------- A1 load --
 struct TriSrc {
@@ -280,7 +305,7 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
     }
     float th[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) th[k] = atan2f(x[k].y, x[k].x);
+    for (int k = 0; k < 3; ++k) th[k] = fast_atan2(x[k].y, x[k].x);
     // sort 3 angles
     float t0 = fminf(th[0], fminf(th[1], th[2]));
     float t2 = fmaxf(th[0], fmaxf(th[1], th[2]));
@@ -303,7 +328,13 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
         int n = ihi - ilo + 1;
         if (n <= 0) return CULL_AZIMUTH;
         if (n >= E.chi) { R.r_lo = 0; R.r_len = E.chi; }
-        else { int r = ilo % E.chi; R.r_lo = r < 0 ? r + E.chi : r; R.r_len = n; }
+        else {   // ilo is within ~[-1, chi + 1]: wrap without an integer division
+            int r = ilo;
+            while (r < 0) r += E.chi;
+            while (r >= E.chi) r -= E.chi;
+            R.r_lo = r;
+            R.r_len = n;
+        }
     } else {
         // 180 deg: valid indices [0, chi-1]; the arc may also appear one period (2 chi) lower.
         int lo = INT_MAX, hi = INT_MIN;
@@ -414,7 +445,8 @@ __device__ __forceinline__ bool make_setup(const f3 v[3], f3 o, int faces, Setup
         sg[k] = sw ? -1.f : 1.f;
         f3 aP = subf(P, o), e = subf(Q, P);
         n[k] = crossf(aP, e);
-        B[k] = __fmul_rn(__fmul_rn(16.f * kU, sqrtf(dotf(aP, aP))), sqrtf(dotf(e, e)));
+        const float pe = __fmul_rn(dotf(aP, aP), dotf(e, e));
+        B[k] = __fmul_rn(16.1f * kU, pe > 0.f ? __fmul_rn(pe, rsqrtf(pe)) : 0.f);   // 16u|a||e| (+ rsqrt slack)
     }
     // plane (N, h) in fp64 from the exact fp64 edges, rounded: t = h / d.N is then certified to
     // 4.5e-6 for all but |cos(view)| < ~0.05.
@@ -445,10 +477,11 @@ __device__ __forceinline__ bool make_setup(const f3 v[3], f3 o, int faces, Setup
     S.B2 = sign_ok ? B[2] : CUDART_INF_F;
     S.N = scalef(N, s);
     S.habs = habs;
-    const float rh = __fadd_rn(1.01f * kU, __fmul_rn(__fdiv_rn(err64, habs), 1.01f));
-    const float Bn = __fmul_rn(3.1f * kU, sqrtf(dotf(N, N)));
+    const float rh = __fadd_rn(1.01f * kU, __fmul_rn(__fdividef(err64, habs), 1.02f));
+    const float nn = dotf(N, N);
+    const float Bn = __fmul_rn(3.11f * kU, nn > 0.f ? __fmul_rn(nn, rsqrtf(nn)) : 0.f);
     (void)setup64;
-    S.TN = (!sign_ok || !(rh < 2e-6f)) ? CUDART_INF_F : __fmul_rn(__fdiv_rn(Bn, __fsub_rn(kTRel - 3.f * kU, rh)), 1.0001f);
+    S.TN = (!sign_ok || !(rh < 2e-6f)) ? CUDART_INF_F : __fmul_rn(__fdividef(Bn, __fsub_rn(kTRel - 3.f * kU, rh)), 1.0002f);
     return true;
 }
 

@@ -22,7 +22,7 @@ DEBUG_COUNT_ALL_HITS, DEBUG_NO_CULL, PROFILE_KERNELS, DEBUG_FORCE_FP64, DEBUG_SP
 EXPORTS = [
     "grca_create", "grca_destroy", "grca_set_emitters", "grca_update_triangles", "grca_cast",
     "grca_cast_packed", "grca_hits_packed", "grca_unpack", "grca_get_stats", "grca_kernel_times",
-    "grca_debug_all_hits", "grca_debug_large_list", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
+    "grca_debug_all_hits", "grca_debug_large_list", "grca_debug_fast_atan2", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
 ]
 
 
@@ -87,6 +87,7 @@ def load(path: str = LIB_PATH):
         "grca_kernel_times": ([vp, i32, C.POINTER(C.c_float)], C.c_int),
         "grca_debug_all_hits": ([vp, C.POINTER(vp)], C.c_int),
         "grca_debug_large_list": ([vp, vp, i64, C.POINTER(i64)], C.c_int),
+        "grca_debug_fast_atan2": ([vp, vp, vp, i64], C.c_int),
         "grca_get_layout": ([vp, C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "grca_debug_ray_table": ([vp, vp], C.c_int),
         "grca_last_error": ([vp], C.c_char_p),
@@ -102,6 +103,19 @@ def load(path: str = LIB_PATH):
 
 def version() -> str:
     return load().grca_version().decode()
+
+
+def debug_fast_atan2(y, x):
+    """Host evaluation of the cull's azimuth approximation (test-only)."""
+    import numpy as np
+
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.float32))
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float32))
+    out = np.empty_like(y)
+    st = load().grca_debug_fast_atan2(y.ctypes.data, x.ctypes.data, out.ctypes.data, y.size)
+    if st != GRCA_OK:
+        raise GrcaError(st, "grca_debug_fast_atan2")
+    return out
 
 
 class _CudaArray:

@@ -22,7 +22,7 @@ def lib():
 def _declared():
     src = open(os.path.join(ROOT, "include", "grca.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(grca_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(grca_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_header_declares_boundary():
@@ -94,3 +94,26 @@ def test_oracle_not_imported_by_product():
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert not re.search(r"^\s*(import|from)\s+paper_2605_10457_b200\b", txt, flags=re.M), f
             assert '#include "grca.h"' not in txt and "libgrca" not in txt, f
+
+
+def test_fast_atan2_error_bound(lib):
+    """The cull's azimuth approximation stays within 2.0e-6 rad of atan2 (the azimuth pad of 5e-5
+    budgets 2.5e-6 for it)."""
+    import numpy as np
+
+    from paper_2605_10457_b200 import grca
+
+    rng = np.random.default_rng(0)
+    th = rng.uniform(-np.pi, np.pi, 2_000_000)
+    r = np.exp(rng.uniform(-20, 20, th.size))
+    y = (r * np.sin(th)).astype(np.float32)
+    x = (r * np.cos(th)).astype(np.float32)
+    edge = np.array([[0, 1], [1, 0], [0, -1], [-1, 0], [1, 1], [-1, -1], [1e-30, 1], [1, 1e-30], [-0.0, -1]],
+                    np.float32)
+    y = np.concatenate([y, edge[:, 0]])
+    x = np.concatenate([x, edge[:, 1]])
+    got = grca.debug_fast_atan2(y, x).astype(np.float64)
+    ref = np.arctan2(y.astype(np.float64), x.astype(np.float64))
+    err = np.abs(got - ref)
+    err = np.minimum(err, 2 * np.pi - err)   # +-pi are the same azimuth
+    assert err.max() <= 2.0e-6, err.max()
