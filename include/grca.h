@@ -59,8 +59,9 @@ enum {
     GRCA_DEBUG_NO_CULL = 2u,        /* every (tri, emitter) pair tests the full ray grid */
     GRCA_PROFILE_KERNELS = 4u,      /* CUDA events around each kernel; see grca_kernel_times */
     GRCA_DEBUG_FORCE_FP64 = 8u,     /* every candidate takes the fp64 path (precision check) */
-    GRCA_DEBUG_SPLIT_REFINE = 16u   /* run K2b (bounds) and K4s (small work) as two kernels instead of
+    GRCA_DEBUG_SPLIT_REFINE = 16u,  /* run K2b (bounds) and K4s (small work) as two kernels instead of
                                        the fused refine+small kernel (A/B measurement, same results) */
+    GRCA_DEBUG_NO_REFINE = 32u      /* K3 keeps whole rectangle rows (no A7 per-channel refinement) */
 };
 
 typedef struct {

@@ -55,7 +55,7 @@ struct KParams {
     unsigned *n_chunks;
     long long cap_chunks;
     unsigned long long *stats;
-    int faces, nocull, force64, small_max;
+    int faces, nocull, force64, small_max, norefine;
     long long n_rays;
     const EmLite *lite;
     const unsigned char *lut;    // NULL -> binary search
@@ -744,6 +744,8 @@ __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev
 }
 
 __global__ void __launch_bounds__(256) k_bin(const KParams P) {
+    // one warp per large rectangle; lanes = channel rows.  A7 refines each non-pole row of a
+    // partial-arc rectangle to its exact (padded) ray range; rows become chunks of <= kColMax rays.
     __shared__ unsigned long long acc[ST_COUNT];
     if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
     __syncthreads();
@@ -753,58 +755,79 @@ __global__ void __launch_bounds__(256) k_bin(const KParams P) {
     unsigned setup64 = 0;
     const int lane = threadIdx.x & 31;
     const long long n = min((long long)*P.n_large, P.cap_large);
-    const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long base = (long long)blockIdx.x * blockDim.x; base < n; base += stride) {
-        const long long idx = base + threadIdx.x;
-        const bool act = idx < n;
-        int4 D = make_int4(0, 0, 0, 0);
-        Group G[3];
-        int ng = 0, mych = 0;
-        if (act) {
-            D = P.large[idx];
-            const EmDev &E = P.em[D.y & 255];
-            ng = make_groups((unsigned)D.y >> 8, D.z, D.w & 0xffff, (unsigned)D.w >> 16, E, G);
-            for (int k = 0; k < ng; ++k) mych += group_chunks(G[k]);
-        }
-        int incl = mych;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(FULL, incl, 31);
-        unsigned wbase = 0;
-        if (lane == 31 && total) wbase = atomicAdd(P.n_chunks, (unsigned)total);
-        wbase = __shfl_sync(FULL, wbase, 31);
-        if (!act) continue;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += nw) {
+        const int4 D = P.large[w];
         const long long tri = D.x;
         const int e = D.y & 255;
+        const int c_from = (int)((unsigned)D.y >> 8), c_to = D.z;
+        const int r_lo = D.w & 0xffff, r_len = (int)((unsigned)D.w >> 16);
         const EmDev &E = P.em[e];
-        long long pos = (long long)wbase + incl - mych;
-        if (pos + mych > P.cap_chunks) {   // capacity fallback: intersect here (never dropped)
-            cnt[ST_OVF_CHUNK]++;
-            for (int k = 0; k < ng; ++k)
-                intersect_rect_serial(P, E, tri, G[k].row0, G[k].row1 - G[k].row0 + 1, G[k].lo, G[k].len, cnt,
-                                      setup64);
-            continue;
+        const bool full = r_len >= E.chi;
+        d3 x[3];
+        float th_ref = 0.f;
+        if (!full && !P.norefine) {
+            f3 v[3];
+            load_tri(P.tri, tri, v);
+            const d3 O = {(double)E.o[0], (double)E.o[1], (double)E.o[2]};
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const d3 a = subd(tod(v[k]), O);
+                x[k].x = (double)E.A[0] * a.x + (double)E.A[1] * a.y + (double)E.A[2] * a.z;
+                x[k].y = (double)E.A[3] * a.x + (double)E.A[4] * a.y + (double)E.A[5] * a.z;
+                x[k].z = (double)E.A[6] * a.x + (double)E.A[7] * a.y + (double)E.A[8] * a.z;
+            }
+            th_ref = E.theta0 + ((float)r_lo + 0.5f * (float)r_len) * E.dtheta;   // arc centre
         }
-        cnt[ST_CHUNKS] += mych;
-        for (int k = 0; k < ng; ++k) {
-            const Group &g = G[k];
-            if (g.len > kColMax) {
-                for (int r = g.row0; r <= g.row1; ++r)
-                    for (int c0 = 0; c0 < g.len; c0 += kColMax) {
-                        int lo = g.lo + c0;
-                        if (lo >= E.chi) lo -= E.chi;
-                        P.chunks[pos++] = make_int4((int)tri, e | (r << 8), (int)(1u | ((unsigned)lo << 16)),
-                                                    min(kColMax, g.len - c0));
+        for (int j0 = c_from; j0 <= c_to; j0 += 32) {
+            const int j = j0 + lane;
+            int lo = 0, len = 0;
+            if (j <= c_to) {
+                const bool pole_row = j < E.pole_lo || j > E.gamma - 1 - E.pole_hi;
+                if (pole_row) { lo = 0; len = E.chi; }
+                else if (full || P.norefine) { lo = r_lo; len = r_len; }
+                else {
+                    const double sj = (double)P.sin[E.sin_base + j];
+                    float dmin, dmax;
+                    const int nb = refine_row(x, sj - (double)kPadS, sj + (double)kPadS, th_ref, dmin, dmax);
+                    if (nb < 2) { lo = r_lo; len = r_len; }
+                    else {
+                        const int ilo = (int)ceilf((th_ref + dmin - kPadTheta - E.theta0) * E.inv_dtheta);
+                        const int ihi = (int)floorf((th_ref + dmax + kPadTheta - E.theta0) * E.inv_dtheta);
+                        const int a = max(ilo, r_lo), b = min(ihi, r_lo + r_len - 1);
+                        if (a <= b) {
+                            lo = a;
+                            while (lo >= E.chi) lo -= E.chi;
+                            while (lo < 0) lo += E.chi;
+                            len = b - a + 1;
+                        }
                     }
-            } else {
-                const int rpc = max(1, kChunkItems / g.len);
-                for (int r = g.row0; r <= g.row1; r += rpc) {
-                    const int nr = min(rpc, g.row1 - r + 1);
-                    P.chunks[pos++] = make_int4((int)tri, e | (r << 8), (int)((unsigned)nr | ((unsigned)g.lo << 16)), g.len);
                 }
+            }
+            const int mych = (len + kColMax - 1) / kColMax;
+            int incl = mych;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const int total = __shfl_sync(FULL, incl, 31);
+            unsigned wbase = 0;
+            if (lane == 31 && total) wbase = atomicAdd(P.n_chunks, (unsigned)total);
+            wbase = __shfl_sync(FULL, wbase, 31);
+            if (!mych) continue;
+            long long pos = (long long)wbase + incl - mych;
+            if (pos + mych > P.cap_chunks) {   // capacity fallback: intersect here (never dropped)
+                cnt[ST_OVF_CHUNK]++;
+                intersect_rect_serial(P, E, tri, j, 1, lo, len, cnt, setup64);
+                continue;
+            }
+            cnt[ST_CHUNKS] += mych;
+            for (int c0 = 0; c0 < len; c0 += kColMax) {
+                int l0 = lo + c0;
+                if (l0 >= E.chi) l0 -= E.chi;
+                P.chunks[pos++] = make_int4((int)tri, e | (j << 8), (int)(1u | ((unsigned)l0 << 16)),
+                                            min(kColMax, len - c0));
             }
         }
     }
@@ -1015,6 +1038,7 @@ KParams params(grca_t h) {
     P.faces = h->ci.faces;
     P.nocull = (h->ci.debug_flags & GRCA_DEBUG_NO_CULL) ? 1 : 0;
     P.force64 = (h->ci.debug_flags & GRCA_DEBUG_FORCE_FP64) ? 1 : 0;
+    P.norefine = (h->ci.debug_flags & GRCA_DEBUG_NO_REFINE) ? 1 : 0;
     P.small_max = std::min(1023, h->ci.small_max > 0 ? h->ci.small_max : 512);
     P.n_rays = h->n_rays;
     P.lite = h->d_lite;

@@ -416,6 +416,78 @@ __device__ __forceinline__ int quick_cull(const f3 v[3], float emax, const EmLit
     return range ? CULL_RANGE : (keep ? CULL_KEEP : CULL_CHANNEL);
 }
 
+// ------------------------------------------------ A7 per-channel ray range --
+// Late-pass Steps 1-2 made exact: the points of T whose elevation sine lies in
+// the band [s_lo, s_hi] (the channel's rays, widened by the fp32 pad) form a region whose azimuth
+// extremes are boundary points: crossings of T's edges with the two bounding cones (per-edge
+// quadratic; plane case P:518-528 when s = 0) and vertices inside the band.
+// Each cone meets a ray from the apex at most once, so with no pole in T the region's azimuths
+// form one interval between those extremes, measured along T's arc (SURVEY 8(a) A7 rules).
+// Returns the number of boundary points; dmin/dmax are their azimuths relative to th_ref.
+__device__ __forceinline__ void a7_add(double px, double py, float th_ref, int &cnt, float &dmin, float &dmax) {
+    float d = fast_atan2((float)py, (float)px) - th_ref;
+    if (d >= 3.14159265f) d -= 6.28318531f;
+    if (d < -3.14159265f) d += 6.28318531f;
+    dmin = fminf(dmin, d);
+    dmax = fmaxf(dmax, d);
+    ++cnt;
+}
+
+__device__ __noinline__ int refine_row(const d3 x[3], double s_lo, double s_hi, float th_ref, float &dmin, float &dmax) {
+    int cnt = 0;
+    dmin = CUDART_INF_F;
+    dmax = -CUDART_INF_F;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const double r = sqrt(dotd(x[k], x[k]));
+        const double sk = x[k].z / r;
+        if (sk >= s_lo && sk <= s_hi) a7_add(x[k].x, x[k].y, th_ref, cnt, dmin, dmax);
+    }
+    for (int c = 0; c < 2; ++c) {
+        const double sc = c ? s_hi : s_lo;
+        const double s2 = sc * sc;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const d3 p = x[k];
+            const d3 q = x[(k + 1) % 3];
+            const d3 e = subd(q, p);
+            const double a2 = e.z * e.z - s2 * dotd(e, e);
+            const double a1 = 2.0 * (e.z * p.z - s2 * dotd(p, e));
+            const double a0 = p.z * p.z - s2 * dotd(p, p);
+            double lam[2];
+            int nl = 0;
+            const double scale = fabs(a2) + fabs(a1) + fabs(a0);
+            if (!(scale > 0.0)) {   // the whole edge lies on the cone
+                lam[nl++] = 0.0;
+                lam[nl++] = 1.0;
+            } else if (fabs(a2) <= 1e-14 * scale) {   // linear
+                if (fabs(a1) > 1e-300) lam[nl++] = -a0 / a1;
+            } else {
+                double disc = a1 * a1 - 4.0 * a2 * a0;
+                if (disc < 0.0 && disc > -1e-12 * a1 * a1) disc = 0.0;   // tangency within rounding
+                if (disc >= 0.0) {
+                    const double sq = sqrt(disc);
+                    const double qq = -0.5 * (a1 + (a1 >= 0.0 ? sq : -sq));
+                    if (qq != 0.0) {
+                        lam[nl++] = qq / a2;
+                        lam[nl++] = a0 / qq;
+                    } else {
+                        lam[nl++] = -a1 / (2.0 * a2);
+                    }
+                }
+            }
+            for (int m = 0; m < nl; ++m) {
+                const double l = lam[m];
+                if (!(l >= -1e-9 && l <= 1.0 + 1e-9)) continue;
+                const double px = p.x + l * e.x, py = p.y + l * e.y, pz = p.z + l * e.z;
+                if (sc != 0.0 && pz * sc < -1e-12 * (px * px + py * py + pz * pz)) continue;   // mirror nappe
+                a7_add(px, py, th_ref, cnt, dmin, dmax);
+            }
+        }
+    }
+    return cnt;
+}
+
 // --------------------------------------------------- A6 setup + certified test --
 struct Setup {
     f3 n0, n1, n2;     // sigma_k * s * n_k: hit <=> all d.n_k >= 0

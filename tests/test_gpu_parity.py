@@ -356,3 +356,29 @@ def test_split_refine_path_identical():
     for k in ("survivors", "small_pairs", "large_pairs", "rtic_tested", "hits_recorded"):
         assert a[2][k] == b[2][k], k
     check(ems, tris, a[0], a[1])
+
+
+@pytest.mark.parametrize("seed", [3, 8, 13, 21])
+def test_a7_per_channel_refinement(seed):
+    """A7 (late pass): with every pair forced through the large path, refined
+    per-channel ray ranges give bit-identical results to whole rectangle rows, test fewer
+    candidates, and keep every brute-force hit (all-hits invariant)."""
+    ems, tris = sg.random_scene(200 + seed, n_tris=900, n_emitters=2, gamma=24, chi=400, extent=6.0,
+                                max_range=None if seed % 2 else 9.0)
+    ref = run(ems, tris, small_max=1, flags=G.DEBUG_NO_REFINE)
+    a7 = run(ems, tris, small_max=1, flags=G.DEBUG_COUNT_ALL_HITS)
+    assert np.array_equal(ref[1], a7[1]) and np.array_equal(ref[0].view(np.uint32), a7[0].view(np.uint32))
+    assert a7[2]["rtic_tested"] < ref[2]["rtic_tested"]
+    oref = oracle.cast(ems, tris, want_t64=True, want_allhits=True)
+    check(ems, tris, a7[0], a7[1], ref=oref)
+    _check_all_hits(ems, tris, a7[3].debug_all_hits().cpu().numpy(), oref)
+
+
+def test_a7_c1_and_fixtures():
+    """A7 on C1 (ground under the sensor, zenith ceiling, seam triangle, grazing triangle)."""
+    ems = [sg.c1_emitter()]
+    tris = sg.c1_scene()
+    a7 = run(ems, tris, small_max=1, flags=G.DEBUG_COUNT_ALL_HITS)
+    oref = oracle.cast(ems, tris, want_t64=True, want_allhits=True)
+    check(ems, tris, a7[0], a7[1], ref=oref)
+    _check_all_hits(ems, tris, a7[3].debug_all_hits().cpu().numpy(), oref)
