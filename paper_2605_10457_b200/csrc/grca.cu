@@ -29,6 +29,16 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr unsigned long long kMiss = 0x7F800000FFFFFFFFull;
 constexpr int K2_THREADS = 256;
 constexpr int K4_THREADS = 256;
+// fused refine+small: 512 threads x 2 blocks (64 registers) measured best on B200 (occupancy vs spills)
+#ifndef KF_THREADS
+#define KF_THREADS 512
+#endif
+#ifndef KF_MINB
+#define KF_MINB 2
+#endif
+#ifndef K2_MINB
+#define K2_MINB 1
+#endif
 constexpr int kMaxEmitters = 255;
 constexpr int kMaxSin = 4096;
 constexpr int kLutMaxEm = 16;   // channel LUTs staged in smem for up to 16 emitters
@@ -202,7 +212,7 @@ struct EmLitePack {
 };
 
 template <int NE>
-__global__ void __launch_bounds__(K2_THREADS) k_cull_fixed(const KParams P, const EmLitePack EL) {
+__global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const KParams P, const EmLitePack EL) {
     extern __shared__ __align__(16) unsigned char smem[];
     float *sSin = reinterpret_cast<float *>(smem);
     unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
@@ -521,11 +531,11 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const KParams P) {
 // (cull_pair), certified setup of small rectangles into shared-memory float4 slots, then the
 // warp expands all items of its small rectangles with a prefix scan (A5) and tests them 32 at a
 // time (A6).  Large rectangles go to the large list (K3/K4).  One vertex fetch per survivor.
-__global__ void __launch_bounds__(K2_THREADS) k_refine_small(const KParams P) {
+__global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4 *sSlot = reinterpret_cast<float4 *>(smem);   // [warp][6][32]
-    int *sExcl = reinterpret_cast<int *>(sSlot + (K2_THREADS / 32) * 6 * 32);   // [warp][32]
-    EmDev *sE = reinterpret_cast<EmDev *>(sExcl + K2_THREADS);
+    int *sExcl = reinterpret_cast<int *>(sSlot + (KF_THREADS / 32) * 6 * 32);   // [warp][32]
+    EmDev *sE = reinterpret_cast<EmDev *>(sExcl + KF_THREADS);
     float *sSin = reinterpret_cast<float *>(sE + P.n_em);
     unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
     __shared__ unsigned long long acc[ST_COUNT];
@@ -1072,7 +1082,7 @@ static size_t k2b_smem_bytes(int n_em, int n_sin, bool lut) {
 }
 static size_t k4s_smem_bytes(int n_em) { return sizeof(EmDev) * n_em + sizeof(float) * NF * K2_THREADS; }
 static size_t kfused_smem_bytes(int n_em, int n_sin, bool lut) {
-    return sizeof(float4) * (K2_THREADS / 32) * 6 * 32 + sizeof(int) * K2_THREADS + sizeof(EmDev) * n_em +
+    return sizeof(float4) * (KF_THREADS / 32) * 6 * 32 + sizeof(int) * KF_THREADS + sizeof(EmDev) * n_em +
            sizeof(float) * ((n_sin + 3) & ~3) + (lut ? (size_t)n_em * kLutBins : 0);
 }
 
@@ -1363,7 +1373,7 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4s, k_small, K2_THREADS, h->k4s_smem));
     h->k4s_blocks_per_sm = std::max(1, b4s);
     int bf = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_refine_small, K2_THREADS, h->kf_smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_refine_small, KF_THREADS, h->kf_smem));
     h->kf_blocks_per_sm = std::max(1, bf);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_isect, K4_THREADS, sizeof(EmDev) * n_emitters));
     h->k2_blocks_per_sm = std::max(1, b2);
@@ -1433,7 +1443,7 @@ static grca_status launch_packed(grca_t h) {
             k_small<<<(unsigned)grid, K2_THREADS, h->k4s_smem, h->stream>>>(P);
         } else {
             const long long grid = (long long)h->num_sms * h->kf_blocks_per_sm;
-            k_refine_small<<<(unsigned)grid, K2_THREADS, h->kf_smem, h->stream>>>(P);
+            k_refine_small<<<(unsigned)grid, KF_THREADS, h->kf_smem, h->stream>>>(P);
         }
         CK(cudaGetLastError());
     }

@@ -13,7 +13,7 @@ import os
 from typing import Optional, Sequence
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgrca.so")
+LIB_PATH = os.environ.get("GRCA_LIB") or os.path.join(_PKG, "libgrca.so")   # GRCA_LIB: A/B builds only
 
 GRCA_OK, GRCA_E_INVALID, GRCA_E_STATE, GRCA_E_CAPACITY, GRCA_E_CUDA, GRCA_E_NCCL, GRCA_E_OOM = range(7)
 FACES_TWO_SIDED, FACES_KEEP_POS, FACES_KEEP_NEG = 0, 1, 2
