@@ -27,7 +27,7 @@ namespace grca {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr unsigned long long kMiss = 0x7F800000FFFFFFFFull;
-constexpr int K2_THREADS = 256;
+constexpr int K2_THREADS = 256;   // K2 tile = 256 triangles
 constexpr int K4_THREADS = 256;
 // fused refine+small: 512 threads x 2 blocks (64 registers) measured best on B200 (occupancy vs spills)
 #ifndef KF_THREADS
@@ -69,11 +69,9 @@ struct KParams {
     long long n_rays;
     const EmLite *lite;
     const unsigned char *lut;    // NULL -> binary search
-    unsigned short *surv;        // per tile: K2_THREADS * n_em entries (local_tri << 8 | emitter)
-    int *tile_count;
-    unsigned long long *desc;    // per survivor entry: small-rectangle descriptor (0 = none)
-    unsigned *rounds;            // work units of 32 survivor entries: tile << 6 | round
-    unsigned *n_rounds;
+    unsigned long long *surv;    // dense K2 survivor list: tri << 8 | emitter
+    unsigned *n_surv;
+    unsigned long long *desc;    // split path: per survivor, small-rectangle descriptor (0 = none)
 };
 
 // slot fields (SoA per warp in shared memory) for the inline small-pair expansion
@@ -125,6 +123,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
     unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
     unsigned short *sQ = reinterpret_cast<unsigned short *>(sLut + (P.lut ? ((P.n_em * kLutBins + 15) & ~15) : 0));
     __shared__ int qn;
+    __shared__ unsigned qbase;
     __shared__ unsigned long long acc[ST_COUNT];
     {
         const int nw = P.n_em * (int)(sizeof(EmLite) / 4);
@@ -182,15 +181,11 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
         }
         __syncthreads();
         const int n = qn;
-        unsigned short *dst = P.surv + tile * (long long)K2_THREADS * P.n_em;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = sQ[i];
-        if (threadIdx.x == 0) {
-            P.tile_count[tile] = n;
-            const int r = (n + 31) >> 5;   // work units of 32 survivors for K2b / K4s
-            if (r) {
-                const unsigned base = atomicAdd(P.n_rounds, (unsigned)r);
-                for (int k = 0; k < r; ++k) P.rounds[base + k] = ((unsigned)tile << 6) | (unsigned)k;
-            }
+        if (threadIdx.x == 0) qbase = n ? atomicAdd(P.n_surv, (unsigned)n) : 0u;   // one atomic per tile
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const unsigned q = sQ[i];
+            P.surv[qbase + i] = ((unsigned long long)(tile * K2_THREADS + (q >> 8)) << 8) | (q & 255u);
         }
         __syncthreads();
     }
@@ -217,6 +212,7 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const KParam
     float *sSin = reinterpret_cast<float *>(smem);
     unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
     __shared__ int wsum[K2_THREADS / 32];
+    __shared__ unsigned qbase;
     __shared__ unsigned long long acc[ST_COUNT];
     for (int i = threadIdx.x; i < P.n_sin; i += blockDim.x) sSin[i] = P.sin[i];
     if (P.lut)
@@ -272,21 +268,15 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const KParam
             wbase += (w < wib) ? x : 0;
             total += x;
         }
-        unsigned short *dst = P.surv + tile * (long long)K2_THREADS * P.n_em + wbase + incl - cntk;
+        if (threadIdx.x == 0) qbase = total ? atomicAdd(P.n_surv, (unsigned)total) : 0u;   // one atomic per tile
+        __syncthreads();
+        unsigned long long *dst = P.surv + qbase + wbase + incl - cntk;
         while (keep) {
             const int e = __ffs(keep) - 1;
             keep &= keep - 1u;
-            *dst++ = (unsigned short)((threadIdx.x << 8) | e);
+            *dst++ = ((unsigned long long)t << 8) | (unsigned)e;
         }
-        if (threadIdx.x == 0) {
-            P.tile_count[tile] = total;
-            const int r = (total + 31) >> 5;   // work units of 32 survivors for K2b / K4s
-            if (r) {
-                const unsigned base = atomicAdd(P.n_rounds, (unsigned)r);
-                for (int k = 0; k < r; ++k) P.rounds[base + k] = ((unsigned)tile << 6) | (unsigned)k;
-            }
-        }
-        __syncthreads();   // wsum reuse
+        __syncthreads();   // wsum / qbase reuse
     }
     unsigned long long cnt[ST_COUNT];
 #pragma unroll
@@ -333,16 +323,14 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
     unsigned setup64 = 0;
     // work = rounds of 32 survivor entries, interleaved over all warps (balanced: no tile tails)
-    const unsigned nr = *P.n_rounds;
+    const unsigned ns = *P.n_surv;
+    const unsigned nr = (ns + 31) >> 5;   // dense rounds of 32 survivors
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
     for (unsigned w = wid; w < nr; w += nwarps) {
-        const unsigned ru = P.rounds[w];
-        const long long tile = ru >> 6;
-        const int n = P.tile_count[tile];
-        const long long region = tile * (long long)K2_THREADS * P.n_em;
+        const int n = (int)ns;
         {
-            const int idx = (int)(ru & 63u) * 32 + lane;
+            const int idx = (int)(w * 32u) + lane;
             const bool act = idx < n;
             int e = 0, st = -1;
             long long t = 0;
@@ -350,9 +338,9 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
             unsigned long long desc = 0ull;
             bool large = false;
             if (act) {
-                const unsigned ent = P.surv[region + idx];
-                e = ent & 255;
-                t = tile * K2_THREADS + (ent >> 8);
+                const unsigned long long ent = P.surv[idx];
+                e = (int)(ent & 255u);
+                t = (long long)(ent >> 8);
                 f3 v[3];
                 load_tri(P.tri, t, v);
                 st = cull_pair(v, sE[e], sSin + sE[e].sin_base, P.lut ? sLut + e * kLutBins : nullptr,
@@ -367,7 +355,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
                 else if (st == CULL_CHANNEL) cnt[ST_CHANNEL]++;
                 else if (st == CULL_AZIMUTH) cnt[ST_AZIMUTH]++;
                 else cnt[ST_DEGEN]++;
-                P.desc[region + idx] = desc;
+                P.desc[idx] = desc;
             }
             const unsigned lm = __ballot_sync(FULL, large);
             if (lm) {
@@ -418,24 +406,22 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const KParams P) {
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
     unsigned setup64 = 0;
-    const unsigned nr = *P.n_rounds;
+    const unsigned ns = *P.n_surv;
+    const unsigned nr = (ns + 31) >> 5;   // dense rounds of 32 survivors
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
     for (unsigned w = wid; w < nr; w += nwarps) {
-        const unsigned ru = P.rounds[w];
-        const long long tile = ru >> 6;
-        const int n = P.tile_count[tile];
-        const long long region = tile * (long long)K2_THREADS * P.n_em;
+        const int n = (int)ns;
         {
-            const int idx = (int)(ru & 63u) * 32 + lane;
+            const int idx = (int)(w * 32u) + lane;
             int my = 0;
             if (idx < n) {
-                const unsigned long long desc = P.desc[region + idx];
+                const unsigned long long desc = P.desc[idx];
                 const int nrows = (int)((desc >> 16) & 1023u);
                 if (nrows) {
-                    const unsigned ent = P.surv[region + idx];
-                    const int e = ent & 255;
-                    const long long t = tile * K2_THREADS + (ent >> 8);
+                    const unsigned long long ent = P.surv[idx];
+                    const int e = (int)(ent & 255u);
+                    const long long t = (long long)(ent >> 8);
                     const EmDev &E = sE[e];
                     f3 v[3];
                     load_tri(P.tri, t, v);
@@ -557,23 +543,21 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
     unsigned setup64 = 0;
-    const unsigned nr = *P.n_rounds;
+    const unsigned ns = *P.n_surv;
+    const unsigned nr = (ns + 31) >> 5;   // dense rounds of 32 survivors
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
     for (unsigned w = wid; w < nr; w += nwarps) {
-        const unsigned ru = P.rounds[w];
-        const long long tile = ru >> 6;
-        const int n = P.tile_count[tile];
-        const long long region = tile * (long long)K2_THREADS * P.n_em;
-        const int idx = (int)(ru & 63u) * 32 + lane;
+        const int n = (int)ns;
+        const int idx = (int)(w * 32u) + lane;
         int my = 0, e = 0;
         long long t = 0;
         Rect R;
         bool large = false;
         if (idx < n) {
-            const unsigned ent = P.surv[region + idx];
-            e = ent & 255;
-            t = tile * K2_THREADS + (ent >> 8);
+            const unsigned long long ent = P.surv[idx];
+            e = (int)(ent & 255u);
+            t = (long long)(ent >> 8);
             f3 v[3];
             load_tri(P.tri, t, v);
             const EmDev &E = sE[e];
@@ -950,10 +934,8 @@ struct grca_ctx {
     EmLite *d_lite = nullptr;
     unsigned char *d_lut = nullptr;    // n_em * kLutBins when n_em <= kLutMaxEm and all gamma <= 255
     bool use_lut = false;
-    unsigned short *d_surv = nullptr;  // K2 survivors, per tile K2_THREADS * n_em entries
-    int *d_tile_count = nullptr;
+    unsigned long long *d_surv = nullptr;   // dense K2 survivor list (capacity tiles * 256 * n_em)
     unsigned long long *d_desc = nullptr;
-    unsigned *d_rounds = nullptr;
     long long surv_cap_tiles = 0;
     int surv_n_em = 0;
     EmLitePack lite_pack{};
@@ -1012,9 +994,7 @@ void free_all(grca_t h) {
     cudaFree(h->d_lite);
     cudaFree(h->d_lut);
     cudaFree(h->d_surv);
-    cudaFree(h->d_tile_count);
     cudaFree(h->d_desc);
-    cudaFree(h->d_rounds);
     cudaFree(h->d_large);
     cudaFree(h->d_chunks);
     cudaFree(h->d_ctrl);
@@ -1041,8 +1021,7 @@ KParams params(grca_t h) {
     P.cap_large = h->cap_large;
     P.chunks = h->d_chunks;
     P.n_chunks = h->d_ctrl + 1;
-    P.n_rounds = h->d_ctrl + 2;
-    P.rounds = h->d_rounds;
+    P.n_surv = h->d_ctrl + 2;
     P.cap_chunks = h->cap_chunks;
     P.stats = h->d_stats;
     P.faces = h->ci.faces;
@@ -1054,7 +1033,6 @@ KParams params(grca_t h) {
     P.lite = h->d_lite;
     P.lut = h->use_lut ? h->d_lut : nullptr;
     P.surv = h->d_surv;
-    P.tile_count = h->d_tile_count;
     P.desc = h->d_desc;
     return P;
 }
@@ -1326,17 +1304,11 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     const long long tiles = (std::max<long long>(1, h->ci.max_triangles) + K2_THREADS - 1) / K2_THREADS;
     if (!h->d_surv || h->surv_n_em < n_emitters) {
         cudaFree(h->d_surv);
-        cudaFree(h->d_tile_count);
         cudaFree(h->d_desc);
-        cudaFree(h->d_rounds);
-        h->d_rounds = nullptr;
         h->d_surv = nullptr;
-        h->d_tile_count = nullptr;
         h->d_desc = nullptr;
-        if (cudaMalloc((void **)&h->d_surv, sizeof(unsigned short) * tiles * K2_THREADS * n_emitters) != cudaSuccess ||
-            cudaMalloc((void **)&h->d_tile_count, sizeof(int) * tiles) != cudaSuccess ||
-            cudaMalloc((void **)&h->d_desc, sizeof(unsigned long long) * tiles * K2_THREADS * n_emitters) != cudaSuccess ||
-            cudaMalloc((void **)&h->d_rounds, sizeof(unsigned) * tiles * ((K2_THREADS * n_emitters + 31) / 32)) != cudaSuccess) {
+        if (cudaMalloc((void **)&h->d_surv, sizeof(unsigned long long) * tiles * K2_THREADS * n_emitters) != cudaSuccess ||
+            cudaMalloc((void **)&h->d_desc, sizeof(unsigned long long) * tiles * K2_THREADS * n_emitters) != cudaSuccess) {
             cudaGetLastError();
             h->surv_n_em = 0;
             return fail(h, GRCA_E_OOM, "survivor buffer allocation failed");
