@@ -236,25 +236,13 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const KParam
                              (v[0].z - v[2].z) * (v[0].z - v[2].z);
             const float m2 = fmaxf(l0, fmaxf(l1, l2));
             const float emax = m2 * rsqrtf(m2) * (1.f + 1e-5f);   // triangle diameter (0 if degenerate)
-            // bounding sphere: centroid and max vertex distance (emitter-independent)
-            const f3 cen = {(v[0].x + v[1].x + v[2].x) * (1.f / 3.f), (v[0].y + v[1].y + v[2].y) * (1.f / 3.f),
-                            (v[0].z + v[1].z + v[2].z) * (1.f / 3.f)};
-            float r2m = 0.f;
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const float dx = v[k].x - cen.x, dy = v[k].y - cen.y, dz = v[k].z - cen.z;
-                r2m = fmaxf(r2m, dx * dx + dy * dy + dz * dz);
-            }
-            const float rho = (r2m * rsqrtf(r2m) + 1e-6f * fabsf(cen.x) + 1e-6f * fabsf(cen.y) + 1e-6f * fabsf(cen.z)) *
-                              (1.f + 1e-5f);
             c_pairs += NE;
             unsigned chan = 0u;
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
-                const float *sT = sSin + EL.e[e].sin_base;
-                const unsigned char *lt = P.lut ? sLut + e * kLutBins : nullptr;
-                int st = P.nocull ? CULL_KEEP : sphere_cull(cen, rho, EL.e[e], sT, lt);
-                if (st == CULL_KEEP && !P.nocull) st = quick_cull(v, emax, EL.e[e], sT, lt);
+                const int st = P.nocull ? CULL_KEEP
+                                        : quick_cull(v, emax, EL.e[e], sSin + EL.e[e].sin_base,
+                                                     P.lut ? sLut + e * kLutBins : nullptr);
                 keep |= (st == CULL_KEEP ? 1u : 0u) << e;
                 rng |= (st == CULL_RANGE ? 1u : 0u) << e;
                 chan += (st == CULL_CHANNEL);

@@ -361,49 +361,6 @@ __device__ __forceinline__ long long rect_items(const Rect &R, const EmDev &E) {
     return (long long)(plo + phi) * E.chi + (rows - plo - phi) * R.r_len;
 }
 
-// K2 sphere pre-test (cheaper first stage of quick_cull): every point p of T lies within rho of
-// the centroid c, so with d = |c - o| > rho the direction of p - o is within asin(rho / d) of that
-// of c, and sin(elevation) is 1-Lipschitz in angle: |s_p - s_c| <= asin(rho / d) <= 1.1 rho / d
-// for rho / d <= 0.45.  Returns CULL_CHANNEL / CULL_RANGE when the whole sphere is culled, else
-// CULL_KEEP (-> vertex test).  Same LUT probe as quick_cull.
-__device__ __forceinline__ int sphere_cull(f3 c, float rho, const EmLite &L, const float *sinT, const unsigned char *lut) {
-    const f3 a = {c.x - L.o[0], c.y - L.o[1], c.z - L.o[2]};
-    const float w2 = a.x * a.x + a.y * a.y + a.z * a.z;
-    const float xu = L.Au[0] * a.x + L.Au[1] * a.y + L.Au[2] * a.z;
-    const float iw = rsqrtf(w2);
-    float sc;
-    if (L.ortho) {
-        sc = xu * iw;
-    } else {
-        const float x2 = L.G[0] * a.x * a.x + L.G[1] * a.y * a.y + L.G[2] * a.z * a.z +
-                         2.f * (L.G[3] * a.x * a.y + L.G[4] * a.x * a.z + L.G[5] * a.y * a.z);
-        sc = xu * rsqrtf(x2);
-    }
-    const float d = w2 * iw;
-    if (d - rho > L.lim) return CULL_RANGE;
-    const float rr = rho * iw;
-    if (!(rr <= 0.45f)) return CULL_KEEP;
-    const float half = 1.1f * rr + L.pad0;
-    const float lo = sc - half, hi = sc + half;
-    if (!(hi < 1.f && lo > -1.f)) return CULL_KEEP;   // the band reaches a pole
-    float vj;
-    if (lut) {
-        int b = (int)((lo + 1.f) * (0.5f * kLutBins));
-        b = min(max(b, 0), kLutBins - 1);
-        int j = lut[b];
-        const float v0 = sinT[j], v1 = sinT[j + 1];
-        vj = v0 >= lo ? v0 : v1;
-        if (v1 < lo) {
-            j += 2;
-            while (sinT[j] < lo) ++j;
-            vj = sinT[j];
-        }
-    } else {
-        vj = sinT[lower_bound_f(sinT, L.gamma, lo)];
-    }
-    return vj <= hi ? CULL_KEEP : CULL_CHANNEL;
-}
-
 // K2 phase A: cheap conservative elevation pre-test of one (triangle, emitter) pair.
 // Bounds: every point of T is within emax (= T's diameter) of each vertex,
 // so |p - o| >= r_lb = max_k |a_k| - emax; the angle L subtended by any chord of T is <= q =
