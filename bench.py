@@ -201,7 +201,7 @@ def ncu_traffic():
     return out, os.path.basename(files[-1])
 
 
-def kernel_rooflines(kernel_ms, st, n_rays, n_tri, n_em, clk, device):
+def kernel_rooflines(kernel_ms, st, n_rays, n_tri, n_em, clk, device, split=False):
     import torch
 
     pk = peaks()
@@ -214,8 +214,10 @@ def kernel_rooflines(kernel_ms, st, n_rays, n_tri, n_em, clk, device):
     work = {
         "K0_init": ("hbm", 8 * n_rays),
         "K2_cull": ("alu", ALU_PER_PAIR_K2 * st["pairs"]),
-        "K2b_refine": ("alu", ALU_PER_SURV_K2B * st["prefilter_survivors"]),
-        "K4s_small": ("alu", ALU_PER_ITEM * small_items + ALU_PER_SETUP * st["small_pairs"]),
+        "K2b_refine": ("alu", ALU_PER_SURV_K2B * st["prefilter_survivors"] if split else 0),
+        # fused default: the refine+small kernel also does K2b's per-survivor bounds
+        "K4s_small": ("alu", ALU_PER_ITEM * small_items + ALU_PER_SETUP * st["small_pairs"] +
+                      (0 if split else ALU_PER_SURV_K2B * st["prefilter_survivors"])),
         "K3_bin": ("hbm", 32 * max(1, st["large_pairs"])),
         "K4_large": ("alu", ALU_PER_ITEM * large_items + ALU_PER_SETUP * st["chunks"]),
         "K5_unpack": ("hbm", 16 * n_rays),
@@ -402,7 +404,7 @@ def main():
 
     # ---- per-kernel roofline (per-kernel CUDA events on the launch stream, last <= 64 steps)
     kernel_ms = {n: kms[i] for i, n in enumerate(KERNELS)}
-    roof = kernel_rooflines(kernel_ms, stats, n_rays, scene.n_tri, len(ems), clk, device)
+    roof = kernel_rooflines(kernel_ms, stats, n_rays, scene.n_tri, len(ems), clk, device, split=args.split_refine)
     dom = max(roof, key=lambda n: kernel_ms[n])
     roofline = dict(roof[dom])
     roofline["kernel"] = dom
