@@ -83,12 +83,12 @@ enum SlotF {
 __device__ __forceinline__ f3 em_o(const EmDev &E) { return {E.o[0], E.o[1], E.o[2]}; }
 
 __device__ __forceinline__ void block_flush(unsigned long long *acc_smem, unsigned long long *stats,
-                                            const unsigned long long *mine) {
+                                            const unsigned *mine) {
     // warp reduce then smem then one atomic per block per counter
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) {
-        unsigned long long v = mine[c];
+        unsigned long long v = mine[c];   // per-thread u32 counts, summed in 64 bits
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
         if (lane == 0 && v) atomicAdd(acc_smem + c, v);
@@ -136,9 +136,9 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
         if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
     }
     const int lane = threadIdx.x & 31;
-    unsigned long long cnt[ST_COUNT];
+    unsigned cnt[ST_COUNT];
 #pragma unroll
-    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
+    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0u;
     unsigned c_pairs = 0, c_range = 0, c_chan = 0, c_surv = 0;
     const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -278,9 +278,9 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const KParam
         }
         __syncthreads();   // wsum / qbase reuse
     }
-    unsigned long long cnt[ST_COUNT];
+    unsigned cnt[ST_COUNT];
 #pragma unroll
-    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
+    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0u;
     cnt[ST_PAIRS] = c_pairs;
     cnt[ST_RANGE] = c_range;
     cnt[ST_CHANNEL] = c_chan;
@@ -298,7 +298,7 @@ __device__ __forceinline__ unsigned long long pack_small(int c_from, int nrows, 
 }
 
 __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev &E, long long t, int row0, int nrows, int lo,
-                                      int len, unsigned long long *cnt, unsigned &setup64);
+                                                   int len);
 
 __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -318,9 +318,9 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
     }
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    unsigned long long cnt[ST_COUNT];
+    unsigned cnt[ST_COUNT];
 #pragma unroll
-    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
+    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0u;
     unsigned setup64 = 0;
     // work = rounds of 32 survivor entries, interleaved over all warps (balanced: no tile tails)
     const unsigned ns = *P.n_surv;
@@ -372,8 +372,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
                     } else {   // capacity fallback: intersect here (slow, never dropped)
                         cnt[ST_OVF_LARGE]++;
                         if (R.pole_rows) { R.r_lo = 0; R.r_len = sE[e].chi; }
-                        intersect_rect_serial(P, sE[e], t, R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len, cnt,
-                                              setup64);
+                        intersect_rect_serial(P, sE[e], t, R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len);
                     }
                 }
             }
@@ -402,9 +401,9 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const KParams P) {
     __syncthreads();
     const int lane = threadIdx.x & 31;
     float *slot = sSlot + (threadIdx.x >> 5) * (NF * 32);
-    unsigned long long cnt[ST_COUNT];
+    unsigned cnt[ST_COUNT];
 #pragma unroll
-    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
+    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0u;
     unsigned setup64 = 0;
     const unsigned ns = *P.n_surv;
     const unsigned nr = (ns + 31) >> 5;   // dense rounds of 32 survivors
@@ -539,18 +538,20 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     float4 *slot = sSlot + wib * 6 * 32;
     int *excl = sExcl + wib * 32;
-    unsigned long long cnt[ST_COUNT];
-#pragma unroll
-    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
-    unsigned setup64 = 0;
+    unsigned setup64 = 0, nhits = 0, nfp64 = 0;
+    // stats: per-lane category codes, counted warp-aggregated into shared memory at convergent
+    // points (no per-thread counter registers)
+    enum { C_NONE = 0, C_SMALL, C_LARGE, C_OVF, C_RANGE, C_CHAN, C_AZI, C_DEGEN };
     const unsigned ns = *P.n_surv;
     const unsigned nr = (ns + 31) >> 5;   // dense rounds of 32 survivors
-    const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
-    for (unsigned w = wid; w < nr; w += nwarps) {
+    // dynamic round fetching (one global atomic per warp per round): no tail imbalance
+    unsigned w = 0;
+    if (lane == 0) w = atomicAdd(P.n_surv + 2, 1u);
+    w = __shfl_sync(FULL, w, 0);
+    for (; w < nr;) {
         const int n = (int)ns;
         const int idx = (int)(w * 32u) + lane;
-        int my = 0, e = 0;
+        int my = 0, e = 0, cat = C_NONE;
         long long t = 0;
         Rect R;
         bool large = false;
@@ -564,14 +565,12 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
             const int st = cull_pair(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
                                      P.nocull != 0, R);
             if (st == CULL_KEEP) {
-                cnt[ST_SURV]++;
                 const long long items = rect_items(R, E);
                 if (items <= P.small_max && !R.pole_rows) {
                     Setup S;
                     if (make_setup(v, em_o(E), P.faces, S, setup64)) {
                         my = (int)items;
-                        cnt[ST_SMALL]++;
-                        cnt[ST_ITEMS_SMALL] += (unsigned long long)my;
+                        cat = C_SMALL;
                         slot[0 * 32 + lane] = make_float4(S.n0.x, S.n0.y, S.n0.z, S.B0);
                         slot[1 * 32 + lane] = make_float4(S.n1.x, S.n1.y, S.n1.z, S.B1);
                         slot[2 * 32 + lane] = make_float4(S.n2.x, S.n2.y, S.n2.z, S.B2);
@@ -581,15 +580,12 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
                         slot[5 * 32 + lane] = make_float4(__int_as_float(R.c_from), __int_as_float(R.r_lo),
                                                           __int_as_float(R.r_len), 1.f / (float)R.r_len);
                     } else {
-                        cnt[ST_DEGEN]++;
+                        cat = C_DEGEN;
                     }
                 } else {
                     large = true;
                 }
-            } else if (st == CULL_RANGE) cnt[ST_RANGE]++;
-            else if (st == CULL_CHANNEL) cnt[ST_CHANNEL]++;
-            else if (st == CULL_AZIMUTH) cnt[ST_AZIMUTH]++;
-            else cnt[ST_DEGEN]++;
+            } else cat = st == CULL_RANGE ? C_RANGE : st == CULL_CHANNEL ? C_CHAN : st == CULL_AZIMUTH ? C_AZI : C_DEGEN;
         }
         const unsigned lm = __ballot_sync(FULL, large);
         if (lm) {
@@ -602,12 +598,30 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
                 if (pos < P.cap_large) {
                     P.large[pos] = make_int4((int)t, e | (R.c_from << 8), R.c_to,
                                              (int)((unsigned)R.r_lo | ((unsigned)R.r_len << 16)));
-                    cnt[ST_LARGE]++;
+                    cat = C_LARGE;
                 } else {   // capacity fallback: intersect here (slow, never dropped)
-                    cnt[ST_OVF_LARGE]++;
+                    cat = C_OVF;
                     if (R.pole_rows) { R.r_lo = 0; R.r_len = sE[e].chi; }
-                    intersect_rect_serial(P, sE[e], t, R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len, cnt, setup64);
+                    intersect_rect_serial(P, sE[e], t, R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len);
                 }
+            }
+        }
+        {   // warp-aggregated stats of this round (lane 0 -> shared memory)
+            const unsigned ms = __ballot_sync(FULL, cat == C_SMALL), ml = __ballot_sync(FULL, cat == C_LARGE),
+                           mo = __ballot_sync(FULL, cat == C_OVF), mr = __ballot_sync(FULL, cat == C_RANGE),
+                           mc = __ballot_sync(FULL, cat == C_CHAN), ma = __ballot_sync(FULL, cat == C_AZI),
+                           md = __ballot_sync(FULL, cat == C_DEGEN);
+            const unsigned items = __reduce_add_sync(FULL, (unsigned)my);
+            if (lane == 0) {
+                if (ms | ml | mo) atomicAdd(acc + ST_SURV, (unsigned long long)(__popc(ms) + __popc(ml) + __popc(mo)));
+                if (ms) atomicAdd(acc + ST_SMALL, (unsigned long long)__popc(ms));
+                if (items) atomicAdd(acc + ST_ITEMS_SMALL, (unsigned long long)items);
+                if (ml) atomicAdd(acc + ST_LARGE, (unsigned long long)__popc(ml));
+                if (mo) atomicAdd(acc + ST_OVF_LARGE, (unsigned long long)__popc(mo));
+                if (mr) atomicAdd(acc + ST_RANGE, (unsigned long long)__popc(mr));
+                if (mc) atomicAdd(acc + ST_CHANNEL, (unsigned long long)__popc(mc));
+                if (ma) atomicAdd(acc + ST_AZIMUTH, (unsigned long long)__popc(ma));
+                if (md) atomicAdd(acc + ST_DEGEN, (unsigned long long)__popc(md));
             }
         }
         // A5: warp-level prefix-scan work expansion
@@ -671,21 +685,31 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
                 float th = 0.f;
                 int r = P.force64 ? 2 : test_fast(dv[u], Q, EO.dmax_lo, EO.dmax_hi, th);
                 if (r == 2) {
-                    cnt[ST_FP64]++;
+                    ++nfp64;
                     f3 wv[3];
                     load_tri(P.tri, (long long)__float_as_int(r4.z), wv);
                     r = test_exact(wv, em_o(EO), dv[u], EO.dmax, P.faces, th);
                 }
                 if (r == 1) {
-                    cnt[ST_HITS]++;
+                    ++nhits;
                     record_hit(P.hits, P.allhits, gv[u], th, __float_as_uint(r4.y));
                 }
             }
         }
         __syncwarp();
+        if (lane == 0) w = atomicAdd(P.n_surv + 2, 1u);
+        w = __shfl_sync(FULL, w, 0);
     }
-    cnt[ST_SETUP64] = setup64;
-    block_flush(acc, P.stats, cnt);
+    (void)setup64;
+    {
+        const unsigned h = __reduce_add_sync(FULL, nhits), f = __reduce_add_sync(FULL, nfp64);
+        if (lane == 0) {
+            if (h) atomicAdd(acc + ST_HITS, (unsigned long long)h);
+            if (f) atomicAdd(acc + ST_FP64, (unsigned long long)f);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < ST_COUNT && acc[threadIdx.x]) atomicAdd(P.stats + threadIdx.x, acc[threadIdx.x]);
 }
 
 // ------------------------------------------------------------------ K3 bin --
@@ -717,24 +741,30 @@ __device__ __forceinline__ int group_chunks(const Group &G) {
 }
 
 __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev &E, long long t, int row0, int nrows, int lo,
-                                      int len, unsigned long long *cnt, unsigned &setup64) {
+                                                   int len) {
+    // capacity-overflow fallback (rare): one thread tests a whole rectangle; stats via global atomics
     f3 v[3];
     load_tri(P.tri, t, v);
     const uint32_t id = tri_id(P.tri, t);
     Setup S;
-    if (!make_setup(v, em_o(E), P.faces, S, setup64)) return;
-    for (int r = 0; r < nrows; ++r)
-        for (int c = 0; c < len; ++c) {
-            int i = lo + c;
-            if (i >= E.chi) i -= E.chi;
-            const int g = E.ray_base + (row0 + r) * E.chi + i;
-            const float4 d = __ldg(P.raytab + g);
-            float th;
-            cnt[ST_ITEMS_LARGE]++;
-            int res = P.force64 ? 2 : test_fast(d, S, E.dmax_lo, E.dmax_hi, th);
-            if (res == 2) { cnt[ST_FP64]++; res = test_exact(v, em_o(E), d, E.dmax, P.faces, th); }
-            if (res == 1) { cnt[ST_HITS]++; record_hit(P.hits, P.allhits, g, th, id); }
-        }
+    unsigned setup64 = 0, items = 0, fp64 = 0, hits = 0;
+    if (make_setup(v, em_o(E), P.faces, S, setup64)) {
+        for (int r = 0; r < nrows; ++r)
+            for (int c = 0; c < len; ++c) {
+                int i = lo + c;
+                if (i >= E.chi) i -= E.chi;
+                const int g = E.ray_base + (row0 + r) * E.chi + i;
+                const float4 d = __ldg(P.raytab + g);
+                float th;
+                ++items;
+                int res = P.force64 ? 2 : test_fast(d, S, E.dmax_lo, E.dmax_hi, th);
+                if (res == 2) { ++fp64; res = test_exact(v, em_o(E), d, E.dmax, P.faces, th); }
+                if (res == 1) { ++hits; record_hit(P.hits, P.allhits, g, th, id); }
+            }
+    }
+    atomicAdd(P.stats + ST_ITEMS_LARGE, (unsigned long long)items);
+    atomicAdd(P.stats + ST_FP64, (unsigned long long)fp64);
+    atomicAdd(P.stats + ST_HITS, (unsigned long long)hits);
 }
 
 __global__ void __launch_bounds__(256) k_bin(const KParams P) {
@@ -743,9 +773,9 @@ __global__ void __launch_bounds__(256) k_bin(const KParams P) {
     __shared__ unsigned long long acc[ST_COUNT];
     if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
     __syncthreads();
-    unsigned long long cnt[ST_COUNT];
+    unsigned cnt[ST_COUNT];
 #pragma unroll
-    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
+    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0u;
     unsigned setup64 = 0;
     const int lane = threadIdx.x & 31;
     const long long n = min((long long)*P.n_large, P.cap_large);
@@ -813,7 +843,7 @@ __global__ void __launch_bounds__(256) k_bin(const KParams P) {
             long long pos = (long long)wbase + incl - mych;
             if (pos + mych > P.cap_chunks) {   // capacity fallback: intersect here (never dropped)
                 cnt[ST_OVF_CHUNK]++;
-                intersect_rect_serial(P, E, tri, j, 1, lo, len, cnt, setup64);
+                intersect_rect_serial(P, E, tri, j, 1, lo, len);
                 continue;
             }
             cnt[ST_CHUNKS] += mych;
@@ -842,9 +872,9 @@ __global__ void __launch_bounds__(K4_THREADS) k_isect(const KParams P) {
         if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
     }
     __syncthreads();
-    unsigned long long cnt[ST_COUNT];
+    unsigned cnt[ST_COUNT];
 #pragma unroll
-    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0ull;
+    for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0u;
     unsigned setup64 = 0;
     const int lane = threadIdx.x & 31;
     const long long n = min((long long)*P.n_chunks, P.cap_chunks);
