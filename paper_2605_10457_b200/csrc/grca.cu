@@ -37,7 +37,7 @@ constexpr int K4_THREADS = 256;
 #define KF_MINB 2
 #endif
 #ifndef K2_MINB
-#define K2_MINB 1
+#define K2_MINB 8   // K2 is issue-bound; 8 x 256 threads (32 regs) measured marginally best
 #endif
 constexpr int kMaxEmitters = 255;
 constexpr int kMaxSin = 4096;
