@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
             unsigned long long desc = 0ull;
             bool large = false;
             if (act) {
-                const unsigned long long ent = P.surv[idx];
+                const unsigned long long ent = __ldcs(P.surv + idx);
                 e = (int)(ent & 255u);
                 t = (long long)(ent >> 8);
                 f3 v[3];
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const KParams P) {
                 const unsigned long long desc = P.desc[idx];
                 const int nrows = (int)((desc >> 16) & 1023u);
                 if (nrows) {
-                    const unsigned long long ent = P.surv[idx];
+                    const unsigned long long ent = __ldcs(P.surv + idx);
                     const int e = (int)(ent & 255u);
                     const long long t = (long long)(ent >> 8);
                     const EmDev &E = sE[e];
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
     EmDev *sE = reinterpret_cast<EmDev *>(sExcl + KF_THREADS);
     float *sSin = reinterpret_cast<float *>(sE + P.n_em);
     unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
-    __shared__ unsigned long long acc[ST_COUNT];
+    __shared__ unsigned acc[ST_COUNT];   // 32-bit: native shared atomics (per-block counts < 2^32)
     {
         const int nw = P.n_em * (int)(sizeof(EmDev) / 4);
         const int *src = reinterpret_cast<const int *>(P.em);
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
         for (int i = threadIdx.x; i < P.n_sin; i += blockDim.x) sSin[i] = P.sin[i];
         if (P.lut)
             for (int i = threadIdx.x; i < P.n_em * kLutBins; i += blockDim.x) sLut[i] = P.lut[i];
-        if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
+        if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0u;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -549,6 +549,8 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
     if (lane == 0) w = atomicAdd(P.n_surv + 2, 1u);
     w = __shfl_sync(FULL, w, 0);
     for (; w < nr;) {
+        unsigned wn = 0;
+        if (lane == 0) wn = atomicAdd(P.n_surv + 2, 1u);   // next round, fetched early (latency hidden)
         const int n = (int)ns;
         const int idx = (int)(w * 32u) + lane;
         int my = 0, e = 0, cat = C_NONE;
@@ -556,7 +558,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
         Rect R;
         bool large = false;
         if (idx < n) {
-            const unsigned long long ent = P.surv[idx];
+            const unsigned long long ent = __ldcs(P.surv + idx);
             e = (int)(ent & 255u);
             t = (long long)(ent >> 8);
             f3 v[3];
@@ -613,15 +615,15 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
                            md = __ballot_sync(FULL, cat == C_DEGEN);
             const unsigned items = __reduce_add_sync(FULL, (unsigned)my);
             if (lane == 0) {
-                if (ms | ml | mo) atomicAdd(acc + ST_SURV, (unsigned long long)(__popc(ms) + __popc(ml) + __popc(mo)));
-                if (ms) atomicAdd(acc + ST_SMALL, (unsigned long long)__popc(ms));
-                if (items) atomicAdd(acc + ST_ITEMS_SMALL, (unsigned long long)items);
-                if (ml) atomicAdd(acc + ST_LARGE, (unsigned long long)__popc(ml));
-                if (mo) atomicAdd(acc + ST_OVF_LARGE, (unsigned long long)__popc(mo));
-                if (mr) atomicAdd(acc + ST_RANGE, (unsigned long long)__popc(mr));
-                if (mc) atomicAdd(acc + ST_CHANNEL, (unsigned long long)__popc(mc));
-                if (ma) atomicAdd(acc + ST_AZIMUTH, (unsigned long long)__popc(ma));
-                if (md) atomicAdd(acc + ST_DEGEN, (unsigned long long)__popc(md));
+                if (ms | ml | mo) atomicAdd(acc + ST_SURV, (unsigned)(__popc(ms) + __popc(ml) + __popc(mo)));
+                if (ms) atomicAdd(acc + ST_SMALL, (unsigned)__popc(ms));
+                if (items) atomicAdd(acc + ST_ITEMS_SMALL, (unsigned)items);
+                if (ml) atomicAdd(acc + ST_LARGE, (unsigned)__popc(ml));
+                if (mo) atomicAdd(acc + ST_OVF_LARGE, (unsigned)__popc(mo));
+                if (mr) atomicAdd(acc + ST_RANGE, (unsigned)__popc(mr));
+                if (mc) atomicAdd(acc + ST_CHANNEL, (unsigned)__popc(mc));
+                if (ma) atomicAdd(acc + ST_AZIMUTH, (unsigned)__popc(ma));
+                if (md) atomicAdd(acc + ST_DEGEN, (unsigned)__popc(md));
             }
         }
         // A5: warp-level prefix-scan work expansion
@@ -697,19 +699,18 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
             }
         }
         __syncwarp();
-        if (lane == 0) w = atomicAdd(P.n_surv + 2, 1u);
-        w = __shfl_sync(FULL, w, 0);
+        w = __shfl_sync(FULL, wn, 0);
     }
     (void)setup64;
     {
         const unsigned h = __reduce_add_sync(FULL, nhits), f = __reduce_add_sync(FULL, nfp64);
         if (lane == 0) {
-            if (h) atomicAdd(acc + ST_HITS, (unsigned long long)h);
-            if (f) atomicAdd(acc + ST_FP64, (unsigned long long)f);
+            if (h) atomicAdd(acc + ST_HITS, (unsigned)h);
+            if (f) atomicAdd(acc + ST_FP64, (unsigned)f);
         }
     }
     __syncthreads();
-    if (threadIdx.x < ST_COUNT && acc[threadIdx.x]) atomicAdd(P.stats + threadIdx.x, acc[threadIdx.x]);
+    if (threadIdx.x < ST_COUNT && acc[threadIdx.x]) atomicAdd(P.stats + threadIdx.x, (unsigned long long)acc[threadIdx.x]);
 }
 
 // ------------------------------------------------------------------ K3 bin --
@@ -969,6 +970,7 @@ struct grca_ctx {
     long long surv_cap_tiles = 0;
     int surv_n_em = 0;
     EmLitePack lite_pack{};
+    cudaAccessPolicyWindow l2win{};   // persisting window over ray table + hits (num_bytes 0 = off)
     size_t k2f_smem = 0;
     int4 *d_large = nullptr;
     int4 *d_chunks = nullptr;
@@ -1016,8 +1018,7 @@ grca_status fail(grca_t h, grca_status s, const std::string &m) {
 }
 
 void free_all(grca_t h) {
-    cudaFree(h->d_raytab);
-    cudaFree(h->d_hits);
+    cudaFree(h->d_raytab);   // (d_hits lives in the same allocation)
     cudaFree(h->d_allhits);
     cudaFree(h->d_em);
     cudaFree(h->d_sin);
@@ -1129,8 +1130,10 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     auto alloc = [&](void **p, size_t bytes) {
         if (ok && cudaMalloc(p, bytes) != cudaSuccess) ok = false;
     };
-    alloc((void **)&h->d_raytab, sizeof(float4) * ci->max_rays);
-    alloc((void **)&h->d_hits, sizeof(unsigned long long) * ci->max_rays);
+    // ray table and hit keys in ONE allocation so a single persisting L2 access-policy window
+    // covers both (the gathers of K4s/K4 hit them randomly; the triangle stream must not evict them)
+    alloc((void **)&h->d_raytab, (sizeof(float4) + sizeof(unsigned long long)) * ci->max_rays);
+    if (ok) h->d_hits = reinterpret_cast<unsigned long long *>(h->d_raytab + ci->max_rays);
     if (ci->debug_flags & GRCA_DEBUG_COUNT_ALL_HITS) alloc((void **)&h->d_allhits, sizeof(unsigned) * ci->max_rays);
     alloc((void **)&h->d_em, sizeof(EmDev) * kMaxEmitters);
     alloc((void **)&h->d_sin, sizeof(float) * kMaxSin);
@@ -1162,6 +1165,24 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     cudaFuncSetAttribute(k_refine_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kfused_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_isect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(EmDev) * kMaxEmitters));
+    {   // persisting L2 for the ray table + hits (GRCA_L2_PERSIST=0 in debug_flags disables)
+        int max_persist = 0;
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+        const size_t win = (sizeof(float4) + sizeof(unsigned long long)) * (size_t)ci->max_rays;
+        if (max_persist > 0 && !(ci->debug_flags & GRCA_DEBUG_NO_L2_PERSIST)) {
+            size_t cur = 0;
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            const size_t want = std::min<size_t>(win, (size_t)max_persist);
+            if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+            cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            h->l2win.base_ptr = h->d_raytab;
+            h->l2win.num_bytes = std::min<size_t>(win, (size_t)max_persist * 4);
+            h->l2win.hitRatio = (float)std::min(1.0, (double)cur / (double)h->l2win.num_bytes);
+            h->l2win.hitProp = cudaAccessPropertyPersisting;
+            h->l2win.missProp = cudaAccessPropertyStreaming;
+        }
+        cudaGetLastError();
+    }
     cudaStreamSynchronize(h->stream);
     if (cudaGetLastError() != cudaSuccess) {
         g_create_err = "CUDA setup failed (is this an sm_100a device?)";
@@ -1405,6 +1426,25 @@ grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_v
     return GRCA_OK;
 }
 
+// Launch a gather kernel with the persisting L2 window over the ray table + hits as a per-launch
+// attribute (the caller's stream itself is left untouched).
+static cudaError_t launch_l2(grca_t h, const void *fn, unsigned grid, unsigned block, size_t smem, KParams &P) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = h->stream;
+    cudaLaunchAttribute attr[1];
+    if (h->l2win.num_bytes) {
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow = h->l2win;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    void *args[] = {(void *)&P};
+    return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 static grca_status launch_packed(grca_t h) {
     if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
     if (!h->have_tri) return fail(h, GRCA_E_STATE, "grca_update_triangles has not been called");
@@ -1445,7 +1485,7 @@ static grca_status launch_packed(grca_t h) {
             k_small<<<(unsigned)grid, K2_THREADS, h->k4s_smem, h->stream>>>(P);
         } else {
             const long long grid = (long long)h->num_sms * h->kf_blocks_per_sm;
-            k_refine_small<<<(unsigned)grid, KF_THREADS, h->kf_smem, h->stream>>>(P);
+            CK(launch_l2(h, (const void *)k_refine_small, (unsigned)grid, KF_THREADS, h->kf_smem, P));
         }
         CK(cudaGetLastError());
     }
@@ -1458,7 +1498,7 @@ static grca_status launch_packed(grca_t h) {
     if (prof) CK(cudaEventRecord(h->ev[slot][5], h->stream));
     if (h->n_tri > 0) {   // K4
         const int grid = h->num_sms * h->k4_blocks_per_sm;
-        k_isect<<<grid, K4_THREADS, sizeof(EmDev) * h->n_em, h->stream>>>(P);
+        CK(launch_l2(h, (const void *)k_isect, (unsigned)grid, K4_THREADS, sizeof(EmDev) * h->n_em, P));
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][6], h->stream));

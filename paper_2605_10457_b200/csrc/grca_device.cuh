@@ -117,16 +117,18 @@ struct TriSrc {
     const int32_t *ids;    // NULL -> id_base + local
     int32_t id_base;
 };
+// Streaming (evict-first) loads: the ~1 GB triangle stream must not evict the L2-resident ray
+// table (67 MB at C4) and hit buffer (33.5 MB) that the intersection kernels gather from.
 __device__ __forceinline__ void load_tri(const TriSrc &T, long long t, f3 v[3]) {
     if (T.idx) {
-        const uint32_t i0 = __ldg(T.idx + 3 * t), i1 = __ldg(T.idx + 3 * t + 1), i2 = __ldg(T.idx + 3 * t + 2);
-        v[0] = mk(__ldg(T.v + i0));
-        v[1] = mk(__ldg(T.v + i1));
-        v[2] = mk(__ldg(T.v + i2));
+        const uint32_t i0 = __ldcs(T.idx + 3 * t), i1 = __ldcs(T.idx + 3 * t + 1), i2 = __ldcs(T.idx + 3 * t + 2);
+        v[0] = mk(__ldcs(T.v + i0));
+        v[1] = mk(__ldcs(T.v + i1));
+        v[2] = mk(__ldcs(T.v + i2));
     } else {
-        v[0] = mk(__ldg(T.v + 3 * t));
-        v[1] = mk(__ldg(T.v + 3 * t + 1));
-        v[2] = mk(__ldg(T.v + 3 * t + 2));
+        v[0] = mk(__ldcs(T.v + 3 * t));
+        v[1] = mk(__ldcs(T.v + 3 * t + 1));
+        v[2] = mk(__ldcs(T.v + 3 * t + 2));
     }
 }
 __device__ __forceinline__ uint32_t tri_id(const TriSrc &T, long long t) {
