@@ -255,7 +255,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--small-max", type=int, default=0)
     ap.add_argument("--split-refine", action="store_true", help="K2b and K4s as two kernels (A/B)")
-    ap.add_argument("--no-l2-persist", action="store_true", help="A/B: no persisting L2 window")
+    ap.add_argument("--l2-persist", action="store_true", help="A/B: persisting L2 window (opt-in)")
     ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters"])
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 logic with several ranks on one GPU")
@@ -322,7 +322,7 @@ def main():
     n_rays = sg.n_rays_total(ems)
     n_rays_job = sg.n_rays_total(scene.w["emitters"])
     g = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays, debug_flags=G.PROFILE_KERNELS | (G.DEBUG_SPLIT_REFINE if args.split_refine else 0)
-             | (G.DEBUG_NO_L2_PERSIST if args.no_l2_persist else 0),
+             | (G.L2_PERSIST if args.l2_persist else 0),
              small_max=args.small_max, nranks=world, rank=rank)
     g.set_emitters(ems)
     dist_out = torch.empty(n_rays, dtype=torch.float32, device=device)

@@ -62,9 +62,9 @@ enum {
     GRCA_DEBUG_SPLIT_REFINE = 16u,  /* run K2b (bounds) and K4s (small work) as two kernels instead of
                                        the fused refine+small kernel (A/B measurement, same results) */
     GRCA_DEBUG_NO_REFINE = 32u,     /* K3 keeps whole rectangle rows (no A7 per-channel refinement) */
-    GRCA_DEBUG_NO_L2_PERSIST = 64u  /* do not reserve persisting L2 for the ray table + hit keys
-                                       (by default grca_create raises cudaLimitPersistingL2CacheSize
-                                       to cover them, device-wide, and uses a per-launch window) */
+    GRCA_L2_PERSIST = 64u           /* opt-in: reserve persisting L2 for the ray table + hit keys
+                                       (raises cudaLimitPersistingL2CacheSize device-wide and sets a
+                                       per-launch access-policy window on the gather kernels) */
 };
 
 typedef struct {

@@ -1165,11 +1165,12 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     cudaFuncSetAttribute(k_refine_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kfused_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_isect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(EmDev) * kMaxEmitters));
-    {   // persisting L2 for the ray table + hits (GRCA_L2_PERSIST=0 in debug_flags disables)
+    {   // opt-in persisting L2 window for the ray table + hits (measured: no gain at C4 after the
+        // triangle streams were made evict-first, and K0/K5 lose from the carve-out)
         int max_persist = 0;
         cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, h->device);
         const size_t win = (sizeof(float4) + sizeof(unsigned long long)) * (size_t)ci->max_rays;
-        if (max_persist > 0 && !(ci->debug_flags & GRCA_DEBUG_NO_L2_PERSIST)) {
+        if (max_persist > 0 && (ci->debug_flags & GRCA_L2_PERSIST)) {
             size_t cur = 0;
             cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
             const size_t want = std::min<size_t>(win, (size_t)max_persist);

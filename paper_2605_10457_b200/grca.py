@@ -19,7 +19,7 @@ GRCA_OK, GRCA_E_INVALID, GRCA_E_STATE, GRCA_E_CAPACITY, GRCA_E_CUDA, GRCA_E_NCCL
 FACES_TWO_SIDED, FACES_KEEP_POS, FACES_KEEP_NEG = 0, 1, 2
 DEBUG_COUNT_ALL_HITS, DEBUG_NO_CULL, PROFILE_KERNELS, DEBUG_FORCE_FP64, DEBUG_SPLIT_REFINE, DEBUG_NO_REFINE = (
     1, 2, 4, 8, 16, 32)
-DEBUG_NO_L2_PERSIST = 64
+L2_PERSIST = 64
 
 EXPORTS = [
     "grca_create", "grca_destroy", "grca_set_emitters", "grca_update_triangles", "grca_cast",
