@@ -90,13 +90,15 @@ class ClockSampler:
 class Scene:
     """Resident C-config frames on the GPU (harness: input generation, not the hot path)."""
 
-    def __init__(self, config: str, rank: int, world: int, device, deformation: str = "ND", shard: str = "triangles"):
+    def __init__(self, config: str, rank: int, world: int, device, deformation: str = "ND", shard: str = "triangles",
+                 max_range=-1.0, subdiv: int = 0, car_scale=None):
         import torch
 
         from paper_2605_10457_b200 import dist as D
 
-        w = sg.workload(config, frame=0, deformation=deformation)
+        w = sg.workload(config, frame=0, deformation=deformation, max_range=max_range, subdiv=subdiv)
         self.w = w
+        self.scale = car_scale or sg.WORKLOADS.get(config, (0,) * 7)[6] if config != "C1" else (1.0, 1.0)
         self.emitters = w["emitters"]
         n_static, n_dyn = w["n_static"], w["n_dynamic"]
         self.n_tri_global = n_static + n_dyn
@@ -134,7 +136,8 @@ class Scene:
         v = R (s * v_local) + p.  Computed with torch on the device; returns (3 * n_own_dyn, 3)."""
         import torch
 
-        poses = sg.pose_instances(self.n_cars, self.bbox, int(self.config[1:]), frame)
+        poses = sg.pose_instances(self.n_cars, self.bbox, int(self.config[1:]), frame, scale_lo=self.scale[0],
+                                  scale_hi=self.scale[1])
         R = torch.as_tensor(np.stack([p.rotation for p in poses]), dtype=torch.float32, device=self.device)
         s = torch.as_tensor(np.stack([p.scale for p in poses]), dtype=torch.float32, device=self.device)
         p = torch.as_tensor(np.stack([p.position for p in poses]), dtype=torch.float32, device=self.device)
@@ -254,6 +257,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--small-max", type=int, default=0)
+    ap.add_argument("--max-range", type=float, default=-1.0, help="metres; -1 = config default, 0 = unlimited")
+    ap.add_argument("--subdiv", type=int, default=0, help="C5: car subdivision level (4^L triangles each)")
+    ap.add_argument("--car-scale", default=None, help="lo,hi per-axis car scale (C5 'large triangles' variant)")
     ap.add_argument("--split-refine", action="store_true", help="K2b and K4s as two kernels (A/B)")
     ap.add_argument("--l2-persist", action="store_true", help="A/B: persisting L2 window (opt-in)")
     ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters"])
@@ -317,7 +323,9 @@ def main():
     n_em_total = len(sg.workload(args.config)["emitters"]) if args.config == "C1" else sg.WORKLOADS[args.config][0]
     shard = args.shard if args.shard != "auto" else (D.choose_mode(n_em_total, world) if world > 1 else "triangles")
 
-    scene = Scene(args.config, rank, world, device, args.deformation, shard=shard)
+    car_scale = tuple(float(x) for x in args.car_scale.split(",")) if args.car_scale else None
+    scene = Scene(args.config, rank, world, device, args.deformation, shard=shard,
+                  max_range=(None if args.max_range == 0 else args.max_range), subdiv=args.subdiv, car_scale=car_scale)
     ems = scene.emitters
     n_rays = sg.n_rays_total(ems)
     n_rays_job = sg.n_rays_total(scene.w["emitters"])
@@ -426,6 +434,7 @@ def main():
             "config": {"workload": args.config, "emitters": len(scene.w["emitters"]), "rays_per_frame": n_rays_job,
                        "triangles": scene.n_tri_global, "dynamic_triangles": int(scene.w["n_dynamic"]),
                        "deformation": args.deformation, "max_range_m": float(ems[0].max_range),
+                       "subdiv": args.subdiv, "car_scale": list(scene.scale),
                        "sharding": ("none" if world == 1 else
                                     f"triangles block-interleaved ({D.BLOCK}) + all-reduce(MIN) x {world}"
                                     if shard == "triangles" else f"emitters (n mod P) x {world}, no reduction"),
