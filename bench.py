@@ -256,6 +256,7 @@ def main():
     ap.add_argument("--impl", default="grca", choices=["grca", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-hybrid", action="store_true")
     ap.add_argument("--small-max", type=int, default=0)
     ap.add_argument("--max-range", type=float, default=-1.0, help="metres; -1 = config default, 0 = unlimited")
     ap.add_argument("--subdiv", type=int, default=0, help="C5: car subdivision level (4^L triangles each)")
@@ -412,6 +413,36 @@ def main():
                "h2d_bytes_per_step": int(n_dyn_vals * 16), "d2h_bytes_per_step": int(n_rays * 8), "steps": k_e2e,
                "what": "pinned H2D of this frame's dynamic vertices + grca_cast + D2H of (dist, id) per ray"}
 
+    # ---- hybrid static/dynamic (NEXT-f2; NOT the headline: static triangles cached across frames)
+    hybrid = None
+    if world == 1 and not args.no_hybrid and scene.n_static_local > 0:
+        gh = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays)
+        gh.set_emitters(ems)
+        ns3 = 3 * scene.n_static_local
+        gh.set_static_triangles(scene.frames[0][:ns3], tri_ids=scene.ids[: scene.n_static_local])
+        dyn_ids = scene.ids[scene.n_static_local:]
+
+        def hstep(k):
+            gh.update_triangles(scene.frames[k % N_FRAMES][ns3:], tri_ids=dyn_ids)
+            gh.cast(dist_out, tri_out)
+
+        for k in range(3):
+            hstep(k)
+        barrier()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        kh = max(4, min(args.steps, 100))
+        h0.record(stream)
+        for k in range(kh):
+            hstep(k)
+        h1.record(stream)
+        barrier()
+        hms = h0.elapsed_time(h1) / kh
+        hybrid = {"ms_per_step": hms, "value": n_rays_job / (hms / 1e3), "unit": "rays/s", "steps": kh,
+                  "static_triangles": int(scene.n_static_local), "dynamic_triangles": int(scene.n_tri - scene.n_static_local),
+                  "note": "static triangles cast once into cached per-ray keys (emitters static); each frame culls "
+                          "only the dynamic ones -- exact (min-lattice); context, not the headline (PAPER.md:2077-2085)"}
+        gh.close()
+
     # ---- per-kernel roofline (per-kernel CUDA events on the launch stream, last <= 64 steps)
     kernel_ms = {n: kms[i] for i, n in enumerate(KERNELS)}
     roof = kernel_rooflines(kernel_ms, stats, n_rays, scene.n_tri, len(ems), clk, device, split=args.split_refine)
@@ -450,7 +481,7 @@ def main():
                 "pairs", "range_culled", "channel_culled", "azimuth_culled", "survivors", "small_pairs", "large_pairs",
                 "chunks", "fp64_fallbacks", "hits_recorded", "overflow")},
             "roofline": roofline, "gpu_launches": 7 * args.steps, "clocks": clk,
-            "e2e": e2e, "cpu_baseline": cpu,
+            "e2e": e2e, "cpu_baseline": cpu, "hybrid_static_cache": hybrid,
             "context": "paper (PAPER.md:1758-1762): GRCA_GPU 10.7 ms/frame on RTX 5090 for PP30 Omega=8 "
                        "(3.9e8 rays/s), 1.98x OptiX 9.1; other hardware, not a target",
         }

@@ -144,6 +144,19 @@ grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_v
                                   const uint32_t *d_indices, int64_t n_triangles,
                                   const int32_t *d_tri_ids, int32_t tri_id_base);
 
+/* Hybrid static/dynamic mode (NEXT-f2; "GRCA on dynamic, static BVH on static,
+ * per-ray min merge", here without any BVH): borrow a static triangle set (same conventions as
+ * grca_update_triangles; buffers must stay alive and unmodified while set).  The next cast (and the
+ * first cast after every grca_set_emitters) casts them once into a cached per-ray key buffer; every
+ * cast then starts from those keys instead of MISS and culls only the grca_update_triangles set.
+ * Exact: the per-ray closest hit is a min over triangles.  Ids of both sets share one space.
+ * Errors: as grca_update_triangles. */
+grca_status grca_set_static_triangles(grca_t h, const float *d_vertices, int64_t n_vertices,
+                                      const uint32_t *d_indices, int64_t n_triangles,
+                                      const int32_t *d_tri_ids, int32_t tri_id_base);
+/* Leave hybrid mode (the static set is forgotten; nothing is freed). */
+grca_status grca_clear_static(grca_t h);
+
 /* Cast one frame: K0 init -> K2 cull (+ inline small work) -> K3 bin -> K4 intersect ->
  * K5 unpack, all enqueued on the handle's stream (no allocation, no host sync unless
  * h_stats != NULL).  d_out_dist: device float[n_rays] (+inf on a miss); d_out_tri: device

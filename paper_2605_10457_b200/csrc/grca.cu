@@ -99,15 +99,22 @@ __device__ __forceinline__ void block_flush(unsigned long long *acc_smem, unsign
 
 // ------------------------------------------------------------------- K0 init --
 __global__ void k_init(unsigned long long *hits, unsigned *allhits, long long n, unsigned *ctrl,
-                       unsigned long long *stats) {
+                       unsigned long long *stats, const unsigned long long *src, const unsigned *src_allhits) {
+    // hits = MISS, or the cached static-scene keys (hybrid mode, NEXT-f2)
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
     const long long n2 = n >> 1;
     ulonglong2 *h2 = reinterpret_cast<ulonglong2 *>(hits);
-    for (long long i = tid; i < n2; i += stride) h2[i] = make_ulonglong2(kMiss, kMiss);
-    if (tid == 0 && (n & 1)) hits[n - 1] = kMiss;
+    if (src) {
+        const ulonglong2 *s2 = reinterpret_cast<const ulonglong2 *>(src);
+        for (long long i = tid; i < n2; i += stride) h2[i] = __ldcs(s2 + i);
+        if (tid == 0 && (n & 1)) hits[n - 1] = src[n - 1];
+    } else {
+        for (long long i = tid; i < n2; i += stride) h2[i] = make_ulonglong2(kMiss, kMiss);
+        if (tid == 0 && (n & 1)) hits[n - 1] = kMiss;
+    }
     if (allhits)
-        for (long long i = tid; i < n; i += stride) allhits[i] = 0u;
+        for (long long i = tid; i < n; i += stride) allhits[i] = src_allhits ? src_allhits[i] : 0u;
     if (tid < ST_COUNT) stats[tid] = 0ull;
     if (tid < 8) ctrl[tid] = 0u;
 }
@@ -977,10 +984,16 @@ struct grca_ctx {
     unsigned *d_ctrl = nullptr;
     unsigned long long *d_stats = nullptr;
     long long cap_large = 0, cap_chunks = 0;
-    // triangles
+    // triangles (dynamic / per frame)
     TriSrc tri{};
     long long n_tri = 0;
     bool have_tri = false;
+    // hybrid static/dynamic (NEXT-f2): static triangles cast once into cached keys
+    TriSrc st_tri{};
+    long long st_n = 0;
+    bool st_set = false, st_dirty = false;
+    unsigned long long *d_static_keys = nullptr;
+    unsigned *d_static_allhits = nullptr;
     // profiling ring
     cudaEvent_t ev[kRing][kEv];
     bool ev_ok = false;
@@ -1019,6 +1032,8 @@ grca_status fail(grca_t h, grca_status s, const std::string &m) {
 
 void free_all(grca_t h) {
     cudaFree(h->d_raytab);   // (d_hits lives in the same allocation)
+    cudaFree(h->d_static_keys);
+    cudaFree(h->d_static_allhits);
     cudaFree(h->d_allhits);
     cudaFree(h->d_em);
     cudaFree(h->d_sin);
@@ -1135,6 +1150,8 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     alloc((void **)&h->d_raytab, (sizeof(float4) + sizeof(unsigned long long)) * ci->max_rays);
     if (ok) h->d_hits = reinterpret_cast<unsigned long long *>(h->d_raytab + ci->max_rays);
     if (ci->debug_flags & GRCA_DEBUG_COUNT_ALL_HITS) alloc((void **)&h->d_allhits, sizeof(unsigned) * ci->max_rays);
+    alloc((void **)&h->d_static_keys, sizeof(unsigned long long) * ci->max_rays);
+    if (ci->debug_flags & GRCA_DEBUG_COUNT_ALL_HITS) alloc((void **)&h->d_static_allhits, sizeof(unsigned) * ci->max_rays);
     alloc((void **)&h->d_em, sizeof(EmDev) * kMaxEmitters);
     alloc((void **)&h->d_sin, sizeof(float) * kMaxSin);
     alloc((void **)&h->d_lite, sizeof(EmLite) * kMaxEmitters);
@@ -1375,6 +1392,7 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     if (use_lut) CK(cudaMemcpy(h->d_lut, lut.data(), sizeof(unsigned char) * lut.size(), cudaMemcpyHostToDevice));
     h->use_lut = use_lut;
     h->n_em = n_emitters;
+    h->st_dirty = h->st_set;   // cached static keys depend on the emitters
     h->n_sin = (int)sins.size();
     h->n_rays = offs[n_emitters];
     h->offsets = offs;
@@ -1406,9 +1424,8 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     return GRCA_OK;
 }
 
-grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_vertices, const uint32_t *d_indices,
+static grca_status check_tri_args(grca_t h, const float *d_vertices, int64_t n_vertices, const uint32_t *d_indices,
                                   int64_t n_triangles, const int32_t *d_tri_ids, int32_t tri_id_base) {
-    if (!h) return GRCA_E_INVALID;
     if (n_triangles < 0) return fail(h, GRCA_E_INVALID, "n_triangles < 0");
     if (n_triangles > h->ci.max_triangles) return fail(h, GRCA_E_CAPACITY, "n_triangles exceeds max_triangles");
     if (n_triangles > 0 && !d_vertices) return fail(h, GRCA_E_INVALID, "null vertex buffer");
@@ -1418,12 +1435,43 @@ grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_v
     if (((uintptr_t)d_vertices & 15) != 0) return fail(h, GRCA_E_INVALID, "vertex buffer must be 16-byte aligned");
     if (tri_id_base < 0 || (!d_tri_ids && (long long)tri_id_base + n_triangles > 0x7fffffffll))
         return fail(h, GRCA_E_INVALID, "triangle ids must be in [0, 2^31)");
+    return GRCA_OK;
+}
+
+grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_vertices, const uint32_t *d_indices,
+                                  int64_t n_triangles, const int32_t *d_tri_ids, int32_t tri_id_base) {
+    if (!h) return GRCA_E_INVALID;
+    grca_status st = check_tri_args(h, d_vertices, n_vertices, d_indices, n_triangles, d_tri_ids, tri_id_base);
+    if (st != GRCA_OK) return st;
     h->tri.v = reinterpret_cast<const float4 *>(d_vertices);
     h->tri.idx = d_indices;
     h->tri.ids = d_tri_ids;
     h->tri.id_base = tri_id_base;
     h->n_tri = n_triangles;
     h->have_tri = true;
+    return GRCA_OK;
+}
+
+grca_status grca_set_static_triangles(grca_t h, const float *d_vertices, int64_t n_vertices, const uint32_t *d_indices,
+                                      int64_t n_triangles, const int32_t *d_tri_ids, int32_t tri_id_base) {
+    if (!h) return GRCA_E_INVALID;
+    grca_status st = check_tri_args(h, d_vertices, n_vertices, d_indices, n_triangles, d_tri_ids, tri_id_base);
+    if (st != GRCA_OK) return st;
+    h->st_tri.v = reinterpret_cast<const float4 *>(d_vertices);
+    h->st_tri.idx = d_indices;
+    h->st_tri.ids = d_tri_ids;
+    h->st_tri.id_base = tri_id_base;
+    h->st_n = n_triangles;
+    h->st_set = true;
+    h->st_dirty = true;
+    return GRCA_OK;
+}
+
+grca_status grca_clear_static(grca_t h) {
+    if (!h) return GRCA_E_INVALID;
+    h->st_set = false;
+    h->st_dirty = false;
+    h->st_n = 0;
     return GRCA_OK;
 }
 
@@ -1446,22 +1494,10 @@ static cudaError_t launch_l2(grca_t h, const void *fn, unsigned grid, unsigned b
     return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-static grca_status launch_packed(grca_t h) {
-    if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
-    if (!h->have_tri) return fail(h, GRCA_E_STATE, "grca_update_triangles has not been called");
-    DeviceGuard dg(h->device);
-    KParams P = params(h);
-    const int slot = (int)(h->n_casts % kRing);
-    const bool prof = h->ev_ok;
-    if (prof) CK(cudaEventRecord(h->ev[slot][0], h->stream));
-    {   // K0
-        const int grid = h->num_sms * 4;
-        k_init<<<grid, 256, 0, h->stream>>>(h->d_hits, P.allhits, h->n_rays, h->d_ctrl, h->d_stats);
-        CK(cudaGetLastError());
-    }
-    if (prof) CK(cudaEventRecord(h->ev[slot][1], h->stream));
-    if (h->n_tri > 0) {   // K2
-        const long long tiles = (h->n_tri + K2_THREADS - 1) / K2_THREADS;
+// K2 .. K4 for the triangle source in P (events only when prof).
+static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof, int slot) {
+    if (n_tri > 0) {   // K2
+        const long long tiles = (n_tri + K2_THREADS - 1) / K2_THREADS;
         const long long grid = std::min<long long>(tiles, (long long)h->num_sms * h->k2_blocks_per_sm);
         if (h->n_em <= kFixedEm) {
             void *args[] = {(void *)&P, (void *)&h->lite_pack};
@@ -1474,13 +1510,13 @@ static grca_status launch_packed(grca_t h) {
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][2], h->stream));
     const bool split = (h->ci.debug_flags & GRCA_DEBUG_SPLIT_REFINE) != 0;
-    if (h->n_tri > 0 && split) {   // K2b (bounds only), rounds interleaved over warps
+    if (n_tri > 0 && split) {   // K2b (bounds only), rounds interleaved over warps
         const long long grid = (long long)h->num_sms * h->k2b_blocks_per_sm;
         k_refine<<<(unsigned)grid, K2_THREADS, h->k2b_smem, h->stream>>>(P);
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][3], h->stream));
-    if (h->n_tri > 0) {   // K4s (split) or fused K2b+K4s
+    if (n_tri > 0) {   // K4s (split) or fused K2b+K4s
         if (split) {
             const long long grid = (long long)h->num_sms * h->k4s_blocks_per_sm;
             k_small<<<(unsigned)grid, K2_THREADS, h->k4s_smem, h->stream>>>(P);
@@ -1491,17 +1527,55 @@ static grca_status launch_packed(grca_t h) {
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][4], h->stream));
-    if (h->n_tri > 0) {   // K3
+    if (n_tri > 0) {   // K3
         const long long grid = std::min<long long>((h->cap_large + 255) / 256, (long long)h->num_sms * 4);
         k_bin<<<(unsigned)grid, 256, 0, h->stream>>>(P);
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][5], h->stream));
-    if (h->n_tri > 0) {   // K4
+    if (n_tri > 0) {   // K4
         const int grid = h->num_sms * h->k4_blocks_per_sm;
         CK(launch_l2(h, (const void *)k_isect, (unsigned)grid, K4_THREADS, sizeof(EmDev) * h->n_em, P));
         CK(cudaGetLastError());
     }
+    return GRCA_OK;
+}
+
+static grca_status launch_packed(grca_t h) {
+    if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
+    if (!h->have_tri && !h->st_set) return fail(h, GRCA_E_STATE, "grca_update_triangles has not been called");
+    DeviceGuard dg(h->device);
+    const int slot = (int)(h->n_casts % kRing);
+    const bool prof = h->ev_ok;
+    KParams P = params(h);
+    if (h->st_set && h->st_dirty) {   // hybrid: (re)cast the static triangles into the cached keys
+        KParams PS = P;
+        PS.tri = h->st_tri;
+        PS.n_tri = h->st_n;
+        k_init<<<h->num_sms * 4, 256, 0, h->stream>>>(h->d_hits, PS.allhits, h->n_rays, h->d_ctrl, h->d_stats,
+                                                      nullptr, nullptr);
+        CK(cudaGetLastError());
+        grca_status st = launch_core(h, PS, h->st_n, false, slot);
+        if (st != GRCA_OK) return st;
+        CK(cudaMemcpyAsync(h->d_static_keys, h->d_hits, sizeof(unsigned long long) * h->n_rays,
+                           cudaMemcpyDeviceToDevice, h->stream));
+        if (PS.allhits)
+            CK(cudaMemcpyAsync(h->d_static_allhits, PS.allhits, sizeof(unsigned) * h->n_rays, cudaMemcpyDeviceToDevice,
+                               h->stream));
+        h->st_dirty = false;
+    }
+    if (prof) CK(cudaEventRecord(h->ev[slot][0], h->stream));
+    {   // K0
+        const int grid = h->num_sms * 4;
+        k_init<<<grid, 256, 0, h->stream>>>(h->d_hits, P.allhits, h->n_rays, h->d_ctrl, h->d_stats,
+                                            h->st_set ? h->d_static_keys : nullptr,
+                                            (h->st_set && P.allhits) ? h->d_static_allhits : nullptr);
+        CK(cudaGetLastError());
+    }
+    if (prof) CK(cudaEventRecord(h->ev[slot][1], h->stream));
+    if (!h->have_tri) P.n_tri = 0;
+    grca_status st = launch_core(h, P, P.n_tri, prof, slot);
+    if (st != GRCA_OK) return st;
     if (prof) CK(cudaEventRecord(h->ev[slot][6], h->stream));
     return GRCA_OK;
 }
@@ -1534,7 +1608,7 @@ static grca_status fill_stats(grca_t h, grca_stats *s) {
     s->large_pairs = (int64_t)st[ST_LARGE];
     s->chunks = (int64_t)st[ST_CHUNKS];
     s->rtic_tested = (int64_t)(st[ST_ITEMS_SMALL] + st[ST_ITEMS_LARGE]);
-    s->rtic_brute = (int64_t)(h->n_rays * h->n_tri);
+    s->rtic_brute = (int64_t)(h->n_rays * ((h->have_tri ? h->n_tri : 0) + (h->st_set ? h->st_n : 0)));
     s->fp64_fallbacks = (int64_t)st[ST_FP64];
     s->hits_recorded = (int64_t)st[ST_HITS];
     s->overflow_inline = (int64_t)(st[ST_OVF_LARGE] + st[ST_OVF_CHUNK]);

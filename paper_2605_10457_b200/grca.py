@@ -23,7 +23,7 @@ L2_PERSIST = 64
 
 EXPORTS = [
     "grca_create", "grca_destroy", "grca_set_emitters", "grca_update_triangles", "grca_cast",
-    "grca_cast_packed", "grca_hits_packed", "grca_unpack", "grca_get_stats", "grca_kernel_times",
+    "grca_cast_packed", "grca_hits_packed", "grca_set_static_triangles", "grca_clear_static", "grca_unpack", "grca_get_stats", "grca_kernel_times",
     "grca_debug_all_hits", "grca_debug_large_list", "grca_debug_fast_atan2", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
 ]
 
@@ -83,6 +83,8 @@ def load(path: str = LIB_PATH):
         "grca_update_triangles": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
         "grca_cast": ([vp, vp, vp, C.POINTER(Stats)], C.c_int),
         "grca_cast_packed": ([vp], C.c_int),
+        "grca_set_static_triangles": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
+        "grca_clear_static": ([vp], C.c_int),
         "grca_hits_packed": ([vp, C.POINTER(vp), C.POINTER(i64)], C.c_int),
         "grca_unpack": ([vp, vp, vp], C.c_int),
         "grca_get_stats": ([vp, C.POINTER(Stats)], C.c_int),
@@ -228,6 +230,25 @@ class Grca:
         self._tri_refs = (vertices, indices, tri_ids)
         self.n_triangles = ntri
         return self
+
+    # -- grca_set_static_triangles / grca_clear_static (hybrid static/dynamic, NEXT-f2)
+    def set_static_triangles(self, vertices, indices=None, tri_ids=None, tri_id_base: int = 0, n_triangles=None):
+        import torch
+
+        assert vertices.is_cuda and vertices.dtype == torch.float32 and vertices.shape[-1] == 4
+        assert vertices.is_contiguous()
+        nv = vertices.numel() // 4
+        ntri = (indices.numel() // 3) if indices is not None else nv // 3
+        if n_triangles is not None:
+            ntri = int(n_triangles)
+        self._check(self._L.grca_set_static_triangles(self._h, _ptr(vertices), nv, _ptr(indices), ntri, _ptr(tri_ids),
+                                                      int(tri_id_base)))
+        self._static_refs = (vertices, indices, tri_ids)
+        return self
+
+    def clear_static(self):
+        self._check(self._L.grca_clear_static(self._h))
+        self._static_refs = ()
 
     # -- grca_cast
     def cast(self, out_dist=None, out_tri=None, stats: bool = False):

@@ -382,3 +382,38 @@ def test_a7_c1_and_fixtures():
     oref = oracle.cast(ems, tris, want_t64=True, want_allhits=True)
     check(ems, tris, a7[0], a7[1], ref=oref)
     _check_all_hits(ems, tris, a7[3].debug_all_hits().cpu().numpy(), oref)
+
+
+def test_hybrid_static_dynamic_exact():
+    """NEXT-f2 hybrid: static triangles cast once into cached keys, frames cull only the dynamic ones;
+    bit-identical to casting everything, across frames, emitter changes and clear_static."""
+    ems, tris = sg.random_scene(300, n_tris=2400, n_emitters=2, gamma=16, chi=256, extent=8.0)
+    n_s = 1500
+    st = tris[:n_s]
+    g = Grca(device=0, max_triangles=len(tris), max_rays=sg.n_rays_total(ems) + 4096,
+             debug_flags=G.DEBUG_COUNT_ALL_HITS)
+    g.set_emitters(ems)
+    g.set_static_triangles(tris_to_float4(st), tri_id_base=0)
+    rng = np.random.default_rng(0)
+    for frame in range(3):
+        dyn = tris[n_s:] + np.float32(rng.normal(size=3) * 0.5)          # moved dynamic triangles
+        g.update_triangles(tris_to_float4(dyn), tri_id_base=n_s)
+        d_h, t_h = g.cast()
+        allh = g.debug_all_hits().cpu().numpy().copy()
+        full = np.concatenate([st, dyn], 0)
+        d_f, t_f, _, gf = run(ems, full, flags=G.DEBUG_COUNT_ALL_HITS)
+        assert np.array_equal(t_h.cpu().numpy(), t_f)
+        assert np.array_equal(d_h.cpu().numpy().view(np.uint32), d_f.view(np.uint32))
+        assert np.array_equal(allh, gf.debug_all_hits().cpu().numpy())
+    check(ems, full, d_f, t_f)
+    # emitters change -> the static cache is recomputed
+    ems2, _ = sg.random_scene(301, n_tris=10, n_emitters=1, gamma=12, chi=300)
+    g.set_emitters(ems2)
+    d_h, t_h = g.cast()
+    d_f, t_f, _, _ = run(ems2, full)
+    assert np.array_equal(t_h.cpu().numpy(), t_f)
+    # leave hybrid mode
+    g.clear_static()
+    d_c, t_c = g.cast()
+    d_f, t_f, _, _ = run(ems2, dyn, ids=np.arange(n_s, len(tris)))
+    assert np.array_equal(t_c.cpu().numpy(), t_f)
