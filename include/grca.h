@@ -80,7 +80,10 @@ typedef struct {
     uint32_t debug_flags;    /* GRCA_DEBUG_* | GRCA_PROFILE_KERNELS */
     int32_t small_max;       /* pairs with <= small_max candidates (<= 1023) take the small-rectangle
                                 path (K4s); larger ones are chunked (K3/K4).  0 -> default 512 */
-    int32_t reserved[7];
+    float apparent_area_eps; /* NEXT-f1 paper mode, APPROXIMATE: skip a (triangle, emitter) pair when
+                                (A_T (c-o).n)^2 < eps^2 |c-o|^6 (eps_A = 1e-6 there;
+                                |.| of (c-o).n in two-sided mode).  0 -> off (exact results) */
+    int32_t reserved[6];
 } grca_create_info;
 
 /* One spinning LiDAR (ray origin); SPEC SensorConfig. */
@@ -112,6 +115,10 @@ typedef struct {
     int64_t overflow_inline; /* large pairs processed inline because the list was full */
     int64_t prefilter_survivors; /* pairs passed by the K2 elevation pre-test to K2b */
     int64_t rtic_small;      /* part of rtic_tested done by K4s (small rectangles) */
+    int64_t sat_pairs;       /* paper classification of surviving pairs (Eq. sat_cond):
+                                SAT = no seam wrap and gamma_span <= 64 and chi_span <= 64 ... */
+    int64_t bat_pairs;       /* ... BAT = the rest (counts only; the build bins by item count) */
+    int64_t area_culled;     /* pairs skipped by the apparent-area cull (paper mode) */
     int32_t overflow;        /* 1 if any capacity fallback happened */
     float ms_total;          /* device time of the last cast if GRCA_PROFILE_KERNELS */
     float ms_k[8];           /* per kernel: K0 init, K2 cull, K2b refine (split mode only), K2b+K4s

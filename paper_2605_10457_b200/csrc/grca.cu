@@ -46,7 +46,7 @@ constexpr int kLutMaxEm = 16;   // channel LUTs staged in smem for up to 16 emit
 enum Stat {
     ST_PAIRS = 0, ST_RANGE, ST_CHANNEL, ST_AZIMUTH, ST_SURV, ST_SMALL, ST_LARGE, ST_ITEMS_SMALL,
     ST_ITEMS_LARGE, ST_FP64, ST_HITS, ST_CHUNKS, ST_OVF_LARGE, ST_OVF_CHUNK, ST_SETUP64, ST_DEGEN,
-    ST_K2SURV, ST_COUNT
+    ST_K2SURV, ST_SAT, ST_BAT, ST_AREA, ST_COUNT
 };
 
 struct KParams {
@@ -66,6 +66,7 @@ struct KParams {
     long long cap_chunks;
     unsigned long long *stats;
     int faces, nocull, force64, small_max, norefine;
+    float area_eps2;             // (apparent-area eps)^2, 0 = off
     long long n_rays;
     const EmLite *lite;
     const unsigned char *lut;    // NULL -> binary search
@@ -227,7 +228,7 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const KParam
     if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
     __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned c_pairs = 0, c_range = 0, c_chan = 0, c_surv = 0;
+    unsigned c_pairs = 0, c_range = 0, c_chan = 0, c_surv = 0, c_area = 0;
     const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long t = tile * K2_THREADS + threadIdx.x;
@@ -247,9 +248,18 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const KParam
             unsigned chan = 0u;
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
-                const int st = P.nocull ? CULL_KEEP
-                                        : quick_cull(v, emax, EL.e[e], sSin + EL.e[e].sin_base,
-                                                     P.lut ? sLut + e * kLutBins : nullptr);
+                int st = P.nocull ? CULL_KEEP
+                                  : quick_cull(v, emax, EL.e[e], sSin + EL.e[e].sin_base,
+                                               P.lut ? sLut + e * kLutBins : nullptr);
+                if (P.area_eps2 > 0.f && st == CULL_KEEP) {   // NEXT-f1 paper mode (approximate):
+                    // apparent-area cull, PAPER.md:622-632 (recomputed per pair: paper mode only)
+                    const f3 cen = {(v[0].x + v[1].x + v[2].x) * (1.f / 3.f), (v[0].y + v[1].y + v[2].y) * (1.f / 3.f),
+                                    (v[0].z + v[1].z + v[2].z) * (1.f / 3.f)};
+                    const f3 hN = scalef(crossf(subf(v[1], v[0]), subf(v[2], v[0])), 0.5f);   // A_T * n
+                    const f3 co = {cen.x - EL.e[e].o[0], cen.y - EL.e[e].o[1], cen.z - EL.e[e].o[2]};
+                    const float an = dotf(hN, co), d2 = dotf(co, co);
+                    if (an * an < P.area_eps2 * d2 * d2 * d2) { st = CULL_AREA; ++c_area; }
+                }
                 keep |= (st == CULL_KEEP ? 1u : 0u) << e;
                 rng |= (st == CULL_RANGE ? 1u : 0u) << e;
                 chan += (st == CULL_CHANNEL);
@@ -292,6 +302,7 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const KParam
     cnt[ST_RANGE] = c_range;
     cnt[ST_CHANNEL] = c_chan;
     cnt[ST_K2SURV] = c_surv;
+    cnt[ST_AREA] = c_area;
     block_flush(acc, P.stats, cnt);
 }
 
@@ -561,6 +572,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
         const int n = (int)ns;
         const int idx = (int)(w * 32u) + lane;
         int my = 0, e = 0, cat = C_NONE;
+        bool sat = false, bat = false;   // paper classification counters
         long long t = 0;
         Rect R;
         bool large = false;
@@ -574,6 +586,10 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
             const int st = cull_pair(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
                                      P.nocull != 0, R);
             if (st == CULL_KEEP) {
+                // Eq. sat_cond with (gamma_T, chi_T) = (64, 64); all-CW = the arc does not wrap the seam
+                const bool wraps = R.r_len >= E.chi || R.r_lo + R.r_len > E.chi || R.pole_rows;
+                sat = !wraps && (R.c_to - R.c_from + 1) <= 64 && R.r_len <= 64;
+                bat = !sat;
                 const long long items = rect_items(R, E);
                 if (items <= P.small_max && !R.pole_rows) {
                     Setup S;
@@ -621,6 +637,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
                            mc = __ballot_sync(FULL, cat == C_CHAN), ma = __ballot_sync(FULL, cat == C_AZI),
                            md = __ballot_sync(FULL, cat == C_DEGEN);
             const unsigned items = __reduce_add_sync(FULL, (unsigned)my);
+            const unsigned msat = __ballot_sync(FULL, sat), mbat = __ballot_sync(FULL, bat);
             if (lane == 0) {
                 if (ms | ml | mo) atomicAdd(acc + ST_SURV, (unsigned)(__popc(ms) + __popc(ml) + __popc(mo)));
                 if (ms) atomicAdd(acc + ST_SMALL, (unsigned)__popc(ms));
@@ -631,6 +648,8 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
                 if (mc) atomicAdd(acc + ST_CHANNEL, (unsigned)__popc(mc));
                 if (ma) atomicAdd(acc + ST_AZIMUTH, (unsigned)__popc(ma));
                 if (md) atomicAdd(acc + ST_DEGEN, (unsigned)__popc(md));
+                if (msat) atomicAdd(acc + ST_SAT, (unsigned)__popc(msat));
+                if (mbat) atomicAdd(acc + ST_BAT, (unsigned)__popc(mbat));
             }
         }
         // A5: warp-level prefix-scan work expansion
@@ -1075,6 +1094,7 @@ KParams params(grca_t h) {
     P.force64 = (h->ci.debug_flags & GRCA_DEBUG_FORCE_FP64) ? 1 : 0;
     P.norefine = (h->ci.debug_flags & GRCA_DEBUG_NO_REFINE) ? 1 : 0;
     P.small_max = std::min(1023, h->ci.small_max > 0 ? h->ci.small_max : 512);
+    P.area_eps2 = h->ci.apparent_area_eps > 0.f ? h->ci.apparent_area_eps * h->ci.apparent_area_eps : 0.f;
     P.n_rays = h->n_rays;
     P.lite = h->d_lite;
     P.lut = h->use_lut ? h->d_lut : nullptr;
@@ -1614,6 +1634,9 @@ static grca_status fill_stats(grca_t h, grca_stats *s) {
     s->overflow_inline = (int64_t)(st[ST_OVF_LARGE] + st[ST_OVF_CHUNK]);
     s->prefilter_survivors = (int64_t)st[ST_K2SURV];
     s->rtic_small = (int64_t)st[ST_ITEMS_SMALL];
+    s->sat_pairs = (int64_t)st[ST_SAT];
+    s->bat_pairs = (int64_t)st[ST_BAT];
+    s->area_culled = (int64_t)st[ST_AREA];
     s->overflow = s->overflow_inline > 0;
     if (h->ev_ok && h->n_casts > 0) {
         const int slot = (int)((h->n_casts - 1) % kRing);

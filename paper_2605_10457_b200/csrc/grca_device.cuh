@@ -162,7 +162,7 @@ struct Rect {
     int pole_rows;      // 1 if the range touches pole channels (full-azimuth rows)
 };
 
-enum { CULL_KEEP = 0, CULL_RANGE = 1, CULL_CHANNEL = 2, CULL_AZIMUTH = 3, CULL_DEGENERATE = 4 };
+enum { CULL_KEEP = 0, CULL_RANGE = 1, CULL_CHANNEL = 2, CULL_AZIMUTH = 3, CULL_DEGENERATE = 4, CULL_AREA = 5 };
 
 __device__ __forceinline__ int lower_bound_f(const float *t, int n, float x) {   // first j: t[j] >= x
     int lo = 0, hi = n;

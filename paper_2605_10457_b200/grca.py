@@ -39,7 +39,7 @@ class CreateInfo(C.Structure):
         ("device", C.c_int32), ("stream", C.c_void_p), ("nranks", C.c_int32), ("rank", C.c_int32),
         ("max_triangles", C.c_int64), ("max_rays", C.c_int64), ("max_large_items", C.c_int64),
         ("faces", C.c_int32), ("debug_flags", C.c_uint32), ("small_max", C.c_int32),
-        ("reserved", C.c_int32 * 7),
+        ("apparent_area_eps", C.c_float), ("reserved", C.c_int32 * 6),
     ]
 
 
@@ -55,7 +55,7 @@ class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "pairs", "range_culled", "channel_culled", "azimuth_culled", "survivors", "small_pairs", "large_pairs",
         "chunks", "rtic_tested", "rtic_brute", "fp64_fallbacks", "hits_recorded", "overflow_inline",
-        "prefilter_survivors", "rtic_small")] + [
+        "prefilter_survivors", "rtic_small", "sat_pairs", "bat_pairs", "area_culled")] + [
         ("overflow", C.c_int32), ("ms_total", C.c_float), ("ms_k", C.c_float * 8)]
 
     def as_dict(self) -> dict:
@@ -159,7 +159,7 @@ class Grca:
 
     def __init__(self, device: int = 0, stream=None, max_triangles: int = 1 << 20, max_rays: int = 1 << 20,
                  max_large_items: int = 0, faces: int = 0, debug_flags: int = 0, small_max: int = 0,
-                 nranks: int = 1, rank: int = 0):
+                 nranks: int = 1, rank: int = 0, apparent_area_eps: float = 0.0):
         import torch
 
         L = load()
@@ -174,6 +174,7 @@ class Grca:
         ci.nranks, ci.rank = int(nranks), int(rank)
         ci.max_triangles, ci.max_rays, ci.max_large_items = int(max_triangles), int(max_rays), int(max_large_items)
         ci.faces, ci.debug_flags, ci.small_max = int(faces), int(debug_flags), int(small_max)
+        ci.apparent_area_eps = float(apparent_area_eps)
         h = C.c_void_p()
         st = L.grca_create(C.byref(ci), C.byref(h))
         if st != GRCA_OK:
