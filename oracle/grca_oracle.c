@@ -19,6 +19,8 @@
  *      dtheta = H / chi  (H = 2*pi for a 360 deg emitter, pi for 180 deg),
  *      theta_i = -floor(chi/2)*dtheta + i*dtheta
  *      phi_j   = channel_elev_rad[j]   (sorted table)
+ *      (noise model: a perturbed per-ray azimuth table theta*_i replaces the
+ *       grid when given; per-channel perturbed elevations are simply the elevation table)
  *      d = RN32( cos(theta)cos(phi) f + sin(theta)cos(phi) r + sin(phi) u )
  *      evaluated in fp64 left to right, rounded componentwise to fp32.
  *      Global ray index g = O_n + j*chi_n + i
@@ -52,6 +54,8 @@ typedef struct {
     int32_t rays_per_channel;      /* chi_n   */
     int32_t hfov_deg;              /* 360 or 180 */
     float max_range;               /* <= 0 or +inf: no limit */
+    const float *ray_azimuth_rad;  /* NULL: grid theta_i; else the pre-stored perturbed azimuths
+                                      theta*_i of the noise model */
 } oracle_emitter;
 
 /* ---------------------------------------------------------------- O1 -- */
@@ -90,7 +94,7 @@ static void ray_direction(const oracle_emitter *e, int32_t j, int32_t i,
     const double H = (e->hfov_deg == 180) ? M_PI : 2.0 * M_PI;
     const double dtheta = H / (double)e->rays_per_channel;
     const double theta0 = -(double)(e->rays_per_channel / 2) * dtheta;
-    const double theta = theta0 + (double)i * dtheta;
+    const double theta = e->ray_azimuth_rad ? (double)e->ray_azimuth_rad[i] : theta0 + (double)i * dtheta;
     const double phi = (double)e->channel_elev_rad[j];
     const double ct = cos(theta), st = sin(theta);
     const double cp = cos(phi), sp = sin(phi);

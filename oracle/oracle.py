@@ -43,6 +43,7 @@ class _Em(C.Structure):
         ("rays_per_channel", C.c_int32),
         ("hfov_deg", C.c_int32),
         ("max_range", C.c_float),
+        ("ray_azimuth_rad", C.POINTER(C.c_float)),
     ]
 
 
@@ -88,6 +89,12 @@ class _EmArray:
             s.rays_per_channel = int(e.rays_per_channel)
             s.hfov_deg = int(e.hfov_deg)
             s.max_range = float(e.max_range)
+            az = getattr(e, "ray_azimuth", None)
+            if az is not None:
+                az = np.ascontiguousarray(np.asarray(az, dtype=np.float32))
+                assert az.shape[0] == int(e.rays_per_channel)
+                self.elevs.append(az)
+                s.ray_azimuth_rad = az.ctypes.data_as(C.POINTER(C.c_float))
         self.n = len(emitters)
 
 

@@ -45,6 +45,7 @@ class Emitter:
     rays_per_channel: int = 512
     hfov_deg: int = 360
     max_range: float = INF
+    ray_azimuth: Optional[np.ndarray] = None   # noise model: pre-stored perturbed azimuths (chi,)
 
     def __post_init__(self):
         self.origin = np.asarray(self.origin, dtype=np.float32).reshape(3)
@@ -75,6 +76,31 @@ def full_sphere_elev(n_channels: int) -> np.ndarray:
     dphi = math.pi / g
     phi0 = -(g // 2) * dphi
     return np.array([phi0 + j * dphi for j in range(g)], dtype=np.float64).astype(np.float32)
+
+
+def perturbed_azimuths(chi: int, hfov_deg: int, seed: int, frac: float = 0.45) -> np.ndarray:
+    """Noise-model input: per-ray azimuths theta*_i = theta_i + U(-frac, frac) dtheta
+    around the nominal scan pattern theta_i = -floor(chi/2) dtheta + i dtheta (frac < 0.5: no ray
+    crosses its neighbour), rounded to fp32."""
+    rng = np.random.default_rng([int(seed), 0xA21])
+    H = 2 * math.pi if hfov_deg == 360 else math.pi
+    dth = H / chi
+    th = np.array([-(chi // 2) * dth + i * dth for i in range(chi)])
+    return (th + rng.uniform(-frac, frac, size=chi) * dth).astype(np.float32)
+
+
+def perturbed_elev(elev: np.ndarray, seed: int, frac: float = 0.3) -> np.ndarray:
+    """Noise-model input: per-channel perturbed elevations phi*_j, each moved by at
+    most frac of its gap to the neighbours (order kept), clipped to [-RN32(pi/2), RN32(pi/2)]."""
+    rng = np.random.default_rng([int(seed), 0xE1E])
+    e = np.asarray(elev, dtype=np.float64)
+    gaps = np.diff(e)
+    lo = np.concatenate([[gaps[0] if len(gaps) else 0.01], gaps])
+    hi = np.concatenate([gaps, [gaps[-1] if len(gaps) else 0.01]])
+    step = np.minimum(lo, hi) * frac
+    out = e + rng.uniform(-1, 1, size=e.shape) * step
+    lim = float(np.float32(math.pi / 2))
+    return np.clip(out, -lim, lim).astype(np.float32)
 
 
 def vlp16_elev() -> np.ndarray:

@@ -333,3 +333,24 @@ def test_comparator_self_and_perturbed(oracle_lib):
     t[hit_rays[1]] = np.inf                     # a dropped hit (not near an edge in general)
     rep = oracle.compare(ems, tris, t, i, ref)
     assert not rep["passed"] and rep["kinds"]["dist"] == 1 and rep["kinds"]["gpu_miss"] == 1
+
+
+def test_perturbed_azimuth_table(oracle_lib):
+    """Noise model: a pre-stored per-ray azimuth table theta*_i replaces the grid
+    angle of ray i.  Pins: the azimuth of every direction (in the frame) equals theta*_i within the fp32
+    rounding of d, theta* = 0 gives f exactly, and a table equal to the grid reproduces the grid rays."""
+    f, r, u = np.float32([1, 0, 0]), np.float32([0, -1, 0]), np.float32([0, 0, 1])
+    az = sg.perturbed_azimuths(64, 360, seed=3)
+    az[10] = 0.0
+    em = _em(forward=f, right=r, up=u, elev=np.array([-0.3, 0.0, 0.4], np.float32), rays_per_channel=64)
+    em.ray_azimuth = az
+    tab = oracle.ray_table([em]).astype(np.float64)
+    x_f, x_r = tab @ f.astype(np.float64), tab @ r.astype(np.float64)
+    got = np.arctan2(x_r, x_f).reshape(3, 64)
+    np.testing.assert_allclose(got, np.broadcast_to(az.astype(np.float64), (3, 64)), atol=3e-7)
+    np.testing.assert_array_equal(tab[64 + 10], f)            # channel phi = 0, theta* = 0 -> f
+    grid = _em(elev=np.array([0.2], np.float32), rays_per_channel=8, hfov_deg=180)
+    g2 = _em(elev=np.array([0.2], np.float32), rays_per_channel=8, hfov_deg=180)
+    g2.ray_azimuth = np.array([-(8 // 2) * (math.pi / 8) + i * (math.pi / 8) for i in range(8)], np.float64).astype(np.float32)
+    a, b = oracle.ray_table([grid]), oracle.ray_table([g2])
+    np.testing.assert_allclose(a, b, atol=2e-7)
