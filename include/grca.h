@@ -96,6 +96,10 @@ typedef struct {
     int32_t rays_per_channel;          /* chi_n in [1, 65535] */
     int32_t hfov_deg;                  /* 360 or 180 */
     float max_range;                   /* D_max > 0; <= 0 or +inf -> unlimited */
+    const float *ray_azimuth_rad;      /* NULL -> grid theta_i = -floor(chi/2) dth + i dth; else the noise
+                                          model's pre-stored perturbed azimuths theta*_i (chi entries,
+                                          strictly ascending, |theta*_i - theta_i| < dth; PAPER.md:
+                                          2276-2283).  Per-channel elevation noise = the elevation table */
 } grca_emitter;
 
 /* Per-cast counters (SURVEY 5 "Metrics"; Eq. 1 and 2131-2144 Eq. rtic_reduced). */
@@ -179,6 +183,11 @@ grca_status grca_cast(grca_t h, float *d_out_dist, int32_t *d_out_tri, grca_stat
 grca_status grca_cast_packed(grca_t h);
 grca_status grca_hits_packed(grca_t h, uint64_t **d_hits, int64_t *n_rays);
 grca_status grca_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri);
+
+/* Distance noise (noise model: "a post-processing perturbation added after output
+ * conversion"): K5 adds sigma * N(0,1) to every hit distance (clamped at 0; misses stay +inf), the
+ * normal drawn from a counter-based generator keyed by (seed, cast index, ray).  sigma <= 0 -> off. */
+grca_status grca_set_distance_noise(grca_t h, float sigma, uint64_t seed);
 
 /* Counters of the last cast (synchronizes the stream). */
 grca_status grca_get_stats(grca_t h, grca_stats *h_stats);

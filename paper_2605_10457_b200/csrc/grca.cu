@@ -843,8 +843,9 @@ __global__ void __launch_bounds__(256) k_bin(const KParams P) {
                     const int nb = refine_row(x, sj - (double)kPadS, sj + (double)kPadS, th_ref, dmin, dmax);
                     if (nb < 2) { lo = r_lo; len = r_len; }
                     else {
-                        const int ilo = (int)ceilf((th_ref + dmin - kPadTheta - E.theta0) * E.inv_dtheta);
-                        const int ihi = (int)floorf((th_ref + dmax + kPadTheta - E.theta0) * E.inv_dtheta);
+                        const float padth = kPadTheta + (E.noisy ? E.dtheta : 0.f);
+                        const int ilo = (int)ceilf((th_ref + dmin - padth - E.theta0) * E.inv_dtheta);
+                        const int ihi = (int)floorf((th_ref + dmax + padth - E.theta0) * E.inv_dtheta);
                         const int a = max(ilo, r_lo), b = min(ihi, r_lo + r_len - 1);
                         if (a <= b) {
                             lo = a;
@@ -948,12 +949,30 @@ __global__ void __launch_bounds__(K4_THREADS) k_isect(const KParams P) {
 }
 
 // ---------------------------------------------------------------- K5 unpack --
+// counter-based normal deviate (splitmix64 -> two uniforms -> Box-Muller)
+__device__ __forceinline__ unsigned long long splitmix64(unsigned long long x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__device__ __forceinline__ float gauss01(unsigned long long key) {
+    const unsigned long long r = splitmix64(key);
+    const float u1 = ((unsigned)(r >> 40) + 0.5f) * (1.f / 16777216.f);
+    const float u2 = ((unsigned)(r & 0xFFFFFFu) + 0.5f) * (1.f / 16777216.f);
+    return sqrtf(-2.f * __logf(u1)) * __cosf(6.283185307f * u2);
+}
+
 __global__ void k_unpack(const unsigned long long *__restrict__ hits, float *__restrict__ dist,
-                         int32_t *__restrict__ tri, long long n) {
+                         int32_t *__restrict__ tri, long long n, float sigma, unsigned long long seed,
+                         unsigned long long cast_idx) {
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const unsigned long long k = __ldcs(hits + i);
-        if (dist) __stcs(dist + i, __uint_as_float((unsigned)(k >> 32)));
+        float dv = __uint_as_float((unsigned)(k >> 32));
+        if (sigma > 0.f && dv < CUDART_INF_F)   // noise model: range noise after output conversion
+            dv = fmaxf(0.f, dv + sigma * gauss01(splitmix64(seed ^ (cast_idx << 40)) ^ (unsigned long long)i));
+        if (dist) __stcs(dist + i, dv);
         if (tri) __stcs(tri + i, (int32_t)(unsigned)(k & 0xffffffffull));
     }
 }
@@ -996,7 +1015,9 @@ struct grca_ctx {
     long long surv_cap_tiles = 0;
     int surv_n_em = 0;
     EmLitePack lite_pack{};
-    cudaAccessPolicyWindow l2win{};   // persisting window over ray table + hits (num_bytes 0 = off)
+    cudaAccessPolicyWindow l2win{};
+    float noise_sigma = 0.f;           // distance noise (K5), 0 = off
+    unsigned long long noise_seed = 0;   // persisting window over ray table + hits (num_bytes 0 = off)
     size_t k2f_smem = 0;
     int4 *d_large = nullptr;
     int4 *d_chunks = nullptr;
@@ -1314,6 +1335,17 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
         while (phi < E.n_channels - plo && cos((double)E.channel_elev_rad[E.n_channels - 1 - phi]) < 0.01) ++phi;
         D.pole_lo = plo;
         D.pole_hi = phi;
+        D.noisy = E.ray_azimuth_rad ? 1 : 0;
+        if (E.ray_azimuth_rad) {   // noise model: |theta*_i - theta_i| < dtheta, strictly ascending
+            const double th0 = -(double)(E.rays_per_channel / 2) * dth;
+            for (int i = 0; i < E.rays_per_channel; ++i) {
+                const double a = (double)E.ray_azimuth_rad[i];
+                if (!(fabs(a - (th0 + (double)i * dth)) < dth))
+                    return fail(h, GRCA_E_INVALID, tag + "ray_azimuth_rad[i] not within dtheta of the grid angle");
+                if (i && !(E.ray_azimuth_rad[i] > E.ray_azimuth_rad[i - 1]))
+                    return fail(h, GRCA_E_INVALID, tag + "ray_azimuth_rad not strictly ascending");
+            }
+        }
         offs[n + 1] = offs[n] + (long long)E.n_channels * E.rays_per_channel;
     }
     if ((int)sins.size() > kMaxSin) return fail(h, GRCA_E_INVALID, "sum of (n_channels + 2) over emitters > 4096");
@@ -1327,7 +1359,7 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
         const double th0 = -(double)(E.rays_per_channel / 2) * dth;
         std::vector<double> ct(E.rays_per_channel), st(E.rays_per_channel);
         for (int i = 0; i < E.rays_per_channel; ++i) {
-            const double th = th0 + (double)i * dth;
+            const double th = E.ray_azimuth_rad ? (double)E.ray_azimuth_rad[i] : th0 + (double)i * dth;
             ct[i] = cos(th);
             st[i] = sin(th);
         }
@@ -1605,8 +1637,8 @@ static grca_status launch_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri
     const int slot = (int)(h->n_casts % kRing);
     if (d_out_dist || d_out_tri) {
         const long long blocks = std::min<long long>((h->n_rays + 255) / 256, (long long)h->num_sms * 8);
-        k_unpack<<<(unsigned)std::max<long long>(1, blocks), 256, 0, h->stream>>>(h->d_hits, d_out_dist, d_out_tri,
-                                                                                 h->n_rays);
+        k_unpack<<<(unsigned)std::max<long long>(1, blocks), 256, 0, h->stream>>>(
+            h->d_hits, d_out_dist, d_out_tri, h->n_rays, h->noise_sigma, h->noise_seed, (unsigned long long)h->n_casts);
         CK(cudaGetLastError());
     }
     if (h->ev_ok) CK(cudaEventRecord(h->ev[slot][7], h->stream));
@@ -1680,6 +1712,14 @@ grca_status grca_hits_packed(grca_t h, uint64_t **d_hits, int64_t *n_rays) {
     if (!h || !d_hits) return GRCA_E_INVALID;
     *d_hits = reinterpret_cast<uint64_t *>(h->d_hits);
     if (n_rays) *n_rays = h->n_rays;
+    return GRCA_OK;
+}
+
+grca_status grca_set_distance_noise(grca_t h, float sigma, uint64_t seed) {
+    if (!h) return GRCA_E_INVALID;
+    if (!(sigma >= 0.f) || !std::isfinite(sigma)) return fail(h, GRCA_E_INVALID, "sigma must be finite and >= 0");
+    h->noise_sigma = sigma;
+    h->noise_seed = seed;
     return GRCA_OK;
 }
 

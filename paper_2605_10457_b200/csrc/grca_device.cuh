@@ -38,7 +38,7 @@ struct EmDev {
     float theta0, dtheta, inv_dtheta;
     float dmax_lo, dmax_hi;   // certified accept / reject bounds around D_max (+inf if none)
     double dmax;              // fp64 D_max for the fallback (+inf if none)
-    int gamma, chi, hfov, ray_base, sin_base, pole_lo, pole_hi, pad_;
+    int gamma, chi, hfov, ray_base, sin_base, pole_lo, pole_hi, noisy;   // noisy: perturbed theta*_i
 };
 
 // Phase-A (K2) view of an emitter: just what the elevation pre-test needs.
@@ -323,8 +323,10 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
         R.r_lo = 0; R.r_len = E.chi; R.pole_rows = 0;
         return CULL_KEEP;
     }
-    float xlo = (start - kPadTheta - E.theta0) * E.inv_dtheta;
-    float xhi = (start + len + kPadTheta - E.theta0) * E.inv_dtheta;
+    // perturbed azimuths (noise model): |theta*_i - theta_i| < dtheta -> one more ray each side
+    const float padth = kPadTheta + (E.noisy ? E.dtheta : 0.f);
+    float xlo = (start - padth - E.theta0) * E.inv_dtheta;
+    float xhi = (start + len + padth - E.theta0) * E.inv_dtheta;
     int ilo = (int)ceilf(xlo), ihi = (int)floorf(xhi);
     if (E.hfov == 360) {
         int n = ihi - ilo + 1;

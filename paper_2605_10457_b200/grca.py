@@ -23,7 +23,7 @@ L2_PERSIST = 64
 
 EXPORTS = [
     "grca_create", "grca_destroy", "grca_set_emitters", "grca_update_triangles", "grca_cast",
-    "grca_cast_packed", "grca_hits_packed", "grca_set_static_triangles", "grca_clear_static", "grca_unpack", "grca_get_stats", "grca_kernel_times",
+    "grca_cast_packed", "grca_hits_packed", "grca_set_static_triangles", "grca_clear_static", "grca_unpack", "grca_get_stats", "grca_kernel_times", "grca_set_distance_noise",
     "grca_debug_all_hits", "grca_debug_large_list", "grca_debug_fast_atan2", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
 ]
 
@@ -48,6 +48,7 @@ class EmitterC(C.Structure):
         ("origin", C.c_float * 3), ("forward", C.c_float * 3), ("right", C.c_float * 3), ("up", C.c_float * 3),
         ("channel_elev_rad", C.POINTER(C.c_float)), ("n_channels", C.c_int32),
         ("rays_per_channel", C.c_int32), ("hfov_deg", C.c_int32), ("max_range", C.c_float),
+        ("ray_azimuth_rad", C.POINTER(C.c_float)),
     ]
 
 
@@ -88,6 +89,7 @@ def load(path: str = LIB_PATH):
         "grca_hits_packed": ([vp, C.POINTER(vp), C.POINTER(i64)], C.c_int),
         "grca_unpack": ([vp, vp, vp], C.c_int),
         "grca_get_stats": ([vp, C.POINTER(Stats)], C.c_int),
+        "grca_set_distance_noise": ([vp, C.c_float, C.c_uint64], C.c_int),
         "grca_kernel_times": ([vp, i32, C.POINTER(C.c_float)], C.c_int),
         "grca_debug_all_hits": ([vp, C.POINTER(vp)], C.c_int),
         "grca_debug_large_list": ([vp, vp, i64, C.POINTER(i64)], C.c_int),
@@ -147,6 +149,11 @@ def _emitters_c(emitters: Sequence):
         s.hfov_deg = int(e.hfov_deg)
         mr = float(e.max_range)
         s.max_range = mr if math.isfinite(mr) else float("inf")
+        az = getattr(e, "ray_azimuth", None)
+        if az is not None:
+            az = np.ascontiguousarray(np.asarray(az, dtype=np.float32))
+            keep.append(az)
+            s.ray_azimuth_rad = az.ctypes.data_as(C.POINTER(C.c_float))
     return arr, keep
 
 
@@ -277,6 +284,9 @@ class Grca:
 
     def unpack(self, out_dist, out_tri):
         self._check(self._L.grca_unpack(self._h, _ptr(out_dist), _ptr(out_tri)))
+
+    def set_distance_noise(self, sigma: float, seed: int = 0):
+        self._check(self._L.grca_set_distance_noise(self._h, float(sigma), int(seed)))
 
     def get_stats(self) -> dict:
         s = Stats()

@@ -466,3 +466,55 @@ def test_paper_mode_apparent_area_cull(scene):
     exact = oracle.cast(ems, tris, want_t64=True)
     rep = oracle.compare(ems, tris, dist, tri, exact)
     assert rep["hit_pct_1mm"] >= 98.0, rep["hit_pct_1mm"]
+
+
+def _noisy_emitters(seed, n_em=2):
+    ems, tris = sg.random_scene(seed, n_tris=1200, n_emitters=n_em, gamma=14, chi=300, extent=7.0)
+    for k, e in enumerate(ems):
+        e.ray_azimuth = sg.perturbed_azimuths(e.rays_per_channel, e.hfov_deg, seed + k, frac=0.45)
+        e.elev = sg.perturbed_elev(e.elev, seed + k)
+    return ems, tris
+
+
+@pytest.mark.parametrize("seed", [5, 6])
+def test_noise_model_angles(seed):
+    """NEXT-f4 noise model (PAPER.md:2276-2299): perturbed per-ray azimuths and per-channel elevations;
+    the ray table matches the oracle bit for bit and the result is exact (cull widened by one ray)."""
+    ems, tris = _noisy_emitters(400 + seed)
+    g = Grca(device=0, max_triangles=len(tris), max_rays=sg.n_rays_total(ems))
+    g.set_emitters(ems)
+    assert np.array_equal(g.debug_ray_table().view(np.uint32), oracle.ray_table(ems).view(np.uint32))
+    for small_max, flags in ((0, G.DEBUG_COUNT_ALL_HITS), (1, G.DEBUG_COUNT_ALL_HITS)):
+        dist, tri, st, gg = run(ems, tris, small_max=small_max, flags=flags)
+        ref = oracle.cast(ems, tris, want_t64=True, want_allhits=True)
+        check(ems, tris, dist, tri, ref=ref)
+        _check_all_hits(ems, tris, gg.debug_all_hits().cpu().numpy(), ref)
+
+
+def test_distance_noise():
+    """Distance noise is a post-process of hit distances: ids unchanged, misses stay +inf, the
+    deviation is N(0, sigma^2), reproducible for a seed and cast index, different across casts."""
+    ems, tris = sg.random_scene(510, n_tris=3000, n_emitters=2, gamma=32, chi=600, extent=6.0)
+    g = Grca(device=0, max_triangles=len(tris), max_rays=sg.n_rays_total(ems))
+    g.set_emitters(ems)
+    g.update_triangles(tris_to_float4(tris))
+    d0, t0 = [x.cpu().numpy() for x in g.cast()]
+    sigma = 0.05
+    g.set_distance_noise(sigma, seed=123)
+    d1, t1 = [x.cpu().numpy() for x in g.cast()]
+    d2, _ = [x.cpu().numpy() for x in g.cast()]
+    assert np.array_equal(t0, t1)
+    hit = t0 >= 0
+    assert hit.sum() > 5000 and np.all(np.isinf(d1[~hit]))
+    dev = (d1[hit].astype(np.float64) - d0[hit])
+    mask = d0[hit] > 10 * sigma   # away from the clamp at 0
+    dv = dev[mask]
+    assert abs(dv.mean()) < 4 * sigma / np.sqrt(dv.size) and abs(dv.std() / sigma - 1) < 0.05
+    assert not np.array_equal(d1, d2)
+    g2 = Grca(device=0, max_triangles=len(tris), max_rays=sg.n_rays_total(ems))
+    g2.set_emitters(ems)
+    g2.update_triangles(tris_to_float4(tris))
+    g2.cast()
+    g2.set_distance_noise(sigma, seed=123)
+    d3, _ = [x.cpu().numpy() for x in g2.cast()]
+    assert np.array_equal(d3.view(np.uint32), d1.view(np.uint32))   # same seed, same cast index
