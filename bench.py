@@ -263,6 +263,7 @@ def main():
     ap.add_argument("--car-scale", default=None, help="lo,hi per-axis car scale (C5 'large triangles' variant)")
     ap.add_argument("--split-refine", action="store_true", help="K2b and K4s as two kernels (A/B)")
     ap.add_argument("--l2-persist", action="store_true", help="A/B: persisting L2 window (opt-in)")
+    ap.add_argument("--no-packed", action="store_true", help="A/B: K2 without packed fp32x2 math")
     ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters"])
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 logic with several ranks on one GPU")
@@ -331,7 +332,7 @@ def main():
     n_rays = sg.n_rays_total(ems)
     n_rays_job = sg.n_rays_total(scene.w["emitters"])
     g = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays, debug_flags=G.PROFILE_KERNELS | (G.DEBUG_SPLIT_REFINE if args.split_refine else 0)
-             | (G.L2_PERSIST if args.l2_persist else 0),
+             | (G.L2_PERSIST if args.l2_persist else 0) | (G.DEBUG_NO_PACKED if args.no_packed else 0),
              small_max=args.small_max, nranks=world, rank=rank)
     g.set_emitters(ems)
     dist_out = torch.empty(n_rays, dtype=torch.float32, device=device)

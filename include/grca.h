@@ -62,6 +62,7 @@ enum {
     GRCA_DEBUG_SPLIT_REFINE = 16u,  /* run K2b (bounds) and K4s (small work) as two kernels instead of
                                        the fused refine+small kernel (A/B measurement, same results) */
     GRCA_DEBUG_NO_REFINE = 32u,     /* K3 keeps whole rectangle rows (no A7 per-channel refinement) */
+    GRCA_DEBUG_NO_PACKED = 128u,    /* K2 without the packed fp32x2 (two-emitter) path (A/B) */
     GRCA_L2_PERSIST = 64u           /* opt-in: reserve persisting L2 for the ray table + hit keys
                                        (raises cudaLimitPersistingL2CacheSize device-wide and sets a
                                        per-launch access-policy window on the gather kernels) */

@@ -67,6 +67,7 @@ struct KParams {
     unsigned long long *stats;
     int faces, nocull, force64, small_max, norefine;
     float area_eps2;             // (apparent-area eps)^2, 0 = off
+    int pairs_ok;                // all emitter frames orthonormal (packed fp32x2 K2 path)
     long long n_rays;
     const EmLite *lite;
     const unsigned char *lut;    // NULL -> binary search
@@ -246,11 +247,27 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const KParam
             const float emax = m2 * rsqrtf(m2) * (1.f + 1e-5f);   // triangle diameter (0 if degenerate)
             c_pairs += NE;
             unsigned chan = 0u;
+            int stv[NE];
+            if (P.nocull) {
+#pragma unroll
+                for (int e = 0; e < NE; ++e) stv[e] = CULL_KEEP;
+            } else if (P.pairs_ok) {   // both frames of every pair orthonormal: packed fp32x2 path
+#pragma unroll
+                for (int e = 0; e + 1 < NE; e += 2)
+                    quick_cull2(v, emax, EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base, sSin + EL.e[e + 1].sin_base,
+                                P.lut ? sLut + e * kLutBins : nullptr, P.lut ? sLut + (e + 1) * kLutBins : nullptr,
+                                stv[e], stv[e + 1]);
+                if (NE & 1)
+                    stv[NE - 1] = quick_cull(v, emax, EL.e[NE - 1], sSin + EL.e[NE - 1].sin_base,
+                                             P.lut ? sLut + (NE - 1) * kLutBins : nullptr);
+            } else {
+#pragma unroll
+                for (int e = 0; e < NE; ++e)
+                    stv[e] = quick_cull(v, emax, EL.e[e], sSin + EL.e[e].sin_base, P.lut ? sLut + e * kLutBins : nullptr);
+            }
 #pragma unroll
             for (int e = 0; e < NE; ++e) {
-                int st = P.nocull ? CULL_KEEP
-                                  : quick_cull(v, emax, EL.e[e], sSin + EL.e[e].sin_base,
-                                               P.lut ? sLut + e * kLutBins : nullptr);
+                int st = stv[e];
                 if (P.area_eps2 > 0.f && st == CULL_KEEP) {   // NEXT-f1 paper mode (approximate):
                     // apparent-area cull, PAPER.md:622-632 (recomputed per pair: paper mode only)
                     const f3 cen = {(v[0].x + v[1].x + v[2].x) * (1.f / 3.f), (v[0].y + v[1].y + v[2].y) * (1.f / 3.f),
@@ -1017,6 +1034,7 @@ struct grca_ctx {
     EmLitePack lite_pack{};
     cudaAccessPolicyWindow l2win{};
     float noise_sigma = 0.f;           // distance noise (K5), 0 = off
+    bool all_ortho = false;
     unsigned long long noise_seed = 0;   // persisting window over ray table + hits (num_bytes 0 = off)
     size_t k2f_smem = 0;
     int4 *d_large = nullptr;
@@ -1116,6 +1134,7 @@ KParams params(grca_t h) {
     P.norefine = (h->ci.debug_flags & GRCA_DEBUG_NO_REFINE) ? 1 : 0;
     P.small_max = std::min(1023, h->ci.small_max > 0 ? h->ci.small_max : 512);
     P.area_eps2 = h->ci.apparent_area_eps > 0.f ? h->ci.apparent_area_eps * h->ci.apparent_area_eps : 0.f;
+    P.pairs_ok = h->all_ortho && !(h->ci.debug_flags & GRCA_DEBUG_NO_PACKED) ? 1 : 0;
     P.n_rays = h->n_rays;
     P.lite = h->d_lite;
     P.lut = h->use_lut ? h->d_lut : nullptr;
@@ -1443,6 +1462,8 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     CK(cudaMemcpy(h->d_lite, lites.data(), sizeof(EmLite) * lites.size(), cudaMemcpyHostToDevice));
     if (use_lut) CK(cudaMemcpy(h->d_lut, lut.data(), sizeof(unsigned char) * lut.size(), cudaMemcpyHostToDevice));
     h->use_lut = use_lut;
+    h->all_ortho = true;
+    for (int n = 0; n < n_emitters; ++n) h->all_ortho = h->all_ortho && lites[n].ortho;
     h->n_em = n_emitters;
     h->st_dirty = h->st_set;   // cached static keys depend on the emitters
     h->n_sin = (int)sins.size();

@@ -110,6 +110,18 @@ __host__ __device__ __forceinline__ float fast_atan2(float y, float x) {
     return copysignf(a, y);
 }
 
+// atan(z) for |z| <= 1 with the same polynomial (|error| <= 2e-6 rad), odd symmetric
+__host__ __device__ __forceinline__ float poly_atan(float z) {
+    const float az = fabsf(z), z2 = az * az;
+    float p = -0.011710336431860924f;
+    p = p * z2 + 0.05262540653347969f;
+    p = p * z2 - 0.11640699207782745f;
+    p = p * z2 + 0.1935330331325531f;
+    p = p * z2 - 0.3326217532157898f;
+    p = p * z2 + 0.999977171421051f;
+    return copysignf(p * az, z);
+}
+
 // ----------------------------------------------------------------- A1 load --
 struct TriSrc {
     const float4 *v;
@@ -248,8 +260,36 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
         xn[k] = r2[k] * inv[k];
     }
     float slo = fminf(s[0], fminf(s[1], s[2])), shi = fmaxf(s[0], fmaxf(s[1], s[2]));
+    bool near_axis = false;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) near_axis |= (x[k].x * x[k].x + x[k].y * x[k].y) < kNearAxis2 * r2[k];
+    // Fast path (most survivors: far, small triangles).  In sensor coordinates every point of T is
+    // within diam of each vertex, so with rlb = max|x_k| - diam > 2 diam every chord subtends <= q =
+    // diam / rlb: edge interiors exceed the vertex elevations by <= q^2/8 and a pole inside T would
+    // force every |s_k| >= cos q >= 1 - q^2/2 (the K2 argument, now in x-space).
+    float e2m = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const f3 ev = subf(x[(k + 1) % 3], x[k]);
+        e2m = fmaxf(e2m, dotf(ev, ev));
+    }
+    const float diam = (e2m > 0.f ? e2m * rsqrtf(e2m) : 0.f) * (1.f + 1e-5f);
+    const float rlb_x = fmaxf(xn[0], fmaxf(xn[1], xn[2])) - diam;
+    bool fast = false;
+    float q2f = 0.f;
+    if (rlb_x > 2.f * diam && !near_axis) {
+        const float q = diam / rlb_x;
+        q2f = q * q;
+        fast = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2]))) < 1.f - 0.51f * q2f - 1e-5f;
+    }
+    bool pole = false;
+    float pad_e = 0.f;
+    bool longedge = false;
+    if (fast) {
+        pad_e = 0.13f * q2f;
+    } else {
     // pole containment: does the spin axis pass through T?  (2-D winding in the x_f x_r plane)
-    bool pos = false, neg = false, near_axis = false;
+    bool pos = false, neg = false;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const int k1 = (k + 1) % 3;
@@ -257,21 +297,18 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
         float eps = 9.f * kU * xn[k] * xn[k1];
         pos |= (w > eps);
         neg |= (w < -eps);
-        near_axis |= (x[k].x * x[k].x + x[k].y * x[k].y) < kNearAxis2 * r2[k];
     }
     // The axis can only meet T if T's horizontal projection straddles it on both coordinates
     // (this rejects degenerate, e.g. radial vertical, projections whose windings all round to ~0).
     const float tolb = 17.f * kU * fmaxf(xn[0], fmaxf(xn[1], xn[2]));
     const bool straddle = fminf(x[0].x, fminf(x[1].x, x[2].x)) <= tolb && fmaxf(x[0].x, fmaxf(x[1].x, x[2].x)) >= -tolb &&
                           fminf(x[0].y, fminf(x[1].y, x[2].y)) <= tolb && fmaxf(x[0].y, fmaxf(x[1].y, x[2].y)) >= -tolb;
-    const bool pole = straddle && !(pos && neg);
+    pole = straddle && !(pos && neg);
     if (pole) {
         if (shi > 0.f) shi = 1.f;
         if (slo < 0.f) slo = -1.f;
     }
     // interior extremes of edges: small arcs -> L^2/8 pad, long arcs -> great-circle extreme
-    float pad_e = 0.f;
-    bool longedge = false;
     f3 xh[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) xh[k] = scalef(x[k], inv[k]);
@@ -295,6 +332,7 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
             if (on_arc(x[k], x[k1], m, Tb)) slo = fminf(slo, -S);
         }
     }
+    }   // !fast
     const float pad = kPadS + pad_e + (longedge ? 1e-5f : 0.f);
     R.c_from = first_channel_ge(sinTab, E.gamma, lut, slo - pad);
     R.c_to = min(first_channel_gt(sinTab, E.gamma, lut, shi + pad), E.gamma) - 1;
@@ -305,6 +343,27 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
         R.r_lo = 0; R.r_len = E.chi; R.pole_rows = 0;
         return CULL_KEEP;
     }
+    float start, len;
+    bool arc_done = false;
+    if (fast) {   // arc from the centroid azimuth and the vertices' small angular offsets
+        const float cx = x[0].x + x[1].x + x[2].x, cy = x[0].y + x[1].y + x[2].y;
+        float dmin = 0.f, dmax = 0.f;
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float cr = cx * x[k].y - cy * x[k].x, dt = cx * x[k].x + cy * x[k].y;
+            ok = ok && dt > 0.f && fabsf(cr) < dt;
+            const float d = poly_atan(__fdividef(cr, dt));
+            dmin = k ? fminf(dmin, d) : d;
+            dmax = k ? fmaxf(dmax, d) : d;
+        }
+        if (ok) {
+            start = fast_atan2(cy, cx) + dmin;
+            len = dmax - dmin;
+            arc_done = true;
+        }
+    }
+    if (!arc_done) {
     float th[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) th[k] = fast_atan2(x[k].y, x[k].x);
@@ -315,10 +374,10 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
     t1 = fminf(fmaxf(t1, t0), t2);
     const float TWO_PI = 6.283185307179586f;
     float g01 = t1 - t0, g12 = t2 - t1, g20 = t0 + TWO_PI - t2;
-    float start, len;
     if (g20 >= g01 && g20 >= g12) { start = t0; len = t2 - t0; }
     else if (g01 >= g12) { start = t1; len = (t0 + TWO_PI) - t1; }
     else { start = t2; len = (t1 + TWO_PI) - t2; }
+    }   // !arc_done
     if (len > 3.1f) {   // arc near pi with the axis outside T only by rounding: be safe
         R.r_lo = 0; R.r_len = E.chi; R.pole_rows = 0;
         return CULL_KEEP;
@@ -490,6 +549,65 @@ __device__ __noinline__ int refine_row(const d3 x[3], double s_lo, double s_hi, 
         }
     }
     return cnt;
+}
+
+// Two emitters at once with packed fp32x2 arithmetic (sm_100 FADD2/FMUL2/FFMA2: two fp32 lanes
+// per FMA-pipe issue).  Same test, same bounds as quick_cull; used when both frames are orthonormal.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+__device__ __forceinline__ int quick_tail(const float s[3], float rmax, float emax, const EmLite &L, const float *sinT,
+                                          const unsigned char *lut) {
+    const float rlb = rmax - emax;
+    const bool range = rlb > L.lim;
+    const bool near = !(rlb > 2.f * emax);
+    const float q = __fdividef(emax, rlb);
+    const float q2 = q * q;
+    const float smax = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));
+    const bool pole = smax >= 1.f - 0.51f * q2 - 1e-5f;
+    const float pad = L.pad0 + 0.13f * q2;
+    const float lo = fminf(s[0], fminf(s[1], s[2])) - pad;
+    const float hi = fmaxf(s[0], fmaxf(s[1], s[2])) + pad;
+    float vj;
+    if (lut) {
+        int b = (int)((lo + 1.f) * (0.5f * kLutBins));
+        b = min(max(b, 0), kLutBins - 1);
+        int j = lut[b];
+        const float v0 = sinT[j], v1 = sinT[j + 1];
+        vj = v0 >= lo ? v0 : v1;
+        if (v1 < lo) {
+            j += 2;
+            while (sinT[j] < lo) ++j;
+            vj = sinT[j];
+        }
+    } else {
+        vj = sinT[lower_bound_f(sinT, L.gamma, lo)];
+    }
+    const bool keep = near || pole || vj <= hi;
+    return range ? CULL_RANGE : (keep ? CULL_KEEP : CULL_CHANNEL);
+}
+
+__device__ __forceinline__ void quick_cull2(const f3 v[3], float emax, const EmLite &L0, const EmLite &L1,
+                                            const float *sinT0, const float *sinT1, const unsigned char *lut0,
+                                            const unsigned char *lut1, int &st0, int &st1) {
+    const float2 nox = f2(-L0.o[0], -L1.o[0]), noy = f2(-L0.o[1], -L1.o[1]), noz = f2(-L0.o[2], -L1.o[2]);
+    const float2 ux = f2(L0.Au[0], L1.Au[0]), uy = f2(L0.Au[1], L1.Au[1]), uz = f2(L0.Au[2], L1.Au[2]);
+    float s0[3], s1[3], r0 = 0.f, r1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float2 ax = __fadd2_rn(f2(v[k].x, v[k].x), nox);
+        const float2 ay = __fadd2_rn(f2(v[k].y, v[k].y), noy);
+        const float2 az = __fadd2_rn(f2(v[k].z, v[k].z), noz);
+        const float2 w2 = __ffma2_rn(az, az, __ffma2_rn(ay, ay, __fmul2_rn(ax, ax)));
+        const float2 xu = __ffma2_rn(uz, az, __ffma2_rn(uy, ay, __fmul2_rn(ux, ax)));
+        const float2 iw = f2(rsqrtf(w2.x), rsqrtf(w2.y));
+        const float2 rr = __fmul2_rn(w2, iw), ss = __fmul2_rn(xu, iw);
+        s0[k] = ss.x;
+        s1[k] = ss.y;
+        r0 = fmaxf(r0, rr.x);
+        r1 = fmaxf(r1, rr.y);
+    }
+    st0 = quick_tail(s0, r0, emax, L0, sinT0, lut0);
+    st1 = quick_tail(s1, r1, emax, L1, sinT1, lut1);
 }
 
 // --------------------------------------------------- A6 setup + certified test --

@@ -20,6 +20,7 @@ FACES_TWO_SIDED, FACES_KEEP_POS, FACES_KEEP_NEG = 0, 1, 2
 DEBUG_COUNT_ALL_HITS, DEBUG_NO_CULL, PROFILE_KERNELS, DEBUG_FORCE_FP64, DEBUG_SPLIT_REFINE, DEBUG_NO_REFINE = (
     1, 2, 4, 8, 16, 32)
 L2_PERSIST = 64
+DEBUG_NO_PACKED = 128
 
 EXPORTS = [
     "grca_create", "grca_destroy", "grca_set_emitters", "grca_update_triangles", "grca_cast",
