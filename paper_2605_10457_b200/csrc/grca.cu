@@ -125,7 +125,7 @@ __global__ void k_init(unsigned long long *hits, unsigned *allhits, long long n,
 // Lean and dense: per triangle (fused K1 load) x per emitter, the O(1) elevation pre-test
 // (quick_cull).  Survivors are compacted per 256-triangle tile in shared memory and written to
 // the tile's own slot of the survivor buffer (no global atomics); K2b refines them.
-__global__ void __launch_bounds__(K2_THREADS) k_cull(const KParams P) {
+__global__ void __launch_bounds__(K2_THREADS) k_cull(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     EmLite *sL = reinterpret_cast<EmLite *>(smem);
     float *sSin = reinterpret_cast<float *>(sL + P.n_em);
@@ -216,7 +216,7 @@ struct EmLitePack {
 };
 
 template <int NE>
-__global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const KParams P, const EmLitePack EL) {
+__global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid_constant__ KParams P, const EmLitePack EL) {
     extern __shared__ __align__(16) unsigned char smem[];
     float *sSin = reinterpret_cast<float *>(smem);
     unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
@@ -335,7 +335,7 @@ __device__ __forceinline__ unsigned long long pack_small(int c_from, int nrows, 
 __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev &E, long long t, int row0, int nrows, int lo,
                                                    int len);
 
-__global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
+__global__ void __launch_bounds__(K2_THREADS) k_refine(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     EmDev *sE = reinterpret_cast<EmDev *>(smem);
     float *sSin = reinterpret_cast<float *>(sE + P.n_em);
@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const KParams P) {
 // One warp per tile: lanes compute the certified setup of their small rectangles (one pair per
 // lane, into shared-memory slots), then the warp expands all items of the 32 pairs with an
 // inclusive prefix scan (A5) and tests them (A6) 32 at a time -- no lane idles on a short pair.
-__global__ void __launch_bounds__(K2_THREADS) k_small(const KParams P) {
+__global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     EmDev *sE = reinterpret_cast<EmDev *>(smem);
     float *sSlot = reinterpret_cast<float *>(sE + P.n_em);
@@ -531,7 +531,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const KParams P) {
                         cnt[ST_FP64]++;
                         f3 w[3];
                         load_tri(P.tri, (long long)__float_as_int(sl[SF_TRI * 32]), w);
-                        r = test_exact(w, em_o(EO), d, EO.dmax, P.faces, th);
+                        r = test_exact_r(w, em_o(EO), d, EO.dmax, P.faces, th);
                     }
                     if (r == 1) {
                         cnt[ST_HITS]++;
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const KParams P) {
 // (cull_pair), certified setup of small rectangles into shared-memory float4 slots, then the
 // warp expands all items of its small rectangles with a prefix scan (A5) and tests them 32 at a
 // time (A6).  Large rectangles go to the large list (K3/K4).  One vertex fetch per survivor.
-__global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KParams P) {
+__global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4 *sSlot = reinterpret_cast<float4 *>(smem);   // [warp][6][32]
     int *sExcl = reinterpret_cast<int *>(sSlot + (KF_THREADS / 32) * 6 * 32);   // [warp][32]
@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     float4 *slot = sSlot + wib * 6 * 32;
     int *excl = sExcl + wib * 32;
-    unsigned setup64 = 0, nhits = 0, nfp64 = 0;
+    unsigned setup64 = 0;
     // stats: per-lane category codes, counted warp-aggregated into shared memory at convergent
     // points (no per-thread counter registers)
     enum { C_NONE = 0, C_SMALL, C_LARGE, C_OVF, C_RANGE, C_CHAN, C_AZI, C_DEGEN };
@@ -679,46 +679,34 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
         excl[lane] = incl - my;
         const int total = __shfl_sync(FULL, incl, 31);
         __syncwarp();
-        // KU candidates per lane in flight: resolve owners and ray indices, issue all ray loads,
-        // then test (memory-level parallelism for the L2-resident ray table)
-        constexpr int KU = 1;
-        for (int b = 0; b < total; b += 32 * KU) {
-            int owv[KU], gv[KU];
-            float4 dv[KU];
+        // one candidate per lane per iteration: resolve the owner (binary search of the inclusive
+        // scan), the ray index, then the certified test (scalar state only: nothing to local memory)
+        for (int b = 0; b < total; b += 32) {
+            const int qi = b + lane;
+            int ow = 0;
 #pragma unroll
-            for (int u = 0; u < KU; ++u) {
-                const int qi = b + u * 32 + lane;
-                int ow = 0;
-#pragma unroll
-                for (int s = 16; s > 0; s >>= 1) {
-                    const int vv = __shfl_sync(FULL, incl, ow + s - 1);
-                    if (vv <= qi) ow += s;
-                }
-                owv[u] = ow;
-                gv[u] = -1;
-                if (qi < total) {
-                    const float4 r5 = slot[5 * 32 + ow];
-                    const EmDev &EO = sE[__float_as_int(slot[4 * 32 + ow].w)];
-                    const int local = qi - excl[ow];
-                    const int len = __float_as_int(r5.z);
-                    int row = (int)(((float)local + 0.5f) * r5.w);
-                    int col = local - row * len;
-                    if (col < 0) { --row; col += len; }
-                    if (col >= len) { ++row; col -= len; }
-                    const int j = __float_as_int(r5.x) + row;
-                    int i = __float_as_int(r5.y) + col;
-                    if (i >= EO.chi) i -= EO.chi;
-                    gv[u] = EO.ray_base + j * EO.chi + i;
-                    dv[u] = __ldg(P.raytab + gv[u]);
-                }
+            for (int s = 16; s > 0; s >>= 1) {
+                const int vv = __shfl_sync(FULL, incl, ow + s - 1);
+                if (vv <= qi) ow += s;
             }
-#pragma unroll
-            for (int u = 0; u < KU; ++u) {
-                if (gv[u] < 0) continue;
-                const int ow = owv[u];
-                const float4 r0 = slot[0 * 32 + ow], r1 = slot[1 * 32 + ow], r2 = slot[2 * 32 + ow],
-                             r3 = slot[3 * 32 + ow], r4 = slot[4 * 32 + ow];
+            bool hit = false, fb = false;
+            if (qi < total) {
+                const float4 r5 = slot[5 * 32 + ow];
+                const float4 r4 = slot[4 * 32 + ow];
                 const EmDev &EO = sE[__float_as_int(r4.w)];
+                const int local = qi - excl[ow];
+                const int len = __float_as_int(r5.z);
+                int row = (int)(((float)local + 0.5f) * r5.w);
+                int col = local - row * len;
+                if (col < 0) { --row; col += len; }
+                if (col >= len) { ++row; col -= len; }
+                const int j = __float_as_int(r5.x) + row;
+                int i = __float_as_int(r5.y) + col;
+                if (i >= EO.chi) i -= EO.chi;
+                const int g = EO.ray_base + j * EO.chi + i;
+                const float4 d = __ldg(P.raytab + g);
+                const float4 r0 = slot[0 * 32 + ow], r1 = slot[1 * 32 + ow], r2 = slot[2 * 32 + ow],
+                             r3 = slot[3 * 32 + ow];
                 Setup Q;
                 Q.n0 = {r0.x, r0.y, r0.z};
                 Q.n1 = {r1.x, r1.y, r1.z};
@@ -728,30 +716,31 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const KPar
                 Q.habs = r3.w;
                 Q.TN = r4.x;
                 float th = 0.f;
-                int r = P.force64 ? 2 : test_fast(dv[u], Q, EO.dmax_lo, EO.dmax_hi, th);
-                if (r == 2) {
-                    ++nfp64;
+                int r = P.force64 ? 2 : test_fast(d, Q, EO.dmax_lo, EO.dmax_hi, th);
+                fb = r == 2;
+                if (r == 2) {   // rare: reload the ray (keeping d live into the fp64 code spills it)
                     f3 wv[3];
                     load_tri(P.tri, (long long)__float_as_int(r4.z), wv);
-                    r = test_exact(wv, em_o(EO), dv[u], EO.dmax, P.faces, th);
+                    const float4 d2 = __ldcg(P.raytab + g);
+                    r = test_exact_r<true>(wv, em_o(EO), d2, EO.dmax, P.faces, th);
                 }
                 if (r == 1) {
-                    ++nhits;
-                    record_hit(P.hits, P.allhits, gv[u], th, __float_as_uint(r4.y));
+                    hit = true;
+                    record_hit(P.hits, P.allhits, g, th, __float_as_uint(r4.y));
                 }
+            }
+            // hit / fp64 counts warp-aggregated per iteration (no per-thread counter live across
+            // the loop: at the 64-register cap it would be spilled to local memory)
+            const unsigned hm = __ballot_sync(FULL, hit), fm = __ballot_sync(FULL, fb);
+            if (lane == 0 && (hm | fm)) {
+                if (hm) atomicAdd(acc + ST_HITS, (unsigned)__popc(hm));
+                if (fm) atomicAdd(acc + ST_FP64, (unsigned)__popc(fm));
             }
         }
         __syncwarp();
         w = __shfl_sync(FULL, wn, 0);
     }
     (void)setup64;
-    {
-        const unsigned h = __reduce_add_sync(FULL, nhits), f = __reduce_add_sync(FULL, nfp64);
-        if (lane == 0) {
-            if (h) atomicAdd(acc + ST_HITS, (unsigned)h);
-            if (f) atomicAdd(acc + ST_FP64, (unsigned)f);
-        }
-    }
     __syncthreads();
     if (threadIdx.x < ST_COUNT && acc[threadIdx.x]) atomicAdd(P.stats + threadIdx.x, (unsigned long long)acc[threadIdx.x]);
 }
@@ -802,7 +791,7 @@ __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev
                 float th;
                 ++items;
                 int res = P.force64 ? 2 : test_fast(d, S, E.dmax_lo, E.dmax_hi, th);
-                if (res == 2) { ++fp64; res = test_exact(v, em_o(E), d, E.dmax, P.faces, th); }
+                if (res == 2) { ++fp64; res = test_exact_r(v, em_o(E), d, E.dmax, P.faces, th); }
                 if (res == 1) { ++hits; record_hit(P.hits, P.allhits, g, th, id); }
             }
     }
@@ -811,7 +800,7 @@ __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev
     atomicAdd(P.stats + ST_HITS, (unsigned long long)hits);
 }
 
-__global__ void __launch_bounds__(256) k_bin(const KParams P) {
+__global__ void __launch_bounds__(256) k_bin(const __grid_constant__ KParams P) {
     // one warp per large rectangle; lanes = channel rows.  A7 refines each non-pole row of a
     // partial-arc rectangle to its exact (padded) ray range; rows become chunks of <= kColMax rays.
     __shared__ unsigned long long acc[ST_COUNT];
@@ -905,7 +894,7 @@ __global__ void __launch_bounds__(256) k_bin(const KParams P) {
 }
 
 // ------------------------------------------------------------ K4 intersect --
-__global__ void __launch_bounds__(K4_THREADS) k_isect(const KParams P) {
+__global__ void __launch_bounds__(K4_THREADS) k_isect(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     EmDev *sE = reinterpret_cast<EmDev *>(smem);
     __shared__ unsigned long long acc[ST_COUNT];
@@ -953,7 +942,7 @@ __global__ void __launch_bounds__(K4_THREADS) k_isect(const KParams P) {
             int r = P.force64 ? 2 : test_fast(d, S, E.dmax_lo, E.dmax_hi, th);
             if (r == 2) {
                 cnt[ST_FP64]++;
-                r = test_exact(v, em_o(E), d, E.dmax, P.faces, th);
+                r = test_exact_r(v, em_o(E), d, E.dmax, P.faces, th);
             }
             if (r == 1) {
                 cnt[ST_HITS]++;

@@ -693,8 +693,12 @@ __device__ __forceinline__ int test_fast(float4 d4, const Setup &S, float dmax_l
     return 2;
 }
 
-// fp64 decision (canonical edges, closed triangle, 0 < t <= dmax).  1 = hit.
-__device__ __noinline__ int test_exact(const f3 v[3], f3 o, float4 d4, double dmax, int faces, float &tout) {
+// fp64 decision (canonical edges, closed triangle, 0 < t <= dmax).  Returns the fp32-rounded t
+// of a hit, -1 otherwise.  All arguments by value and no out-parameter: the call must not force
+// the caller's ray / vertices / t through local memory (it sits inside the hot item loops).
+template <bool kInline>
+__device__ __forceinline__ float test_exact_body(f3 v0, f3 v1, f3 v2, f3 o, float4 d4, double dmax, int faces) {
+    const f3 v[3] = {v0, v1, v2};
     const d3 d = {(double)d4.x, (double)d4.y, (double)d4.z};
     const d3 O = tod(o);
     double F[3];
@@ -710,16 +714,27 @@ __device__ __noinline__ int test_exact(const f3 v[3], f3 o, float4 d4, double dm
     d3 V0 = tod(v[0]);
     d3 N = crossd(subd(tod(v[1]), V0), subd(tod(v[2]), V0));
     double h = dotd(N, subd(V0, O));
-    if (!(h > 0.0 || h < 0.0)) return 0;
-    if ((faces == 1 && h < 0.0) || (faces == 2 && h > 0.0)) return 0;
+    if (!(h > 0.0 || h < 0.0)) return -1.f;
+    if ((faces == 1 && h < 0.0) || (faces == 2 && h > 0.0)) return -1.f;
     if (h < 0.0) { F[0] = -F[0]; F[1] = -F[1]; F[2] = -F[2]; }
-    if (F[0] < 0.0 || F[1] < 0.0 || F[2] < 0.0) return 0;
+    if (F[0] < 0.0 || F[1] < 0.0 || F[2] < 0.0) return -1.f;
     double dN = dotd(d, N);
-    if (!(dN > 0.0 || dN < 0.0)) return 0;
+    if (!(dN > 0.0 || dN < 0.0)) return -1.f;
     double t = h / dN;
-    if (!(t > 0.0 && t <= dmax)) return 0;
-    tout = (float)t;
-    return 1;
+    if (!(t > 0.0 && t <= dmax)) return -1.f;
+    return (float)t;   // >= +0: a hit (the caller tests r >= 0)
+}
+__device__ __noinline__ float test_exact(f3 v0, f3 v1, f3 v2, f3 o, float4 d4, double dmax, int faces) {
+    return test_exact_body<false>(v0, v1, v2, o, d4, dmax, faces);
+}
+// 1 = hit (t set), 0 = miss: adapter for the call sites.  kInline expands the fp64 test at the
+// call site (no CALL: nothing live across an ABI call has to be spilled around it).
+template <bool kInline = false>
+__device__ __forceinline__ int test_exact_r(const f3 v[3], f3 o, float4 d4, double dmax, int faces, float &t) {
+    const float r = kInline ? test_exact_body<true>(v[0], v[1], v[2], o, d4, dmax, faces)
+                            : test_exact(v[0], v[1], v[2], o, d4, dmax, faces);
+    if (r >= 0.f) { t = r; return 1; }
+    return 0;
 }
 
 // Closest-hit update on the packed key (fp32 t bits << 32 | id).  t > 0 so the raw bits
