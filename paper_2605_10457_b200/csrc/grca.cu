@@ -215,6 +215,58 @@ struct EmLitePack {
     EmLite e[kFixedEm];
 };
 
+// K2 per-triangle test (A1 load + A2-A3 pre-test for all NE emitters): keep / range bit masks,
+// channel-culled count; c_area counts paper-mode apparent-area culls.
+template <int NE>
+__device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, const float *sSin,
+                                       const unsigned char *sLut, long long t, unsigned &keep, unsigned &rng,
+                                       unsigned &chan, unsigned &c_area) {
+    f3 v[3];
+    load_tri(P.tri, t, v);   // A1 (fused K1)
+    const float l0 = (v[1].x - v[0].x) * (v[1].x - v[0].x) + (v[1].y - v[0].y) * (v[1].y - v[0].y) +
+                     (v[1].z - v[0].z) * (v[1].z - v[0].z);
+    const float l1 = (v[2].x - v[1].x) * (v[2].x - v[1].x) + (v[2].y - v[1].y) * (v[2].y - v[1].y) +
+                     (v[2].z - v[1].z) * (v[2].z - v[1].z);
+    const float l2 = (v[0].x - v[2].x) * (v[0].x - v[2].x) + (v[0].y - v[2].y) * (v[0].y - v[2].y) +
+                     (v[0].z - v[2].z) * (v[0].z - v[2].z);
+    const float m2 = fmaxf(l0, fmaxf(l1, l2));
+    const float emax = m2 * rsqrtf(m2) * (1.f + 1e-5f);   // triangle diameter (0 if degenerate)
+    int stv[NE];
+    if (P.nocull) {
+#pragma unroll
+        for (int e = 0; e < NE; ++e) stv[e] = CULL_KEEP;
+    } else if (P.pairs_ok) {   // all frames orthonormal: packed fp32x2 path
+#pragma unroll
+        for (int e = 0; e + 1 < NE; e += 2)
+            quick_cull2(v, emax, EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base, sSin + EL.e[e + 1].sin_base,
+                        P.lut ? sLut + e * kLutBins : nullptr, P.lut ? sLut + (e + 1) * kLutBins : nullptr,
+                        stv[e], stv[e + 1]);
+        if (NE & 1)
+            stv[NE - 1] = quick_cull(v, emax, EL.e[NE - 1], sSin + EL.e[NE - 1].sin_base,
+                                     P.lut ? sLut + (NE - 1) * kLutBins : nullptr);
+    } else {
+#pragma unroll
+        for (int e = 0; e < NE; ++e)
+            stv[e] = quick_cull(v, emax, EL.e[e], sSin + EL.e[e].sin_base, P.lut ? sLut + e * kLutBins : nullptr);
+    }
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+        int st = stv[e];
+        if (P.area_eps2 > 0.f && st == CULL_KEEP) {   // NEXT-f1 paper mode (approximate):
+            // apparent-area cull, PAPER.md:622-632 (recomputed per pair: paper mode only)
+            const f3 cen = {(v[0].x + v[1].x + v[2].x) * (1.f / 3.f), (v[0].y + v[1].y + v[2].y) * (1.f / 3.f),
+                            (v[0].z + v[1].z + v[2].z) * (1.f / 3.f)};
+            const f3 hN = scalef(crossf(subf(v[1], v[0]), subf(v[2], v[0])), 0.5f);   // A_T * n
+            const f3 co = {cen.x - EL.e[e].o[0], cen.y - EL.e[e].o[1], cen.z - EL.e[e].o[2]};
+            const float an = dotf(hN, co), d2 = dotf(co, co);
+            if (an * an < P.area_eps2 * d2 * d2 * d2) { st = CULL_AREA; ++c_area; }
+        }
+        keep |= (st == CULL_KEEP ? 1u : 0u) << e;
+        rng |= (st == CULL_RANGE ? 1u : 0u) << e;
+        chan += (st == CULL_CHANNEL);
+    }
+}
+
 template <int NE>
 __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid_constant__ KParams P, const EmLitePack EL) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -235,52 +287,9 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid
         const long long t = tile * K2_THREADS + threadIdx.x;
         unsigned keep = 0u, rng = 0u;
         if (t < P.n_tri) {
-            f3 v[3];
-            load_tri(P.tri, t, v);   // A1 (fused K1)
-            const float l0 = (v[1].x - v[0].x) * (v[1].x - v[0].x) + (v[1].y - v[0].y) * (v[1].y - v[0].y) +
-                             (v[1].z - v[0].z) * (v[1].z - v[0].z);
-            const float l1 = (v[2].x - v[1].x) * (v[2].x - v[1].x) + (v[2].y - v[1].y) * (v[2].y - v[1].y) +
-                             (v[2].z - v[1].z) * (v[2].z - v[1].z);
-            const float l2 = (v[0].x - v[2].x) * (v[0].x - v[2].x) + (v[0].y - v[2].y) * (v[0].y - v[2].y) +
-                             (v[0].z - v[2].z) * (v[0].z - v[2].z);
-            const float m2 = fmaxf(l0, fmaxf(l1, l2));
-            const float emax = m2 * rsqrtf(m2) * (1.f + 1e-5f);   // triangle diameter (0 if degenerate)
-            c_pairs += NE;
             unsigned chan = 0u;
-            int stv[NE];
-            if (P.nocull) {
-#pragma unroll
-                for (int e = 0; e < NE; ++e) stv[e] = CULL_KEEP;
-            } else if (P.pairs_ok) {   // both frames of every pair orthonormal: packed fp32x2 path
-#pragma unroll
-                for (int e = 0; e + 1 < NE; e += 2)
-                    quick_cull2(v, emax, EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base, sSin + EL.e[e + 1].sin_base,
-                                P.lut ? sLut + e * kLutBins : nullptr, P.lut ? sLut + (e + 1) * kLutBins : nullptr,
-                                stv[e], stv[e + 1]);
-                if (NE & 1)
-                    stv[NE - 1] = quick_cull(v, emax, EL.e[NE - 1], sSin + EL.e[NE - 1].sin_base,
-                                             P.lut ? sLut + (NE - 1) * kLutBins : nullptr);
-            } else {
-#pragma unroll
-                for (int e = 0; e < NE; ++e)
-                    stv[e] = quick_cull(v, emax, EL.e[e], sSin + EL.e[e].sin_base, P.lut ? sLut + e * kLutBins : nullptr);
-            }
-#pragma unroll
-            for (int e = 0; e < NE; ++e) {
-                int st = stv[e];
-                if (P.area_eps2 > 0.f && st == CULL_KEEP) {   // NEXT-f1 paper mode (approximate):
-                    // apparent-area cull, PAPER.md:622-632 (recomputed per pair: paper mode only)
-                    const f3 cen = {(v[0].x + v[1].x + v[2].x) * (1.f / 3.f), (v[0].y + v[1].y + v[2].y) * (1.f / 3.f),
-                                    (v[0].z + v[1].z + v[2].z) * (1.f / 3.f)};
-                    const f3 hN = scalef(crossf(subf(v[1], v[0]), subf(v[2], v[0])), 0.5f);   // A_T * n
-                    const f3 co = {cen.x - EL.e[e].o[0], cen.y - EL.e[e].o[1], cen.z - EL.e[e].o[2]};
-                    const float an = dotf(hN, co), d2 = dotf(co, co);
-                    if (an * an < P.area_eps2 * d2 * d2 * d2) { st = CULL_AREA; ++c_area; }
-                }
-                keep |= (st == CULL_KEEP ? 1u : 0u) << e;
-                rng |= (st == CULL_RANGE ? 1u : 0u) << e;
-                chan += (st == CULL_CHANNEL);
-            }
+            k2_tri<NE>(P, EL, sSin, sLut, t, keep, rng, chan, c_area);
+            c_pairs += NE;
             c_chan += chan;
         }
         const int cntk = __popc(keep);
@@ -551,6 +560,167 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KP
 // (cull_pair), certified setup of small rectangles into shared-memory float4 slots, then the
 // warp expands all items of its small rectangles with a prefix scan (A5) and tests them 32 at a
 // time (A6).  Large rectangles go to the large list (K3/K4).  One vertex fetch per survivor.
+// One round of the fused refine + small expansion (A4-A6) for up to 32 survivor entries
+// (tri << 8 | emitter, one per lane, valid lanes only): exact rectangle (cull_pair), small
+// rectangles set up and expanded over the warp (prefix scan), large ones appended to the large
+// list.  Warp-collective; slot / excl are this warp's shared-memory staging areas.
+__device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, const float *sSin,
+                                             const unsigned char *sLut, float4 *slot, int *excl, unsigned *acc,
+                                             int lane, bool valid, unsigned long long ent) {
+    enum { C_NONE = 0, C_SMALL, C_LARGE, C_OVF, C_RANGE, C_CHAN, C_AZI, C_DEGEN };
+    unsigned setup64 = 0;
+    int my = 0, e = 0, cat = C_NONE;
+    bool sat = false, bat = false;   // paper classification counters
+    long long t = 0;
+    Rect R;
+    bool large = false;
+    if (valid) {
+        e = (int)(ent & 255u);
+        t = (long long)(ent >> 8);
+        f3 v[3];
+        load_tri(P.tri, t, v);
+        const EmDev &E = sE[e];
+        const int st = cull_pair(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
+                                 P.nocull != 0, R);
+        if (st == CULL_KEEP) {
+            // Eq. sat_cond with (gamma_T, chi_T) = (64, 64); all-CW = the arc does not wrap the seam
+            const bool wraps = R.r_len >= E.chi || R.r_lo + R.r_len > E.chi || R.pole_rows;
+            sat = !wraps && (R.c_to - R.c_from + 1) <= 64 && R.r_len <= 64;
+            bat = !sat;
+            const long long items = rect_items(R, E);
+            if (items <= P.small_max && !R.pole_rows) {
+                Setup S;
+                if (make_setup(v, em_o(E), P.faces, S, setup64)) {
+                    my = (int)items;
+                    cat = C_SMALL;
+                    slot[0 * 32 + lane] = make_float4(S.n0.x, S.n0.y, S.n0.z, S.B0);
+                    slot[1 * 32 + lane] = make_float4(S.n1.x, S.n1.y, S.n1.z, S.B1);
+                    slot[2 * 32 + lane] = make_float4(S.n2.x, S.n2.y, S.n2.z, S.B2);
+                    slot[3 * 32 + lane] = make_float4(S.N.x, S.N.y, S.N.z, S.habs);
+                    slot[4 * 32 + lane] = make_float4(S.TN, __uint_as_float(tri_id(P.tri, t)),
+                                                      __int_as_float((int)t), __int_as_float(e));
+                    slot[5 * 32 + lane] = make_float4(__int_as_float(R.c_from), __int_as_float(R.r_lo),
+                                                      __int_as_float(R.r_len), 1.f / (float)R.r_len);
+                } else {
+                    cat = C_DEGEN;
+                }
+            } else {
+                large = true;
+            }
+        } else cat = st == CULL_RANGE ? C_RANGE : st == CULL_CHANNEL ? C_CHAN : st == CULL_AZIMUTH ? C_AZI : C_DEGEN;
+    }
+    const unsigned lm = __ballot_sync(FULL, large);
+    if (lm) {
+        const int leader = __ffs(lm) - 1;
+        unsigned base = 0;
+        if (lane == leader) base = atomicAdd(P.n_large, (unsigned)__popc(lm));
+        base = __shfl_sync(FULL, base, leader);
+        if (large) {
+            const long long pos = (long long)base + __popc(lm & ((1u << lane) - 1u));
+            if (pos < P.cap_large) {
+                P.large[pos] = make_int4((int)t, e | (R.c_from << 8), R.c_to,
+                                         (int)((unsigned)R.r_lo | ((unsigned)R.r_len << 16)));
+                cat = C_LARGE;
+            } else {   // capacity fallback: intersect here (slow, never dropped)
+                cat = C_OVF;
+                if (R.pole_rows) { R.r_lo = 0; R.r_len = sE[e].chi; }
+                intersect_rect_serial(P, sE[e], t, R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len);
+            }
+        }
+    }
+    {   // warp-aggregated stats of this round (lane 0 -> shared memory)
+        const unsigned ms = __ballot_sync(FULL, cat == C_SMALL), ml = __ballot_sync(FULL, cat == C_LARGE),
+                       mo = __ballot_sync(FULL, cat == C_OVF), mr = __ballot_sync(FULL, cat == C_RANGE),
+                       mc = __ballot_sync(FULL, cat == C_CHAN), ma = __ballot_sync(FULL, cat == C_AZI),
+                       md = __ballot_sync(FULL, cat == C_DEGEN);
+        const unsigned items = __reduce_add_sync(FULL, (unsigned)my);
+        const unsigned msat = __ballot_sync(FULL, sat), mbat = __ballot_sync(FULL, bat);
+        if (lane == 0) {
+            if (ms | ml | mo) atomicAdd(acc + ST_SURV, (unsigned)(__popc(ms) + __popc(ml) + __popc(mo)));
+            if (ms) atomicAdd(acc + ST_SMALL, (unsigned)__popc(ms));
+            if (items) atomicAdd(acc + ST_ITEMS_SMALL, (unsigned)items);
+            if (ml) atomicAdd(acc + ST_LARGE, (unsigned)__popc(ml));
+            if (mo) atomicAdd(acc + ST_OVF_LARGE, (unsigned)__popc(mo));
+            if (mr) atomicAdd(acc + ST_RANGE, (unsigned)__popc(mr));
+            if (mc) atomicAdd(acc + ST_CHANNEL, (unsigned)__popc(mc));
+            if (ma) atomicAdd(acc + ST_AZIMUTH, (unsigned)__popc(ma));
+            if (md) atomicAdd(acc + ST_DEGEN, (unsigned)__popc(md));
+            if (msat) atomicAdd(acc + ST_SAT, (unsigned)__popc(msat));
+            if (mbat) atomicAdd(acc + ST_BAT, (unsigned)__popc(mbat));
+        }
+    }
+    // A5: warp-level prefix-scan work expansion
+    int incl = my;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+    }
+    excl[lane] = incl - my;
+    const int total = __shfl_sync(FULL, incl, 31);
+    __syncwarp();
+    // one candidate per lane per iteration: resolve the owner (binary search of the inclusive
+    // scan), the ray index, then the certified test (scalar state only: nothing to local memory)
+    for (int b = 0; b < total; b += 32) {
+        const int qi = b + lane;
+        int ow = 0;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            const int vv = __shfl_sync(FULL, incl, ow + s - 1);
+            if (vv <= qi) ow += s;
+        }
+        bool hit = false, fb = false;
+        if (qi < total) {
+            const float4 r5 = slot[5 * 32 + ow];
+            const float4 r4 = slot[4 * 32 + ow];
+            const EmDev &EO = sE[__float_as_int(r4.w)];
+            const int local = qi - excl[ow];
+            const int len = __float_as_int(r5.z);
+            int row = (int)(((float)local + 0.5f) * r5.w);
+            int col = local - row * len;
+            if (col < 0) { --row; col += len; }
+            if (col >= len) { ++row; col -= len; }
+            const int j = __float_as_int(r5.x) + row;
+            int i = __float_as_int(r5.y) + col;
+            if (i >= EO.chi) i -= EO.chi;
+            const int g = EO.ray_base + j * EO.chi + i;
+            const float4 d = __ldg(P.raytab + g);
+            const float4 r0 = slot[0 * 32 + ow], r1 = slot[1 * 32 + ow], r2 = slot[2 * 32 + ow],
+                         r3 = slot[3 * 32 + ow];
+            Setup Q;
+            Q.n0 = {r0.x, r0.y, r0.z};
+            Q.n1 = {r1.x, r1.y, r1.z};
+            Q.n2 = {r2.x, r2.y, r2.z};
+            Q.B0 = r0.w; Q.B1 = r1.w; Q.B2 = r2.w;
+            Q.N = {r3.x, r3.y, r3.z};
+            Q.habs = r3.w;
+            Q.TN = r4.x;
+            float th = 0.f;
+            int r = P.force64 ? 2 : test_fast(d, Q, EO.dmax_lo, EO.dmax_hi, th);
+            fb = r == 2;
+            if (r == 2) {   // rare: reload the ray (keeping d live into the fp64 code spills it)
+                f3 wv[3];
+                load_tri(P.tri, (long long)__float_as_int(r4.z), wv);
+                const float4 d2 = __ldcg(P.raytab + g);
+                r = test_exact_r<true>(wv, em_o(EO), d2, EO.dmax, P.faces, th);
+            }
+            if (r == 1) {
+                hit = true;
+                record_hit(P.hits, P.allhits, g, th, __float_as_uint(r4.y));
+            }
+        }
+        // hit / fp64 counts warp-aggregated per iteration (no per-thread counter live across
+        // the loop: at the 64-register cap it would be spilled to local memory)
+        const unsigned hm = __ballot_sync(FULL, hit), fm = __ballot_sync(FULL, fb);
+        if (lane == 0 && (hm | fm)) {
+            if (hm) atomicAdd(acc + ST_HITS, (unsigned)__popc(hm));
+            if (fm) atomicAdd(acc + ST_FP64, (unsigned)__popc(fm));
+        }
+    }
+    (void)setup64;
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4 *sSlot = reinterpret_cast<float4 *>(smem);   // [warp][6][32]
@@ -573,10 +743,6 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     float4 *slot = sSlot + wib * 6 * 32;
     int *excl = sExcl + wib * 32;
-    unsigned setup64 = 0;
-    // stats: per-lane category codes, counted warp-aggregated into shared memory at convergent
-    // points (no per-thread counter registers)
-    enum { C_NONE = 0, C_SMALL, C_LARGE, C_OVF, C_RANGE, C_CHAN, C_AZI, C_DEGEN };
     const unsigned ns = *P.n_surv;
     const unsigned nr = (ns + 31) >> 5;   // dense rounds of 32 survivors
     // dynamic round fetching (one global atomic per warp per round): no tail imbalance
@@ -586,161 +752,11 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
     for (; w < nr;) {
         unsigned wn = 0;
         if (lane == 0) wn = atomicAdd(P.n_surv + 2, 1u);   // next round, fetched early (latency hidden)
-        const int n = (int)ns;
-        const int idx = (int)(w * 32u) + lane;
-        int my = 0, e = 0, cat = C_NONE;
-        bool sat = false, bat = false;   // paper classification counters
-        long long t = 0;
-        Rect R;
-        bool large = false;
-        if (idx < n) {
-            const unsigned long long ent = __ldcs(P.surv + idx);
-            e = (int)(ent & 255u);
-            t = (long long)(ent >> 8);
-            f3 v[3];
-            load_tri(P.tri, t, v);
-            const EmDev &E = sE[e];
-            const int st = cull_pair(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
-                                     P.nocull != 0, R);
-            if (st == CULL_KEEP) {
-                // Eq. sat_cond with (gamma_T, chi_T) = (64, 64); all-CW = the arc does not wrap the seam
-                const bool wraps = R.r_len >= E.chi || R.r_lo + R.r_len > E.chi || R.pole_rows;
-                sat = !wraps && (R.c_to - R.c_from + 1) <= 64 && R.r_len <= 64;
-                bat = !sat;
-                const long long items = rect_items(R, E);
-                if (items <= P.small_max && !R.pole_rows) {
-                    Setup S;
-                    if (make_setup(v, em_o(E), P.faces, S, setup64)) {
-                        my = (int)items;
-                        cat = C_SMALL;
-                        slot[0 * 32 + lane] = make_float4(S.n0.x, S.n0.y, S.n0.z, S.B0);
-                        slot[1 * 32 + lane] = make_float4(S.n1.x, S.n1.y, S.n1.z, S.B1);
-                        slot[2 * 32 + lane] = make_float4(S.n2.x, S.n2.y, S.n2.z, S.B2);
-                        slot[3 * 32 + lane] = make_float4(S.N.x, S.N.y, S.N.z, S.habs);
-                        slot[4 * 32 + lane] = make_float4(S.TN, __uint_as_float(tri_id(P.tri, t)),
-                                                          __int_as_float((int)t), __int_as_float(e));
-                        slot[5 * 32 + lane] = make_float4(__int_as_float(R.c_from), __int_as_float(R.r_lo),
-                                                          __int_as_float(R.r_len), 1.f / (float)R.r_len);
-                    } else {
-                        cat = C_DEGEN;
-                    }
-                } else {
-                    large = true;
-                }
-            } else cat = st == CULL_RANGE ? C_RANGE : st == CULL_CHANNEL ? C_CHAN : st == CULL_AZIMUTH ? C_AZI : C_DEGEN;
-        }
-        const unsigned lm = __ballot_sync(FULL, large);
-        if (lm) {
-            const int leader = __ffs(lm) - 1;
-            unsigned base = 0;
-            if (lane == leader) base = atomicAdd(P.n_large, (unsigned)__popc(lm));
-            base = __shfl_sync(FULL, base, leader);
-            if (large) {
-                const long long pos = (long long)base + __popc(lm & ((1u << lane) - 1u));
-                if (pos < P.cap_large) {
-                    P.large[pos] = make_int4((int)t, e | (R.c_from << 8), R.c_to,
-                                             (int)((unsigned)R.r_lo | ((unsigned)R.r_len << 16)));
-                    cat = C_LARGE;
-                } else {   // capacity fallback: intersect here (slow, never dropped)
-                    cat = C_OVF;
-                    if (R.pole_rows) { R.r_lo = 0; R.r_len = sE[e].chi; }
-                    intersect_rect_serial(P, sE[e], t, R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len);
-                }
-            }
-        }
-        {   // warp-aggregated stats of this round (lane 0 -> shared memory)
-            const unsigned ms = __ballot_sync(FULL, cat == C_SMALL), ml = __ballot_sync(FULL, cat == C_LARGE),
-                           mo = __ballot_sync(FULL, cat == C_OVF), mr = __ballot_sync(FULL, cat == C_RANGE),
-                           mc = __ballot_sync(FULL, cat == C_CHAN), ma = __ballot_sync(FULL, cat == C_AZI),
-                           md = __ballot_sync(FULL, cat == C_DEGEN);
-            const unsigned items = __reduce_add_sync(FULL, (unsigned)my);
-            const unsigned msat = __ballot_sync(FULL, sat), mbat = __ballot_sync(FULL, bat);
-            if (lane == 0) {
-                if (ms | ml | mo) atomicAdd(acc + ST_SURV, (unsigned)(__popc(ms) + __popc(ml) + __popc(mo)));
-                if (ms) atomicAdd(acc + ST_SMALL, (unsigned)__popc(ms));
-                if (items) atomicAdd(acc + ST_ITEMS_SMALL, (unsigned)items);
-                if (ml) atomicAdd(acc + ST_LARGE, (unsigned)__popc(ml));
-                if (mo) atomicAdd(acc + ST_OVF_LARGE, (unsigned)__popc(mo));
-                if (mr) atomicAdd(acc + ST_RANGE, (unsigned)__popc(mr));
-                if (mc) atomicAdd(acc + ST_CHANNEL, (unsigned)__popc(mc));
-                if (ma) atomicAdd(acc + ST_AZIMUTH, (unsigned)__popc(ma));
-                if (md) atomicAdd(acc + ST_DEGEN, (unsigned)__popc(md));
-                if (msat) atomicAdd(acc + ST_SAT, (unsigned)__popc(msat));
-                if (mbat) atomicAdd(acc + ST_BAT, (unsigned)__popc(mbat));
-            }
-        }
-        // A5: warp-level prefix-scan work expansion
-        int incl = my;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-        }
-        excl[lane] = incl - my;
-        const int total = __shfl_sync(FULL, incl, 31);
-        __syncwarp();
-        // one candidate per lane per iteration: resolve the owner (binary search of the inclusive
-        // scan), the ray index, then the certified test (scalar state only: nothing to local memory)
-        for (int b = 0; b < total; b += 32) {
-            const int qi = b + lane;
-            int ow = 0;
-#pragma unroll
-            for (int s = 16; s > 0; s >>= 1) {
-                const int vv = __shfl_sync(FULL, incl, ow + s - 1);
-                if (vv <= qi) ow += s;
-            }
-            bool hit = false, fb = false;
-            if (qi < total) {
-                const float4 r5 = slot[5 * 32 + ow];
-                const float4 r4 = slot[4 * 32 + ow];
-                const EmDev &EO = sE[__float_as_int(r4.w)];
-                const int local = qi - excl[ow];
-                const int len = __float_as_int(r5.z);
-                int row = (int)(((float)local + 0.5f) * r5.w);
-                int col = local - row * len;
-                if (col < 0) { --row; col += len; }
-                if (col >= len) { ++row; col -= len; }
-                const int j = __float_as_int(r5.x) + row;
-                int i = __float_as_int(r5.y) + col;
-                if (i >= EO.chi) i -= EO.chi;
-                const int g = EO.ray_base + j * EO.chi + i;
-                const float4 d = __ldg(P.raytab + g);
-                const float4 r0 = slot[0 * 32 + ow], r1 = slot[1 * 32 + ow], r2 = slot[2 * 32 + ow],
-                             r3 = slot[3 * 32 + ow];
-                Setup Q;
-                Q.n0 = {r0.x, r0.y, r0.z};
-                Q.n1 = {r1.x, r1.y, r1.z};
-                Q.n2 = {r2.x, r2.y, r2.z};
-                Q.B0 = r0.w; Q.B1 = r1.w; Q.B2 = r2.w;
-                Q.N = {r3.x, r3.y, r3.z};
-                Q.habs = r3.w;
-                Q.TN = r4.x;
-                float th = 0.f;
-                int r = P.force64 ? 2 : test_fast(d, Q, EO.dmax_lo, EO.dmax_hi, th);
-                fb = r == 2;
-                if (r == 2) {   // rare: reload the ray (keeping d live into the fp64 code spills it)
-                    f3 wv[3];
-                    load_tri(P.tri, (long long)__float_as_int(r4.z), wv);
-                    const float4 d2 = __ldcg(P.raytab + g);
-                    r = test_exact_r<true>(wv, em_o(EO), d2, EO.dmax, P.faces, th);
-                }
-                if (r == 1) {
-                    hit = true;
-                    record_hit(P.hits, P.allhits, g, th, __float_as_uint(r4.y));
-                }
-            }
-            // hit / fp64 counts warp-aggregated per iteration (no per-thread counter live across
-            // the loop: at the 64-register cap it would be spilled to local memory)
-            const unsigned hm = __ballot_sync(FULL, hit), fm = __ballot_sync(FULL, fb);
-            if (lane == 0 && (hm | fm)) {
-                if (hm) atomicAdd(acc + ST_HITS, (unsigned)__popc(hm));
-                if (fm) atomicAdd(acc + ST_FP64, (unsigned)__popc(fm));
-            }
-        }
-        __syncwarp();
+        const bool valid = (int)(w * 32u) + lane < (int)ns;
+        refine_round(P, sE, sSin, sLut, slot, excl, acc, lane, valid,
+                     valid ? __ldcs(P.surv + (int)(w * 32u) + lane) : 0ull);
         w = __shfl_sync(FULL, wn, 0);
     }
-    (void)setup64;
     __syncthreads();
     if (threadIdx.x < ST_COUNT && acc[threadIdx.x]) atomicAdd(P.stats + threadIdx.x, (unsigned long long)acc[threadIdx.x]);
 }
@@ -1558,6 +1574,7 @@ static cudaError_t launch_l2(grca_t h, const void *fn, unsigned grid, unsigned b
 
 // K2 .. K4 for the triangle source in P (events only when prof).
 static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof, int slot) {
+    const bool split = (h->ci.debug_flags & GRCA_DEBUG_SPLIT_REFINE) != 0;
     if (n_tri > 0) {   // K2
         const long long tiles = (n_tri + K2_THREADS - 1) / K2_THREADS;
         const long long grid = std::min<long long>(tiles, (long long)h->num_sms * h->k2_blocks_per_sm);
@@ -1571,7 +1588,6 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
         CK(cudaGetLastError());
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][2], h->stream));
-    const bool split = (h->ci.debug_flags & GRCA_DEBUG_SPLIT_REFINE) != 0;
     if (n_tri > 0 && split) {   // K2b (bounds only), rounds interleaved over warps
         const long long grid = (long long)h->num_sms * h->k2b_blocks_per_sm;
         k_refine<<<(unsigned)grid, K2_THREADS, h->k2b_smem, h->stream>>>(P);
