@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_cull(const __grid_constant__ KPa
 constexpr int kFixedEm = 8;
 struct EmLitePack {
     EmLite e[kFixedEm];
+    EmPair p[kFixedEm / 2];   // interleaved pair constants (packed path)
 };
 
 // K2 per-triangle test (A1 load + A2-A3 pre-test for all NE emitters): keep / range bit masks,
@@ -231,40 +232,46 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
                      (v[0].z - v[2].z) * (v[0].z - v[2].z);
     const float m2 = fmaxf(l0, fmaxf(l1, l2));
     const float emax = m2 * rsqrtf(m2) * (1.f + 1e-5f);   // triangle diameter (0 if degenerate)
-    int stv[NE];
+    unsigned kb = 0u, rb = 0u;
     if (P.nocull) {
-#pragma unroll
-        for (int e = 0; e < NE; ++e) stv[e] = CULL_KEEP;
+        kb = (1u << NE) - 1u;
     } else if (P.pairs_ok) {   // all frames orthonormal: packed fp32x2 path
 #pragma unroll
-        for (int e = 0; e + 1 < NE; e += 2)
-            quick_cull2(v, emax, EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base, sSin + EL.e[e + 1].sin_base,
-                        P.lut ? sLut + e * kLutBins : nullptr, P.lut ? sLut + (e + 1) * kLutBins : nullptr,
-                        stv[e], stv[e + 1]);
-        if (NE & 1)
-            stv[NE - 1] = quick_cull(v, emax, EL.e[NE - 1], sSin + EL.e[NE - 1].sin_base,
-                                     P.lut ? sLut + (NE - 1) * kLutBins : nullptr);
+        for (int e = 0; e + 1 < NE; e += 2) {
+            const unsigned r = quick_pair_lut(v, emax, EL.p[e / 2], EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base,
+                                              sSin + EL.e[e + 1].sin_base, sLut + e * kLutBins,
+                                              sLut + (e + 1) * kLutBins);
+            kb |= (r & 3u) << e;
+            rb |= (r >> 2) << e;
+        }
+        if (NE & 1) {
+            const unsigned r = quick_cull_lut(v, emax, EL.e[NE - 1], sSin + EL.e[NE - 1].sin_base,
+                                              sLut + (NE - 1) * kLutBins);
+            kb |= (r & 1u) << (NE - 1);
+            rb |= (r >> 1) << (NE - 1);
+        }
     } else {
 #pragma unroll
-        for (int e = 0; e < NE; ++e)
-            stv[e] = quick_cull(v, emax, EL.e[e], sSin + EL.e[e].sin_base, P.lut ? sLut + e * kLutBins : nullptr);
+        for (int e = 0; e < NE; ++e) {
+            const unsigned r = quick_cull_lut(v, emax, EL.e[e], sSin + EL.e[e].sin_base, sLut + e * kLutBins);
+            kb |= (r & 1u) << e;
+            rb |= (r >> 1) << e;
+        }
     }
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-        int st = stv[e];
-        if (P.area_eps2 > 0.f && st == CULL_KEEP) {   // NEXT-f1 paper mode (approximate):
-            // apparent-area cull, PAPER.md:622-632 (recomputed per pair: paper mode only)
+    chan = (unsigned)(NE - __popc(kb) - __popc(rb));
+    if (P.area_eps2 > 0.f) {   // NEXT-f1 paper mode (approximate): apparent-area cull
+        for (unsigned m = kb; m; m &= m - 1u) {
+            const int e = __ffs(m) - 1;
             const f3 cen = {(v[0].x + v[1].x + v[2].x) * (1.f / 3.f), (v[0].y + v[1].y + v[2].y) * (1.f / 3.f),
                             (v[0].z + v[1].z + v[2].z) * (1.f / 3.f)};
             const f3 hN = scalef(crossf(subf(v[1], v[0]), subf(v[2], v[0])), 0.5f);   // A_T * n
             const f3 co = {cen.x - EL.e[e].o[0], cen.y - EL.e[e].o[1], cen.z - EL.e[e].o[2]};
             const float an = dotf(hN, co), d2 = dotf(co, co);
-            if (an * an < P.area_eps2 * d2 * d2 * d2) { st = CULL_AREA; ++c_area; }
+            if (an * an < P.area_eps2 * d2 * d2 * d2) { kb &= ~(1u << e); ++c_area; }
         }
-        keep |= (st == CULL_KEEP ? 1u : 0u) << e;
-        rng |= (st == CULL_RANGE ? 1u : 0u) << e;
-        chan += (st == CULL_CHANNEL);
     }
+    keep = kb;
+    rng = rb;
 }
 
 template <int NE>
@@ -1478,12 +1485,19 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     h->k2_smem = k2_smem_bytes(n_emitters, h->n_sin, use_lut);
     memset(&h->lite_pack, 0, sizeof(h->lite_pack));
     for (int n = 0; n < n_emitters && n < kFixedEm; ++n) h->lite_pack.e[n] = lites[n];
+    for (int n = 0; n + 1 < n_emitters && n + 1 < kFixedEm; n += 2) {
+        EmPair &pr = h->lite_pack.p[n / 2];
+        for (int c = 0; c < 3; ++c) {
+            pr.no[c] = make_float2(-lites[n].o[c], -lites[n + 1].o[c]);
+            pr.u[c] = make_float2(lites[n].Au[c], lites[n + 1].Au[c]);
+        }
+    }
     h->k2f_smem = sizeof(float) * ((h->n_sin + 3) & ~3) + (use_lut ? (size_t)n_emitters * kLutBins : 0);
     h->k2b_smem = k2b_smem_bytes(n_emitters, h->n_sin, use_lut);
     h->k4s_smem = k4s_smem_bytes(n_emitters);
     h->kf_smem = kfused_smem_bytes(n_emitters, h->n_sin, use_lut);
     int b2 = 0, b2b = 0, b4s = 0, b4 = 0;
-    if (n_emitters <= kFixedEm) {
+    if (n_emitters <= kFixedEm && use_lut) {   // the fixed kernel relies on the LUT (gamma <= 255)
         const void *fn = k2_fixed_fn(n_emitters);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, fn, K2_THREADS, h->k2f_smem));
     } else {
@@ -1578,7 +1592,7 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
     if (n_tri > 0) {   // K2
         const long long tiles = (n_tri + K2_THREADS - 1) / K2_THREADS;
         const long long grid = std::min<long long>(tiles, (long long)h->num_sms * h->k2_blocks_per_sm);
-        if (h->n_em <= kFixedEm) {
+        if (h->n_em <= kFixedEm && h->use_lut) {
             void *args[] = {(void *)&P, (void *)&h->lite_pack};
             CK(cudaLaunchKernel(k2_fixed_fn(h->n_em), dim3((unsigned)grid), dim3(K2_THREADS), args, h->k2f_smem,
                                 h->stream));

@@ -586,6 +586,83 @@ __device__ __forceinline__ int quick_tail(const float s[3], float rmax, float em
     return range ? CULL_RANGE : (keep ? CULL_KEEP : CULL_CHANNEL);
 }
 
+// Fixed-kernel variants (k_cull_fixed, NE <= 8; LUT always present).  Same bounds as quick_tail;
+// differences: (i) no scan past the second LUT channel -- when a bin holds more channels below lo
+// the pair is kept (v1 < lo <= hi), which is conservative since K2b/cull_pair recomputes the exact
+// channel range; (ii) the result is two bits (1 = keep, 2 = range-culled) instead of a code.
+__device__ __forceinline__ unsigned quick_tail_lut(const float s[3], float rmax, float emax, const EmLite &L,
+                                                   const float *sinT, const unsigned char *lut) {
+    const float rlb = rmax - emax;
+    const bool range = rlb > L.lim;
+    const bool near = !(rlb > 2.f * emax);
+    const float q = __fdividef(emax, rlb);
+    const float q2 = q * q;
+    const float smax = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));
+    const bool pole = smax >= 1.f - 0.51f * q2 - 1e-5f;
+    const float pad = L.pad0 + 0.13f * q2;
+    const float lo = fminf(s[0], fminf(s[1], s[2])) - pad;
+    const float hi = fmaxf(s[0], fmaxf(s[1], s[2])) + pad;
+    // bin of lo: one rounding (<= 2.4e-7 in sin units) against the LUT's 1e-6 under-estimate margin
+    const int b = min(max(__float2int_rz(__fmaf_rn(lo, 0.5f * kLutBins, 0.5f * kLutBins)), 0), kLutBins - 1);
+    const float *sj = sinT + lut[b];
+    const float v0 = sj[0], v1 = sj[1];   // two +inf sentinels: j + 1 <= gamma + 1
+    const float vj = v0 >= lo ? v0 : v1;
+    const bool keep = near || pole || vj <= hi;
+    return range ? 2u : (keep ? 1u : 0u);
+}
+
+// scalar pre-test (any frame) with the fixed-kernel LUT tail; returns 1 = keep, 2 = range-culled
+__device__ __forceinline__ unsigned quick_cull_lut(const f3 v[3], float emax, const EmLite &L, const float *sinT,
+                                                   const unsigned char *lut) {
+    float s[3], r[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const f3 a = {v[k].x - L.o[0], v[k].y - L.o[1], v[k].z - L.o[2]};
+        const float w2 = a.x * a.x + a.y * a.y + a.z * a.z;
+        const float xu = L.Au[0] * a.x + L.Au[1] * a.y + L.Au[2] * a.z;
+        const float iw = rsqrtf(w2);
+        r[k] = w2 * iw;
+        if (L.ortho) {
+            s[k] = xu * iw;
+        } else {
+            const float x2 = L.G[0] * a.x * a.x + L.G[1] * a.y * a.y + L.G[2] * a.z * a.z +
+                             2.f * (L.G[3] * a.x * a.y + L.G[4] * a.x * a.z + L.G[5] * a.y * a.z);
+            s[k] = xu * rsqrtf(x2);
+        }
+    }
+    return quick_tail_lut(s, fmaxf(r[0], fmaxf(r[1], r[2])), emax, L, sinT, lut);
+}
+
+// interleaved constants of emitters (2p, 2p+1) for the packed path: one 64-bit constant load each
+struct EmPair {
+    float2 no[3];   // (-o_x), (-o_y), (-o_z)
+    float2 u[3];    // Au_x, Au_y, Au_z
+};
+
+// two emitters at once; returns bits (keep0, keep1) | (range0, range1) << 2
+__device__ __forceinline__ unsigned quick_pair_lut(const f3 v[3], float emax, const EmPair &PR, const EmLite &L0,
+                                                   const EmLite &L1, const float *sinT0, const float *sinT1,
+                                                   const unsigned char *lut0, const unsigned char *lut1) {
+    float s0[3], s1[3], r0 = 0.f, r1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float2 ax = __fadd2_rn(f2(v[k].x, v[k].x), PR.no[0]);
+        const float2 ay = __fadd2_rn(f2(v[k].y, v[k].y), PR.no[1]);
+        const float2 az = __fadd2_rn(f2(v[k].z, v[k].z), PR.no[2]);
+        const float2 w2 = __ffma2_rn(az, az, __ffma2_rn(ay, ay, __fmul2_rn(ax, ax)));
+        const float2 xu = __ffma2_rn(PR.u[2], az, __ffma2_rn(PR.u[1], ay, __fmul2_rn(PR.u[0], ax)));
+        const float2 iw = f2(rsqrtf(w2.x), rsqrtf(w2.y));
+        const float2 rr = __fmul2_rn(w2, iw), ss = __fmul2_rn(xu, iw);
+        s0[k] = ss.x;
+        s1[k] = ss.y;
+        r0 = fmaxf(r0, rr.x);
+        r1 = fmaxf(r1, rr.y);
+    }
+    const unsigned a = quick_tail_lut(s0, r0, emax, L0, sinT0, lut0);
+    const unsigned b = quick_tail_lut(s1, r1, emax, L1, sinT1, lut1);
+    return (a & 1u) | ((b & 1u) << 1) | ((a & 2u) << 1) | ((b & 2u) << 2);
+}
+
 __device__ __forceinline__ void quick_cull2(const f3 v[3], float emax, const EmLite &L0, const EmLite &L1,
                                             const float *sinT0, const float *sinT1, const unsigned char *lut0,
                                             const unsigned char *lut1, int &st0, int &st1) {
