@@ -606,8 +606,11 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
                     slot[3 * 32 + lane] = make_float4(S.N.x, S.N.y, S.N.z, S.habs);
                     slot[4 * 32 + lane] = make_float4(S.TN, __uint_as_float(tri_id(P.tri, t)),
                                                       __int_as_float((int)t), __int_as_float(e));
-                    slot[5 * 32 + lane] = make_float4(__int_as_float(R.c_from), __int_as_float(R.r_lo),
-                                                      __int_as_float(R.r_len), 1.f / (float)R.r_len);
+                    // ray of item (row, col) = gbase + row * chi + col - (col >= chi - r_lo ? chi : 0)
+                    slot[5 * 32 + lane] = make_float4(__int_as_float(E.ray_base + R.c_from * E.chi + R.r_lo),
+                                                      __int_as_float(E.chi - R.r_lo),
+                                                      __uint_as_float((unsigned)R.r_len | ((unsigned)E.chi << 16)),
+                                                      1.f / (float)R.r_len);
                 } else {
                     cat = C_DEGEN;
                 }
@@ -668,6 +671,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
     __syncwarp();
     // one candidate per lane per iteration: resolve the owner (binary search of the inclusive
     // scan), the ray index, then the certified test (scalar state only: nothing to local memory)
+    unsigned hw = 0u, fw = 0u;
     for (int b = 0; b < total; b += 32) {
         const int qi = b + lane;
         int ow = 0;
@@ -682,15 +686,13 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             const float4 r4 = slot[4 * 32 + ow];
             const EmDev &EO = sE[__float_as_int(r4.w)];
             const int local = qi - excl[ow];
-            const int len = __float_as_int(r5.z);
+            const unsigned lc = __float_as_uint(r5.z);
+            const int len = (int)(lc & 0xffffu), chi = (int)(lc >> 16);
             int row = (int)(((float)local + 0.5f) * r5.w);
             int col = local - row * len;
             if (col < 0) { --row; col += len; }
             if (col >= len) { ++row; col -= len; }
-            const int j = __float_as_int(r5.x) + row;
-            int i = __float_as_int(r5.y) + col;
-            if (i >= EO.chi) i -= EO.chi;
-            const int g = EO.ray_base + j * EO.chi + i;
+            const int g = __float_as_int(r5.x) + row * chi + col - (col >= __float_as_int(r5.y) ? chi : 0);
             const float4 d = __ldg(P.raytab + g);
             const float4 r0 = slot[0 * 32 + ow], r1 = slot[1 * 32 + ow], r2 = slot[2 * 32 + ow],
                          r3 = slot[3 * 32 + ow];
@@ -716,13 +718,14 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
                 record_hit(P.hits, P.allhits, g, th, __float_as_uint(r4.y));
             }
         }
-        // hit / fp64 counts warp-aggregated per iteration (no per-thread counter live across
-        // the loop: at the 64-register cap it would be spilled to local memory)
-        const unsigned hm = __ballot_sync(FULL, hit), fm = __ballot_sync(FULL, fb);
-        if (lane == 0 && (hm | fm)) {
-            if (hm) atomicAdd(acc + ST_HITS, (unsigned)__popc(hm));
-            if (fm) atomicAdd(acc + ST_FP64, (unsigned)__popc(fm));
-        }
+        // hit / fp64 counts: warp-uniform sums (a per-lane counter live across the loop would be
+        // spilled at the 64-register cap), flushed once per round
+        hw += __popc(__ballot_sync(FULL, hit));
+        fw += __popc(__ballot_sync(FULL, fb));
+    }
+    if (lane == 0) {
+        if (hw) atomicAdd(acc + ST_HITS, hw);
+        if (fw) atomicAdd(acc + ST_FP64, fw);
     }
     (void)setup64;
     __syncwarp();

@@ -752,8 +752,16 @@ __device__ __forceinline__ bool make_setup(const f3 v[3], f3 o, int faces, Setup
     const float nn = dotf(N, N);
     const float Bn = __fmul_rn(3.11f * kU, nn > 0.f ? __fmul_rn(nn, rsqrtf(nn)) : 0.f);
     (void)setup64;
-    S.TN = (!sign_ok || !(rh < 2e-6f)) ? CUDART_INF_F : __fmul_rn(__fdividef(Bn, __fsub_rn(kTRel - 3.f * kU, rh)), 1.0002f);
+    // budget: kTRel = rel(d.N) + rh + 6u, where 6u covers the rounding of N and h and the approximate
+    // division in test_fast (rcp.approx then multiply: <= 2 ulp = 4u)
+    S.TN = (!sign_ok || !(rh < 2e-6f)) ? CUDART_INF_F : __fmul_rn(__fdividef(Bn, __fsub_rn(kTRel - 6.f * kU, rh)), 1.0002f);
     return true;
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {   // rcp.approx.ftz.f32 (MUFU.RCP, <= 1 ulp)
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
 
 // 0 = certified miss, 1 = certified hit (t set), 2 = uncertain -> fp64
@@ -763,8 +771,8 @@ __device__ __forceinline__ int test_fast(float4 d4, const Setup &S, float dmax_l
     if (F0 < -S.B0 || F1 < -S.B1 || F2 < -S.B2) return 0;
     if (!(F0 > S.B0 && F1 > S.B1 && F2 > S.B2)) return 2;
     const float dN = dotf(d, S.N);
-    if (!(dN >= S.TN)) return 2;
-    t = __fdiv_rn(S.habs, dN);
+    if (!(dN >= S.TN && dN <= 1e30f)) return 2;   // (upper guard: the reciprocal must not flush to 0)
+    t = __fmul_rn(S.habs, rcp_approx(dN));        // <= 2 ulp, inside TN's budget
     if (t <= dmax_lo) return 1;
     if (t > dmax_hi) return 0;
     return 2;
