@@ -610,7 +610,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
                     slot[5 * 32 + lane] = make_float4(__int_as_float(E.ray_base + R.c_from * E.chi + R.r_lo),
                                                       __int_as_float(E.chi - R.r_lo),
                                                       __uint_as_float((unsigned)R.r_len | ((unsigned)E.chi << 16)),
-                                                      1.f / (float)R.r_len);
+                                                      __fdividef(1.f, (float)R.r_len));   // row guess, corrected by +-1
                 } else {
                     cat = C_DEGEN;
                 }

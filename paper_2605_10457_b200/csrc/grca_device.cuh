@@ -85,9 +85,17 @@ __device__ __forceinline__ bool lexless(f3 p, f3 q) {
     return lx | (ex & (ly | (ey & lz)));
 }
 __device__ __forceinline__ bool finite3(f3 a) { return isfinite(a.x) && isfinite(a.y) && isfinite(a.z); }
+// sqrt.approx.ftz (MUFU, relative error ~2^-22, no slow-path call): used only inside conservative
+// pads / tolerances of the culls, never in a certified decision
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 // atan2 with |error| <= 2.0e-6 rad (odd degree-11 least-max polynomial on [0, 1] after octant
-// reduction; bound checked on 2M points by tests/test_abi_cpu.py through grca_debug_fast_atan2).
+// reduction; bound checked on 2M points by tests/test_abi_cpu.py through grca_debug_fast_atan2,
+// the host build).  The device build divides with __fdividef (<= 2 ulp in z, <= 1.2e-7 rad more).
 // Used for vertex azimuths, whose cull pad (kPadTheta = 5e-5) budgets 2.5e-6 for it.
 __host__ __device__ __forceinline__ float fast_atan2(float y, float x) {
     const float ax = fabsf(x), ay = fabsf(y);
@@ -153,7 +161,7 @@ __device__ __forceinline__ uint32_t tri_id(const TriSrc &T, long long t) {
 __device__ __forceinline__ float seg_dist2(f3 a, f3 b) {
     f3 e = subf(b, a);
     float ee = dotf(e, e);
-    float t = ee > 0.f ? fminf(fmaxf(-dotf(a, e) / ee, 0.f), 1.f) : 0.f;
+    float t = ee > 0.f ? fminf(fmaxf(__fdividef(-dotf(a, e), ee), 0.f), 1.f) : 0.f;   // ~2 ulp: 2nd-order in dist
     f3 p = {a.x + t * e.x, a.y + t * e.y, a.z + t * e.z};
     return dotf(p, p);
 }
@@ -164,7 +172,7 @@ __device__ float tri_dist(const f3 a[3]) {
     if (nn > 0.f && ((w0 >= 0.f && w1 >= 0.f && w2 >= 0.f) || (w0 <= 0.f && w1 <= 0.f && w2 <= 0.f)))
         return fabsf(dotf(N, a[0])) * rsqrtf(nn);
     float d2 = fminf(seg_dist2(a[0], a[1]), fminf(seg_dist2(a[1], a[2]), seg_dist2(a[2], a[0])));
-    return sqrtf(d2);
+    return sqrt_approx(d2);   // compared against D_max (1 + 1e-5): far above the 2^-22 error
 }
 
 // ------------------------------------------------------ A3/A4 angular bounds --
@@ -218,8 +226,8 @@ __device__ __forceinline__ int first_channel_gt(const float *sinT, int gamma, co
 // (returns true when unsure) -- including an extreme that is not attained is conservative.
 __device__ __forceinline__ bool on_arc(f3 p, f3 q, f3 m, f3 T) {
     float q1 = dotf(crossf(p, T), m), q2 = dotf(crossf(T, q), m);
-    float tol = 1e-4f * sqrtf(dotf(p, p) * dotf(T, T)) * sqrtf(dotf(m, m));
-    float tol2 = 1e-4f * sqrtf(dotf(q, q) * dotf(T, T)) * sqrtf(dotf(m, m));
+    float tol = 1e-4f * sqrt_approx(dotf(p, p) * dotf(T, T)) * sqrt_approx(dotf(m, m));
+    float tol2 = 1e-4f * sqrt_approx(dotf(q, q) * dotf(T, T)) * sqrt_approx(dotf(m, m));
     return q1 >= -tol && q2 >= -tol2;
 }
 
@@ -278,7 +286,7 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
     bool fast = false;
     float q2f = 0.f;
     if (rlb_x > 2.f * diam && !near_axis) {
-        const float q = diam / rlb_x;
+        const float q = __fdividef(diam, rlb_x);   // ~2 ulp: the 0.13 q^2 pad has 4 % slack over q^2/8
         q2f = q * q;
         fast = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2]))) < 1.f - 0.51f * q2f - 1e-5f;
     }
@@ -325,7 +333,7 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
             float mh2 = m.x * m.x + m.y * m.y;
             float mm = mh2 + m.z * m.z;
             if (!(mm > 0.f)) { shi = fmaxf(shi, 1.f); slo = fminf(slo, -1.f); continue; }
-            float S = sqrtf(mh2 / mm);
+            float S = sqrt_approx(__fdividef(mh2, mm));   // ~1e-7 rel., inside the long-edge pad 1e-5
             f3 T = {-m.z * m.x, -m.z * m.y, mh2};   // top of the great circle (u - (u.m)m) * mm
             if (on_arc(x[k], x[k1], m, T)) shi = fmaxf(shi, S);
             f3 Tb = {-T.x, -T.y, -T.z};
