@@ -4,6 +4,7 @@
     python tools/ncu_summarize.py full <prof.ncu-rep> <out.md> [<traffic.json>]
 """
 import collections
+import re
 import csv
 import json
 import subprocess
@@ -21,7 +22,7 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]
 
 
-def launches(path, out):
+def launches(path, out, cmd="bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-hybrid"):
     rows = list(csv.reader(open(path)))
     hdr, data = None, []
     for r in rows:
@@ -34,18 +35,18 @@ def launches(path, out):
     for d in data:
         name = d["Kernel Name"].split("(")[0]
         agg.setdefault(name, []).append(float(d["Metric Value"]))
-    ours = {k: v for k, v in agg.items() if "grca::" in k}
-    steps = max(len(v) for v in ours.values())
-    step_ns = sum(sum(v) for v in ours.values()) / steps
+    ours = {k: v for k, v in agg.items() if re.match(r"(void )?(grca::)?k_", k)}
+    med = {k: sorted(v)[len(v) // 2] for k, v in ours.items()}
+    step_ns = sum(med.values())
     lines = [f"# ncu launch list ({path.split('/')[-1]})", "",
-             "`ncu --metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 5 --warmup 3`;",
+             f"`ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_` over `{cmd}`;",
              "cold-cache, serialized launches: compare SHARES of the step, not absolutes.", "",
-             "| kernel | launches | mean us | share of step |", "|---|---|---|---|"]
+             "| kernel | launches | median us | min us | max us | share of step (medians) |", "|---|---|---|---|---|---|"]
     for k, v in ours.items():
-        m = sum(v) / len(v)
-        lines.append(f"| {k} | {len(v)} | {m / 1e3:.1f} | {100 * m / step_ns:.1f} % |")
-    lines.append(f"| **step (sum of our kernels)** | | {step_ns / 1e3:.1f} | 100 % |")
-    others = sum(len(v) for k, v in agg.items() if "grca::" not in k)
+        lines.append(f"| {k} | {len(v)} | {med[k] / 1e3:.1f} | {min(v) / 1e3:.1f} | {max(v) / 1e3:.1f} | "
+                     f"{100 * med[k] / step_ns:.1f} % |")
+    lines.append(f"| **step (sum of medians)** | | {step_ns / 1e3:.1f} | | | 100 % |")
+    others = sum(len(v) for k, v in agg.items() if k not in ours)
     lines += ["", f"Other (harness / torch) launches in the capture: {others}."]
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
@@ -103,6 +104,6 @@ def full(rep, out, traffic_json=None):
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
-        launches(sys.argv[2], sys.argv[3])
+        launches(sys.argv[2], sys.argv[3], *sys.argv[4:5])
     else:
         full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
