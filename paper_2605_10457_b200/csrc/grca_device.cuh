@@ -598,16 +598,20 @@ __device__ __forceinline__ int quick_tail(const float s[3], float rmax, float em
 // differences: (i) no scan past the second LUT channel -- when a bin holds more channels below lo
 // the pair is kept (v1 < lo <= hi), which is conservative since K2b/cull_pair recomputes the exact
 // channel range; (ii) the result is two bits (1 = keep, 2 = range-culled) instead of a code.
-__device__ __forceinline__ unsigned quick_tail_lut(const float s[3], float rmax, float emax, const EmLite &L,
+__device__ __forceinline__ unsigned quick_tail_lut(const float s[3], float miw, float emax, const EmLite &L,
                                                    const float *sinT, const unsigned char *lut) {
-    const float rlb = rmax - emax;
-    const bool range = rlb > L.lim;
-    const bool near = !(rlb > 2.f * emax);
-    const float q = __fdividef(emax, rlb);
-    const float q2 = q * q;
+    // x = emax / max_k |a_k| (miw = min_k 1/|a_k| from the rsqrt already taken).  rlb = max|a_k| -
+    // emax > 2 emax  <=>  x < 1/3 (0.33: margin for the rsqrt error); then q = x / (1 - x) gives
+    // q^2 <= 2.25 x^2, so the pads of quick_cull become 0.13 q^2 <= 0.2925 x^2 and the pole bound
+    // 0.51 q^2 <= 1.1475 x^2 (x^2 ~ 1e-6 for typical triangles: no measurable loss of culling).
+    // Range: rlb > lim  <=>  max|a_k| > lim + emax  <=>  miw (lim + emax) < 1.
+    const float x = emax * miw;
+    const float x2 = x * x;
+    const bool range = miw * (L.lim + emax) < 1.f;
+    const bool near = !(x < 0.33f);
     const float smax = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));
-    const bool pole = smax >= 1.f - 0.51f * q2 - 1e-5f;
-    const float pad = L.pad0 + 0.13f * q2;
+    const bool pole = smax >= 1.f - 1.1475f * x2 - 1e-5f;
+    const float pad = L.pad0 + 0.2925f * x2;
     const float lo = fminf(s[0], fminf(s[1], s[2])) - pad;
     const float hi = fmaxf(s[0], fmaxf(s[1], s[2])) + pad;
     // bin of lo: one rounding (<= 2.4e-7 in sin units) against the LUT's 1e-6 under-estimate margin
@@ -622,23 +626,22 @@ __device__ __forceinline__ unsigned quick_tail_lut(const float s[3], float rmax,
 // scalar pre-test (any frame) with the fixed-kernel LUT tail; returns 1 = keep, 2 = range-culled
 __device__ __forceinline__ unsigned quick_cull_lut(const f3 v[3], float emax, const EmLite &L, const float *sinT,
                                                    const unsigned char *lut) {
-    float s[3], r[3];
+    float s[3], iw[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const f3 a = {v[k].x - L.o[0], v[k].y - L.o[1], v[k].z - L.o[2]};
         const float w2 = a.x * a.x + a.y * a.y + a.z * a.z;
         const float xu = L.Au[0] * a.x + L.Au[1] * a.y + L.Au[2] * a.z;
-        const float iw = rsqrtf(w2);
-        r[k] = w2 * iw;
+        iw[k] = rsqrtf(w2);
         if (L.ortho) {
-            s[k] = xu * iw;
+            s[k] = xu * iw[k];
         } else {
             const float x2 = L.G[0] * a.x * a.x + L.G[1] * a.y * a.y + L.G[2] * a.z * a.z +
                              2.f * (L.G[3] * a.x * a.y + L.G[4] * a.x * a.z + L.G[5] * a.y * a.z);
             s[k] = xu * rsqrtf(x2);
         }
     }
-    return quick_tail_lut(s, fmaxf(r[0], fmaxf(r[1], r[2])), emax, L, sinT, lut);
+    return quick_tail_lut(s, fminf(iw[0], fminf(iw[1], iw[2])), emax, L, sinT, lut);
 }
 
 // interleaved constants of emitters (2p, 2p+1) for the packed path: one 64-bit constant load each
@@ -651,7 +654,7 @@ struct EmPair {
 __device__ __forceinline__ unsigned quick_pair_lut(const f3 v[3], float emax, const EmPair &PR, const EmLite &L0,
                                                    const EmLite &L1, const float *sinT0, const float *sinT1,
                                                    const unsigned char *lut0, const unsigned char *lut1) {
-    float s0[3], s1[3], r0 = 0.f, r1 = 0.f;
+    float s0[3], s1[3], m0 = CUDART_INF_F, m1 = CUDART_INF_F;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const float2 ax = __fadd2_rn(f2(v[k].x, v[k].x), PR.no[0]);
@@ -660,14 +663,14 @@ __device__ __forceinline__ unsigned quick_pair_lut(const f3 v[3], float emax, co
         const float2 w2 = __ffma2_rn(az, az, __ffma2_rn(ay, ay, __fmul2_rn(ax, ax)));
         const float2 xu = __ffma2_rn(PR.u[2], az, __ffma2_rn(PR.u[1], ay, __fmul2_rn(PR.u[0], ax)));
         const float2 iw = f2(rsqrtf(w2.x), rsqrtf(w2.y));
-        const float2 rr = __fmul2_rn(w2, iw), ss = __fmul2_rn(xu, iw);
+        const float2 ss = __fmul2_rn(xu, iw);
         s0[k] = ss.x;
         s1[k] = ss.y;
-        r0 = fmaxf(r0, rr.x);
-        r1 = fmaxf(r1, rr.y);
+        m0 = fminf(m0, iw.x);
+        m1 = fminf(m1, iw.y);
     }
-    const unsigned a = quick_tail_lut(s0, r0, emax, L0, sinT0, lut0);
-    const unsigned b = quick_tail_lut(s1, r1, emax, L1, sinT1, lut1);
+    const unsigned a = quick_tail_lut(s0, m0, emax, L0, sinT0, lut0);
+    const unsigned b = quick_tail_lut(s1, m1, emax, L1, sinT1, lut1);
     return (a & 1u) | ((b & 1u) << 1) | ((a & 2u) << 1) | ((b & 2u) << 2);
 }
 
