@@ -575,7 +575,6 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
                                              const unsigned char *sLut, float4 *slot, int *excl, unsigned *acc,
                                              int lane, bool valid, unsigned long long ent) {
     enum { C_NONE = 0, C_SMALL, C_LARGE, C_OVF, C_RANGE, C_CHAN, C_AZI, C_DEGEN };
-    unsigned setup64 = 0;
     int my = 0, e = 0, cat = C_NONE;
     bool sat = false, bat = false;   // paper classification counters
     long long t = 0;
@@ -596,16 +595,9 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             bat = !sat;
             const long long items = rect_items(R, E);
             if (items <= P.small_max && !R.pole_rows) {
-                Setup S;
-                if (make_setup(v, em_o(E), P.faces, S, setup64)) {
+                if (setup_to_slot(v, em_o(E), P.faces, slot + lane, tri_id(P.tri, t), (int)t, e)) {
                     my = (int)items;
                     cat = C_SMALL;
-                    slot[0 * 32 + lane] = make_float4(S.n0.x, S.n0.y, S.n0.z, S.B0);
-                    slot[1 * 32 + lane] = make_float4(S.n1.x, S.n1.y, S.n1.z, S.B1);
-                    slot[2 * 32 + lane] = make_float4(S.n2.x, S.n2.y, S.n2.z, S.B2);
-                    slot[3 * 32 + lane] = make_float4(S.N.x, S.N.y, S.N.z, S.habs);
-                    slot[4 * 32 + lane] = make_float4(S.TN, __uint_as_float(tri_id(P.tri, t)),
-                                                      __int_as_float((int)t), __int_as_float(e));
                     // ray of item (row, col) = gbase + row * chi + col - (col >= chi - r_lo ? chi : 0)
                     slot[5 * 32 + lane] = make_float4(__int_as_float(E.ray_base + R.c_from * E.chi + R.r_lo),
                                                       __int_as_float(E.chi - R.r_lo),
@@ -727,7 +719,6 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
         if (hw) atomicAdd(acc + ST_HITS, hw);
         if (fw) atomicAdd(acc + ST_FP64, fw);
     }
-    (void)setup64;
     __syncwarp();
 }
 

@@ -775,6 +775,51 @@ __device__ __forceinline__ float rcp_approx(float x) {   // rcp.approx.ftz.f32 (
     return r;
 }
 
+// make_setup written straight into a lane's slot column (fused kernel): same values, bit for bit,
+// computed plane first and one edge at a time so that fewer values are live at once (the fused
+// kernel runs at the 64-register cap).  slot[k * 32] = (n_k, B_k) for k < 3, slot[3 * 32] = (N, |h|),
+// slot[4 * 32] = (TN, id, tri, emitter).  Returns false like make_setup.
+__device__ __forceinline__ bool setup_to_slot(const f3 v[3], f3 o, int faces, float4 *slot, uint32_t id, int tri,
+                                              int em) {
+    const d3 V0 = tod(v[0]);
+    const d3 E1 = subd(tod(v[1]), V0), E2 = subd(tod(v[2]), V0);
+    const d3 N64 = crossd(E1, E2);
+    const d3 A0 = subd(V0, tod(o));
+    const double h64 = dotd(N64, A0);
+    if (!(h64 > 0.0 || h64 < 0.0)) return false;
+    const float s = h64 > 0.0 ? 1.f : -1.f;
+    if ((faces == 1 && s < 0.f) || (faces == 2 && s > 0.f)) return false;
+    const f3 N = {(float)N64.x, (float)N64.y, (float)N64.z};
+    const float habs = (float)fabs(h64);
+    const float sE1 = __fadd_rn(__fadd_rn(fabsf((float)E1.x), fabsf((float)E1.y)), fabsf((float)E1.z));
+    const float sE2 = __fadd_rn(__fadd_rn(fabsf((float)E2.x), fabsf((float)E2.y)), fabsf((float)E2.z));
+    const float sN = __fadd_rn(__fadd_rn(fabsf(N.x), fabsf(N.y)), fabsf(N.z));
+    const float l1 = __fadd_rn(__fmul_rn(sE1, sE2), sN);
+    const float la = __fadd_rn(__fadd_rn(fabsf((float)A0.x), fabsf((float)A0.y)), fabsf((float)A0.z));
+    const float err64 = __fmul_rn(__fmul_rn(3.64e-15f, l1), la);
+    const bool sign_ok = habs > 2.f * err64;
+    const float rh = __fadd_rn(1.01f * kU, __fmul_rn(__fdividef(err64, habs), 1.02f));
+    const float nn = dotf(N, N);
+    const float Bn = __fmul_rn(3.11f * kU, nn > 0.f ? __fmul_rn(nn, rsqrtf(nn)) : 0.f);
+    const float TN = (!sign_ok || !(rh < 2e-6f)) ? CUDART_INF_F
+                                                 : __fmul_rn(__fdividef(Bn, __fsub_rn(kTRel - 6.f * kU, rh)), 1.0002f);
+    const f3 SN = scalef(N, s);
+    slot[3 * 32] = make_float4(SN.x, SN.y, SN.z, habs);
+    slot[4 * 32] = make_float4(TN, __uint_as_float(id), __int_as_float(tri), __int_as_float(em));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        f3 Pp = v[k], Qq = v[(k + 1) % 3];
+        const bool sw = lexless(Qq, Pp);
+        if (sw) { f3 t = Pp; Pp = Qq; Qq = t; }
+        const f3 aP = subf(Pp, o), e = subf(Qq, Pp);
+        const f3 n = scalef(crossf(aP, e), s * (sw ? -1.f : 1.f));
+        const float pe = __fmul_rn(dotf(aP, aP), dotf(e, e));
+        const float B = __fmul_rn(16.1f * kU, pe > 0.f ? __fmul_rn(pe, rsqrtf(pe)) : 0.f);
+        slot[k * 32] = make_float4(n.x, n.y, n.z, sign_ok ? B : CUDART_INF_F);
+    }
+    return true;
+}
+
 // 0 = certified miss, 1 = certified hit (t set), 2 = uncertain -> fp64
 __device__ __forceinline__ int test_fast(float4 d4, const Setup &S, float dmax_lo, float dmax_hi, float &t) {
     const f3 d = {d4.x, d4.y, d4.z};
