@@ -36,6 +36,9 @@ constexpr int K4_THREADS = 256;
 #ifndef KF_MINB
 #define KF_MINB 2
 #endif
+#ifndef K4_MINB
+#define K4_MINB 3   // 80 registers: 3 blocks of 256 per SM (measured best; 1 block = 95+ regs, 25 % occupancy)
+#endif
 #ifndef K2_MINB
 #define K2_MINB 8   // K2 is issue-bound; 8 x 256 threads (32 regs) measured marginally best
 #endif
@@ -911,7 +914,7 @@ __global__ void __launch_bounds__(256) k_bin(const __grid_constant__ KParams P) 
 }
 
 // ------------------------------------------------------------ K4 intersect --
-__global__ void __launch_bounds__(K4_THREADS) k_isect(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(K4_THREADS, K4_MINB) k_isect(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     EmDev *sE = reinterpret_cast<EmDev *>(smem);
     __shared__ unsigned long long acc[ST_COUNT];
