@@ -88,10 +88,16 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- scene --
 class Scene:
-    """Resident C-config frames on the GPU (harness: input generation, not the hot path)."""
+    """Resident C-config frames on the GPU (harness: input generation, not the hot path).
+
+    mesh="indexed" (default when the cars are plain meshes, i.e. ND motion and no subdivision):
+    one vertex buffer per frame = [static triangles' own vertices (3 per triangle)] + [posed car
+    vertices (shared grid vertices)], and one index buffer shared by all frames (static: 0..3n-1;
+    cars: their faces).  Same triangles, same order and ids as the soup; a frame's per-step input
+    is then only the car vertices.  mesh="soup": float4 triplets per triangle."""
 
     def __init__(self, config: str, rank: int, world: int, device, deformation: str = "ND", shard: str = "triangles",
-                 max_range=-1.0, subdiv: int = 0, car_scale=None):
+                 max_range=-1.0, subdiv: int = 0, car_scale=None, mesh: str = "indexed"):
         import torch
 
         from paper_2605_10457_b200 import dist as D
@@ -114,26 +120,48 @@ class Scene:
                                    device=device)
         self.n_tri = int(self.ids.numel())
         self.n_static_local = len(self.own_static)
+        self.ns3 = 3 * self.n_static_local
         static = torch.as_tensor(w["tris"][:n_static][self.own_static].reshape(-1, 3), device=device)
-        self.car = torch.as_tensor(w["car_local"], dtype=torch.float32, device=device)   # (m, 3, 3)
         self.n_cars = len(w["poses"])
-        self.own_dyn_t = torch.as_tensor(self.own_dyn, device=device)
         self.bbox = w["bbox"]
         self.config = config
         self.deformation = deformation
         self.device = device
+        cm = w.get("car_mesh")
+        self.indexed = mesh == "indexed" and cm is not None and deformation == "ND" and n_dyn > 0
+        self.mesh = "indexed" if self.indexed else "soup"
+        self.indices = self.idx_dyn = None
+        if self.indexed:
+            car_v, car_f = cm
+            nv_car, nf_car = len(car_v), len(car_f)
+            self.car_v = torch.as_tensor(car_v, dtype=torch.float32, device=device)   # (V, 3)
+            inst, f = self.own_dyn // nf_car, self.own_dyn % nf_car
+            rel = (inst.astype(np.int64) * nv_car)[:, None] + car_f[f].astype(np.int64)
+            self.idx_dyn = torch.as_tensor(rel.astype(np.int32).reshape(-1), device=device)
+            self.indices = torch.cat([torch.arange(self.ns3, dtype=torch.int32, device=device),
+                                      self.idx_dyn + self.ns3]).contiguous()
+            self.n_dyn_vert = self.n_cars * nv_car
+            # algorithmic K2 read per cast: static 48 B vertices + 12 B indices; cars 12 B indices
+            # per triangle + 16 B per shared vertex
+            self.tri_bytes = self.n_static_local * 60 + len(self.own_dyn) * 12 + self.n_dyn_vert * 16
+        else:
+            self.car = torch.as_tensor(w["car_local"], dtype=torch.float32, device=device)   # (m, 3, 3)
+            self.own_dyn_t = torch.as_tensor(self.own_dyn, device=device)
+            self.tri_bytes = self.n_tri * 48
         self.frames = []
-        for f in range(N_FRAMES):
-            buf = torch.zeros((3 * self.n_tri, 4), dtype=torch.float32, device=device)
-            buf[: 3 * self.n_static_local, :3] = static
-            buf[3 * self.n_static_local:, :3] = self.dynamic(f)
+        for fr in range(N_FRAMES):
+            nd = self.n_dyn_vert if self.indexed else 3 * (self.n_tri - self.n_static_local)
+            buf = torch.zeros((self.ns3 + nd, 4), dtype=torch.float32, device=device)
+            buf[: self.ns3, :3] = static
+            buf[self.ns3:, :3] = self.dynamic(fr)
             self.frames.append(buf)
         del static
         torch.cuda.synchronize()
 
     def dynamic(self, frame: int):
         """Motion f.i: per-frame random pose/scale of every car instance; world
-        v = R (s * v_local) + p.  Computed with torch on the device; returns (3 * n_own_dyn, 3)."""
+        v = R (s * v_local) + p.  Computed with torch on the device.  Indexed: the posed car
+        vertices (n_cars * V, 3); soup: the own dynamic triangles' vertices (3 * n_own_dyn, 3)."""
         import torch
 
         poses = sg.pose_instances(self.n_cars, self.bbox, int(self.config[1:]), frame, scale_lo=self.scale[0],
@@ -141,6 +169,9 @@ class Scene:
         R = torch.as_tensor(np.stack([p.rotation for p in poses]), dtype=torch.float32, device=self.device)
         s = torch.as_tensor(np.stack([p.scale for p in poses]), dtype=torch.float32, device=self.device)
         p = torch.as_tensor(np.stack([p.position for p in poses]), dtype=torch.float32, device=self.device)
+        if self.indexed:
+            v = (self.car_v[None] * s[:, None, :]) @ R.transpose(1, 2) + p[:, None, :]
+            return v.reshape(-1, 3)
         v = (self.car[None] * s[:, None, None, :]) @ R.transpose(1, 2)[:, None] + p[:, None, None, :]
         v = v.reshape(-1, 3, 3)
         if self.deformation == "SWD":
@@ -204,7 +235,7 @@ def ncu_traffic():
     return out, os.path.basename(files[-1])
 
 
-def kernel_rooflines(kernel_ms, st, n_rays, n_tri, n_em, clk, device, split=False):
+def kernel_rooflines(kernel_ms, st, n_rays, n_tri, n_em, clk, device, split=False, tri_bytes=None):
     import torch
 
     pk = peaks()
@@ -240,7 +271,7 @@ def kernel_rooflines(kernel_ms, st, n_rays, n_tri, n_em, clk, device, split=Fals
                   "traffic_src": src}
     # K2 also streams the triangle soup once: report its HBM fraction beside the ALU one
     t2 = max(kernel_ms["K2_cull"], 1e-9) / 1e3
-    out["K2_cull"]["hbm_achieved_gbs"] = 48 * n_tri / t2 / 1e9
+    out["K2_cull"]["hbm_achieved_gbs"] = (tri_bytes if tri_bytes is not None else 48 * n_tri) / t2 / 1e9
     out["K2_cull"]["hbm_frac"] = out["K2_cull"]["hbm_achieved_gbs"] / pk["hbm_gbs"]
     return out
 
@@ -264,6 +295,8 @@ def main():
     ap.add_argument("--split-refine", action="store_true", help="K2b and K4s as two kernels (A/B)")
     ap.add_argument("--l2-persist", action="store_true", help="A/B: persisting L2 window (opt-in)")
     ap.add_argument("--no-packed", action="store_true", help="A/B: K2 without packed fp32x2 math")
+    ap.add_argument("--soup", action="store_true", help="triangle-soup scene (float4 triplets) instead of the indexed "
+                    "car meshes (same triangles; the e2e upload is then every dynamic triangle's vertices)")
     ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters"])
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 logic with several ranks on one GPU")
@@ -327,7 +360,8 @@ def main():
 
     car_scale = tuple(float(x) for x in args.car_scale.split(",")) if args.car_scale else None
     scene = Scene(args.config, rank, world, device, args.deformation, shard=shard,
-                  max_range=(None if args.max_range == 0 else args.max_range), subdiv=args.subdiv, car_scale=car_scale)
+                  max_range=(None if args.max_range == 0 else args.max_range), subdiv=args.subdiv, car_scale=car_scale,
+                  mesh="soup" if args.soup else "indexed")
     ems = scene.emitters
     n_rays = sg.n_rays_total(ems)
     n_rays_job = sg.n_rays_total(scene.w["emitters"])
@@ -349,7 +383,7 @@ def main():
             g.cast(dist_out, tri_out)
 
     def step(k):
-        g.update_triangles(scene.frames[k % N_FRAMES], tri_ids=scene.ids)
+        g.update_triangles(scene.frames[k % N_FRAMES], indices=scene.indices, tri_ids=scene.ids)
         cast_once()
 
     stream = torch.cuda.current_stream(device)
@@ -388,8 +422,9 @@ def main():
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        n_dyn_vals = 3 * (scene.n_tri - scene.n_static_local)
-        host_dyn = [scene.frames[f][3 * scene.n_static_local:].cpu().pin_memory() for f in range(N_FRAMES)]
+        ns3 = scene.ns3
+        n_dyn_vals = scene.frames[0].shape[0] - ns3   # float4 vertices uploaded per step
+        host_dyn = [scene.frames[f][ns3:].cpu().pin_memory() for f in range(N_FRAMES)]
         host_dist = torch.empty(n_rays, dtype=torch.float32).pin_memory()
         host_tri = torch.empty(n_rays, dtype=torch.int32).pin_memory()
         dev_buf = scene.frames[0]
@@ -398,8 +433,8 @@ def main():
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for k in range(k_e2e):
-            dev_buf[3 * scene.n_static_local:].copy_(host_dyn[k % N_FRAMES], non_blocking=True)
-            g.update_triangles(dev_buf, tri_ids=scene.ids)
+            dev_buf[ns3:].copy_(host_dyn[k % N_FRAMES], non_blocking=True)
+            g.update_triangles(dev_buf, indices=scene.indices, tri_ids=scene.ids)
             cast_once()
             host_dist.copy_(dist_out, non_blocking=True)
             host_tri.copy_(tri_out, non_blocking=True)
@@ -412,7 +447,8 @@ def main():
             ems_e2e = float(t.item())
         e2e = {"value": n_rays_job * k_e2e / (ems_e2e / 1e3), "unit": "rays/s", "ms_per_step": ems_e2e / k_e2e,
                "h2d_bytes_per_step": int(n_dyn_vals * 16), "d2h_bytes_per_step": int(n_rays * 8), "steps": k_e2e,
-               "what": "pinned H2D of this frame's dynamic vertices + grca_cast + D2H of (dist, id) per ray"}
+               "what": f"pinned H2D of this frame's dynamic vertices ({scene.mesh} mesh) + grca_cast + D2H of "
+                       "(dist, id) per ray"}
 
     # ---- hybrid static/dynamic (NEXT-f2; NOT the headline: static triangles cached across frames)
     hybrid = None
@@ -424,7 +460,7 @@ def main():
         dyn_ids = scene.ids[scene.n_static_local:]
 
         def hstep(k):
-            gh.update_triangles(scene.frames[k % N_FRAMES][ns3:], tri_ids=dyn_ids)
+            gh.update_triangles(scene.frames[k % N_FRAMES][ns3:], indices=scene.idx_dyn, tri_ids=dyn_ids)
             gh.cast(dist_out, tri_out)
 
         for k in range(3):
@@ -446,7 +482,8 @@ def main():
 
     # ---- per-kernel roofline (per-kernel CUDA events on the launch stream, last <= 64 steps)
     kernel_ms = {n: kms[i] for i, n in enumerate(KERNELS)}
-    roof = kernel_rooflines(kernel_ms, stats, n_rays, scene.n_tri, len(ems), clk, device, split=args.split_refine)
+    roof = kernel_rooflines(kernel_ms, stats, n_rays, scene.n_tri, len(ems), clk, device, split=args.split_refine,
+                            tri_bytes=scene.tri_bytes)
     dom = max(roof, key=lambda n: kernel_ms[n])
     roofline = dict(roof[dom])
     roofline["kernel"] = dom
@@ -466,7 +503,7 @@ def main():
             "config": {"workload": args.config, "emitters": len(scene.w["emitters"]), "rays_per_frame": n_rays_job,
                        "triangles": scene.n_tri_global, "dynamic_triangles": int(scene.w["n_dynamic"]),
                        "deformation": args.deformation, "max_range_m": float(ems[0].max_range),
-                       "subdiv": args.subdiv, "car_scale": list(scene.scale),
+                       "subdiv": args.subdiv, "car_scale": list(scene.scale), "mesh": scene.mesh,
                        "sharding": ("none" if world == 1 else
                                     f"triangles block-interleaved ({D.BLOCK}) + all-reduce(MIN) x {world}"
                                     if shard == "triangles" else f"emitters (n mod P) x {world}, no reduction"),

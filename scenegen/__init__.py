@@ -284,11 +284,12 @@ def _tess_box(size, edge: float) -> np.ndarray:
     return np.concatenate(tris, 0)
 
 
-def car(n_theta: int = 388, n_psi: int = 388, dims=(4.57, 2.28, 1.08), exponent: float = 4.0) -> np.ndarray:
-    """Superellipsoid 'sports car' in its local frame: 2*n_theta*n_psi triangles.
+def car_mesh(n_theta: int = 388, n_psi: int = 388, dims=(4.57, 2.28, 1.08), exponent: float = 4.0):
+    """Superellipsoid 'sports car' in its local frame as an indexed mesh: a (n_theta+1) x (n_psi+1)
+    vertex grid and 2*n_theta*n_psi triangles, the two of each quad adjacent in the list.
 
     x = (L/2) sgn(sin t cos p)|sin t cos p|^(2/exponent) etc.  The pole rows give
-    zero-area triangles (never hit).
+    zero-area triangles (never hit).  Returns (vertices (V, 3) fp32, faces (F, 3) int32).
     """
     L, W, H = dims
     k = 2.0 / exponent
@@ -302,12 +303,21 @@ def car(n_theta: int = 388, n_psi: int = 388, dims=(4.57, 2.28, 1.08), exponent:
     X = (L / 2) * sp(np.sin(T) * np.cos(P))
     Yv = (W / 2) * sp(np.sin(T) * np.sin(P))
     Zv = (H / 2) * sp(np.cos(T))
-    Pt = np.stack([X, Yv, Zv], -1)
-    a = Pt[:-1, :-1].reshape(-1, 3)
-    b = Pt[1:, :-1].reshape(-1, 3)
-    c = Pt[1:, 1:].reshape(-1, 3)
-    d = Pt[:-1, 1:].reshape(-1, 3)
-    return np.concatenate([np.stack([a, b, c], 1), np.stack([a, c, d], 1)], 0).astype(np.float32)
+    verts = np.stack([X, Yv, Zv], -1).reshape(-1, 3).astype(np.float32)
+    i, j = np.meshgrid(np.arange(n_theta), np.arange(n_psi), indexing="ij")
+    i, j = i.reshape(-1), j.reshape(-1)
+    a = i * (n_psi + 1) + j
+    b = (i + 1) * (n_psi + 1) + j
+    c = (i + 1) * (n_psi + 1) + j + 1
+    d = i * (n_psi + 1) + j + 1
+    faces = np.stack([np.stack([a, b, c], 1), np.stack([a, c, d], 1)], 1).reshape(-1, 3).astype(np.int32)
+    return verts, faces
+
+
+def car(n_theta: int = 388, n_psi: int = 388, dims=(4.57, 2.28, 1.08), exponent: float = 4.0) -> np.ndarray:
+    """The car_mesh triangles as a (F, 3, 3) fp32 soup (same triangles, same order)."""
+    verts, faces = car_mesh(n_theta, n_psi, dims, exponent)
+    return np.ascontiguousarray(verts[faces])
 
 
 def subdivide(tris: np.ndarray, levels: int) -> np.ndarray:
@@ -451,7 +461,8 @@ def workload(name: str, frame: int = 0, deformation: str = "ND", static_scale: f
     rng_m = rng_default if (max_range is not None and max_range < 0) else max_range
     ems = place_emitters(n_em, bbox, seed, hfovs=hfovs, max_range=rng_m)
     static = plant(max(1, int(n_static * static_scale)), bbox=bbox, seed=seed)
-    local = car()
+    car_v, car_f = car_mesh()
+    local = np.ascontiguousarray(car_v[car_f])
     if subdiv:
         local = subdivide(local, subdiv)
     poses = pose_instances(cars, bbox, seed, frame, scale_lo=slo, scale_hi=shi)
@@ -461,4 +472,5 @@ def workload(name: str, frame: int = 0, deformation: str = "ND", static_scale: f
         dynamic = swd(dynamic, bbox, seed, frame)
     tris = np.ascontiguousarray(np.concatenate([static, dynamic], 0))
     return {"emitters": ems, "tris": tris, "n_static": static.shape[0], "n_dynamic": dynamic.shape[0],
-            "bbox": bbox, "poses": poses, "car_local": local}
+            "bbox": bbox, "poses": poses, "car_local": local,
+            "car_mesh": None if subdiv else (car_v, car_f)}

@@ -10,6 +10,10 @@ def test_car_triangle_count():
     assert c.shape == (301088, 3, 3) and c.dtype == np.float32
     ext = c.reshape(-1, 3).max(0) - c.reshape(-1, 3).min(0)
     np.testing.assert_allclose(ext, [4.57, 2.28, 1.08], rtol=1e-3)
+    v, f = sg.car_mesh()
+    assert v.shape == (389 * 389, 3) and f.shape == (301088, 3) and f.dtype == np.int32
+    assert np.array_equal(v[f], c)                      # the soup is the indexed mesh, same order
+    assert np.array_equal(f[0], [0, 389, 390]) and np.array_equal(f[1], [0, 390, 1])   # quad pairs adjacent
 
 
 def test_plant_exact_count_and_area():
