@@ -51,6 +51,7 @@ enum Stat {
     ST_ITEMS_LARGE, ST_FP64, ST_HITS, ST_CHUNKS, ST_OVF_LARGE, ST_OVF_CHUNK, ST_SETUP64, ST_DEGEN,
     ST_K2SURV, ST_SAT, ST_BAT, ST_AREA, ST_COUNT
 };
+static_assert(ST_COUNT <= 32, "per-warp stat rows hold 32 counters");
 
 struct KParams {
     TriSrc tri;
@@ -575,9 +576,11 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KP
 // rectangles set up and expanded over the warp (prefix scan), large ones appended to the large
 // list.  Warp-collective; slot / excl are this warp's shared-memory staging areas.
 __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, const float *sSin,
-                                             const unsigned char *sLut, float4 *slot, int *excl, unsigned *acc,
-                                             int lane, bool valid, unsigned long long ent) {
-    enum { C_NONE = 0, C_SMALL, C_LARGE, C_OVF, C_RANGE, C_CHAN, C_AZI, C_DEGEN };
+                                             const unsigned char *sLut, float4 *slot, int *excl,
+                                             unsigned long long *wc, int lane, bool valid, unsigned long long ent) {
+    // per-lane category = the stat it counts (warp-private counters wc[], no atomics)
+    enum { C_NONE = -1, C_SMALL = ST_SMALL, C_LARGE = ST_LARGE, C_OVF = ST_OVF_LARGE, C_RANGE = ST_RANGE,
+           C_CHAN = ST_CHANNEL, C_AZI = ST_AZIMUTH, C_DEGEN = ST_DEGEN };
     int my = 0, e = 0, cat = C_NONE;
     bool sat = false, bat = false;   // paper classification counters
     long long t = 0;
@@ -633,25 +636,16 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             }
         }
     }
-    {   // warp-aggregated stats of this round (lane 0 -> shared memory)
-        const unsigned ms = __ballot_sync(FULL, cat == C_SMALL), ml = __ballot_sync(FULL, cat == C_LARGE),
-                       mo = __ballot_sync(FULL, cat == C_OVF), mr = __ballot_sync(FULL, cat == C_RANGE),
-                       mc = __ballot_sync(FULL, cat == C_CHAN), ma = __ballot_sync(FULL, cat == C_AZI),
-                       md = __ballot_sync(FULL, cat == C_DEGEN);
-        const unsigned items = __reduce_add_sync(FULL, (unsigned)my);
+    {   // stats of this round: one match over the category codes, each category's leader lane adds
+        // its count to the warp's private counter row (distinct addresses: no atomics)
+        const unsigned grp = __match_any_sync(FULL, cat);
+        if (cat >= 0 && lane == __ffs(grp) - 1) wc[cat] += (unsigned long long)__popc(grp);
         const unsigned msat = __ballot_sync(FULL, sat), mbat = __ballot_sync(FULL, bat);
+        const unsigned items = __reduce_add_sync(FULL, (unsigned)my);
         if (lane == 0) {
-            if (ms | ml | mo) atomicAdd(acc + ST_SURV, (unsigned)(__popc(ms) + __popc(ml) + __popc(mo)));
-            if (ms) atomicAdd(acc + ST_SMALL, (unsigned)__popc(ms));
-            if (items) atomicAdd(acc + ST_ITEMS_SMALL, (unsigned)items);
-            if (ml) atomicAdd(acc + ST_LARGE, (unsigned)__popc(ml));
-            if (mo) atomicAdd(acc + ST_OVF_LARGE, (unsigned)__popc(mo));
-            if (mr) atomicAdd(acc + ST_RANGE, (unsigned)__popc(mr));
-            if (mc) atomicAdd(acc + ST_CHANNEL, (unsigned)__popc(mc));
-            if (ma) atomicAdd(acc + ST_AZIMUTH, (unsigned)__popc(ma));
-            if (md) atomicAdd(acc + ST_DEGEN, (unsigned)__popc(md));
-            if (msat) atomicAdd(acc + ST_SAT, (unsigned)__popc(msat));
-            if (mbat) atomicAdd(acc + ST_BAT, (unsigned)__popc(mbat));
+            wc[ST_SAT] += __popc(msat);
+            wc[ST_BAT] += __popc(mbat);
+            wc[ST_ITEMS_SMALL] += items;
         }
     }
     // A5: warp-level prefix-scan work expansion
@@ -719,8 +713,8 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
         fw += __popc(__ballot_sync(FULL, fb));
     }
     if (lane == 0) {
-        if (hw) atomicAdd(acc + ST_HITS, hw);
-        if (fw) atomicAdd(acc + ST_FP64, fw);
+        wc[ST_HITS] += hw;
+        wc[ST_FP64] += fw;
     }
     __syncwarp();
 }
@@ -732,7 +726,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
     EmDev *sE = reinterpret_cast<EmDev *>(sExcl + KF_THREADS);
     float *sSin = reinterpret_cast<float *>(sE + P.n_em);
     unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
-    __shared__ unsigned acc[ST_COUNT];   // 32-bit: native shared atomics (per-block counts < 2^32)
+    __shared__ unsigned long long sWc[(KF_THREADS / 32) * 32];   // per-warp stat rows (no atomics)
     {
         const int nw = P.n_em * (int)(sizeof(EmDev) / 4);
         const int *src = reinterpret_cast<const int *>(P.em);
@@ -741,7 +735,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
         for (int i = threadIdx.x; i < P.n_sin; i += blockDim.x) sSin[i] = P.sin[i];
         if (P.lut)
             for (int i = threadIdx.x; i < P.n_em * kLutBins; i += blockDim.x) sLut[i] = P.lut[i];
-        if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0u;
+        for (int i = threadIdx.x; i < (KF_THREADS / 32) * 32; i += blockDim.x) sWc[i] = 0ull;
     }
     __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -757,12 +751,20 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
         unsigned wn = 0;
         if (lane == 0) wn = atomicAdd(P.n_surv + 2, 1u);   // next round, fetched early (latency hidden)
         const bool valid = (int)(w * 32u) + lane < (int)ns;
-        refine_round(P, sE, sSin, sLut, slot, excl, acc, lane, valid,
+        refine_round(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, lane, valid,
                      valid ? __ldcs(P.surv + (int)(w * 32u) + lane) : 0ull);
         w = __shfl_sync(FULL, wn, 0);
     }
     __syncthreads();
-    if (threadIdx.x < ST_COUNT && acc[threadIdx.x]) atomicAdd(P.stats + threadIdx.x, (unsigned long long)acc[threadIdx.x]);
+    if (threadIdx.x < ST_COUNT) {   // block total of each counter, one global atomic each
+        const int c = threadIdx.x;
+        unsigned long long v = 0ull;
+        for (int w2 = 0; w2 < KF_THREADS / 32; ++w2) {
+            const unsigned long long *r = sWc + w2 * 32;
+            v += c == ST_SURV ? r[ST_SMALL] + r[ST_LARGE] + r[ST_OVF_LARGE] : r[c];
+        }
+        if (v) atomicAdd(P.stats + c, v);
+    }
 }
 
 // ------------------------------------------------------------------ K3 bin --
