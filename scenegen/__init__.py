@@ -444,6 +444,22 @@ WORKLOADS = {
 }
 
 
+def indexed_frame(w: dict):
+    """The bench's indexed representation of a workload frame (ND motion, no subdivision): vertices =
+    [static triangles' own vertices, 3 each] + [each car instance's posed grid vertices], indices =
+    [0 .. 3 n_static - 1] + [the cars' faces offset per instance].  verts[idx] reproduces w["tris"]
+    exactly (same per-vertex posing).  Returns (verts (V, 3) fp32, idx (3 T,) int32)."""
+    car_v, car_f = w["car_mesh"]
+    ns = w["n_static"]
+    static_v = w["tris"][:ns].reshape(-1, 3)
+    inst_v = [apply_pose(car_v, p) for p in w["poses"]]
+    verts = np.concatenate([static_v] + inst_v, 0)
+    off = 3 * ns + np.arange(len(inst_v), dtype=np.int64)[:, None, None] * len(car_v)
+    dyn_idx = (car_f[None].astype(np.int64) + off).reshape(-1)
+    idx = np.concatenate([np.arange(3 * ns, dtype=np.int64), dyn_idx]).astype(np.int32)
+    return np.ascontiguousarray(verts.astype(np.float32)), idx
+
+
 def workload(name: str, frame: int = 0, deformation: str = "ND", static_scale: float = 1.0,
              max_range=-1.0, subdiv: int = 0, n_cars: Optional[int] = None) -> dict:
     """BASELINE.json configs as concrete seeded scenes.

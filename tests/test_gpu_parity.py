@@ -331,11 +331,33 @@ def test_c4_full_size_sampled():
     """C4 at full size (8 x 128x4096 rays, ~21.8M triangles), in the launch configuration
     bench.py times, checked on sampled rays against the oracle (all triangles per ray)."""
     w = sg.workload("C4", frame=0)
-    dist, tri, st, _ = run(w["emitters"], w["tris"])
+    dist, tri, st, g = run(w["emitters"], w["tris"])
     rays = _sampled(w["emitters"], 24, 9)
     rep, _ = check(w["emitters"], w["tris"], dist, tri, rays=rays)
     assert st["pairs"] == len(w["tris"]) * 8
     assert rep["oracle_hits"] > 20
+    # bench.py's default representation of the same frame (indexed: trivial static indices +
+    # shared car vertices) gives the bit-identical result
+    di, ti = run_indexed_frame(w, g)
+    assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
+
+
+def run_indexed_frame(w, g):
+    v, idx = sg.indexed_frame(w)
+    g.update_triangles(tris_to_float4(v),   # (V, 3) vertices -> (V, 4)
+                       indices=torch.as_tensor(idx, device="cuda"))
+    d, t = g.cast()
+    torch.cuda.synchronize()
+    return d.cpu().numpy(), t.cpu().numpy()
+
+
+def test_c2_indexed_layout():
+    """C2 at full size in bench.py's indexed layout: bit-identical to the soup, parity on sampled rays."""
+    w = sg.workload("C2", frame=3)
+    dist, tri, st, g = run(w["emitters"], w["tris"])
+    di, ti = run_indexed_frame(w, g)
+    assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
+    check(w["emitters"], w["tris"], di, ti, rays=_sampled(w["emitters"], 1024, 11))
 
 
 @pytest.mark.parametrize("n_em", [9, 17])

@@ -45,3 +45,12 @@ def test_pose_and_swd_seeded():
     w = sg.swd(tris, (10, 10, 10), seed=1, frame=0)
     # rigid per-triangle scatter: edge vectors preserved
     np.testing.assert_allclose(w[:, 1] - w[:, 0], tris[:, 1] - tris[:, 0], atol=1e-4)
+
+
+def test_indexed_frame_reproduces_the_soup():
+    """The bench's indexed layout (trivial static indices + shared car vertices) is the same list
+    of triangles as the workload soup, bit for bit."""
+    w = sg.workload("C2", static_scale=0.02, n_cars=2)
+    v, idx = sg.indexed_frame(w)
+    assert idx.shape == (3 * len(w["tris"]),) and v.shape[0] == 3 * w["n_static"] + 2 * 389 * 389
+    assert np.array_equal(v[idx].reshape(-1, 3, 3), w["tris"])
