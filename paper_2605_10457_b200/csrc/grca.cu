@@ -222,7 +222,7 @@ struct EmLitePack {
 
 // K2 per-triangle test (A1 load + A2-A3 pre-test for all NE emitters): keep / range bit masks,
 // channel-culled count; c_area counts paper-mode apparent-area culls.
-template <int NE>
+template <int NE, bool kLevel>
 __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, const float *sSin,
                                        const unsigned char *sLut, long long t, unsigned &keep, unsigned &rng,
                                        unsigned &chan, unsigned &c_area) {
@@ -242,7 +242,7 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
     } else if (P.pairs_ok) {   // all frames orthonormal: packed fp32x2 path
 #pragma unroll
         for (int e = 0; e + 1 < NE; e += 2) {
-            const unsigned r = quick_pair_lut(v, emax, EL.p[e / 2], EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base,
+            const unsigned r = quick_pair_lut<kLevel>(v, emax, EL.p[e / 2], EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base,
                                               sSin + EL.e[e + 1].sin_base, sLut + e * kLutBins,
                                               sLut + (e + 1) * kLutBins);
             kb |= (r & 3u) << e;
@@ -278,7 +278,7 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
     rng = rb;
 }
 
-template <int NE>
+template <int NE, bool kLevel>
 __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid_constant__ KParams P, const EmLitePack EL) {
     extern __shared__ __align__(16) unsigned char smem[];
     float *sSin = reinterpret_cast<float *>(smem);
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid
         unsigned keep = 0u, rng = 0u;
         if (t < P.n_tri) {
             unsigned chan = 0u;
-            k2_tri<NE>(P, EL, sSin, sLut, t, keep, rng, chan, c_area);
+            k2_tri<NE, kLevel>(P, EL, sSin, sLut, t, keep, rng, chan, c_area);
             c_pairs += NE;
             c_chan += chan;
         }
@@ -1046,6 +1046,7 @@ struct grca_ctx {
     cudaAccessPolicyWindow l2win{};
     float noise_sigma = 0.f;           // distance noise (K5), 0 = off
     bool all_ortho = false;
+    bool all_level = false;   // every frame's up row of M^-1 is exactly (0, 0, 1)
     unsigned long long noise_seed = 0;   // persisting window over ray table + hits (num_bytes 0 = off)
     size_t k2f_smem = 0;
     int4 *d_large = nullptr;
@@ -1155,16 +1156,16 @@ KParams params(grca_t h) {
 }
 }  // namespace
 
-static const void *k2_fixed_fn(int ne) {
+static const void *k2_fixed_fn(int ne, bool level) {
     switch (ne) {
-        case 1: return (const void *)k_cull_fixed<1>;
-        case 2: return (const void *)k_cull_fixed<2>;
-        case 3: return (const void *)k_cull_fixed<3>;
-        case 4: return (const void *)k_cull_fixed<4>;
-        case 5: return (const void *)k_cull_fixed<5>;
-        case 6: return (const void *)k_cull_fixed<6>;
-        case 7: return (const void *)k_cull_fixed<7>;
-        default: return (const void *)k_cull_fixed<8>;
+        case 1: return level ? (const void *)k_cull_fixed<1, true> : (const void *)k_cull_fixed<1, false>;
+        case 2: return level ? (const void *)k_cull_fixed<2, true> : (const void *)k_cull_fixed<2, false>;
+        case 3: return level ? (const void *)k_cull_fixed<3, true> : (const void *)k_cull_fixed<3, false>;
+        case 4: return level ? (const void *)k_cull_fixed<4, true> : (const void *)k_cull_fixed<4, false>;
+        case 5: return level ? (const void *)k_cull_fixed<5, true> : (const void *)k_cull_fixed<5, false>;
+        case 6: return level ? (const void *)k_cull_fixed<6, true> : (const void *)k_cull_fixed<6, false>;
+        case 7: return level ? (const void *)k_cull_fixed<7, true> : (const void *)k_cull_fixed<7, false>;
+        default: return level ? (const void *)k_cull_fixed<8, true> : (const void *)k_cull_fixed<8, false>;
     }
 }
 
@@ -1474,7 +1475,11 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     if (use_lut) CK(cudaMemcpy(h->d_lut, lut.data(), sizeof(unsigned char) * lut.size(), cudaMemcpyHostToDevice));
     h->use_lut = use_lut;
     h->all_ortho = true;
-    for (int n = 0; n < n_emitters; ++n) h->all_ortho = h->all_ortho && lites[n].ortho;
+    h->all_level = true;
+    for (int n = 0; n < n_emitters; ++n) {
+        h->all_ortho = h->all_ortho && lites[n].ortho;
+        h->all_level = h->all_level && lites[n].Au[0] == 0.f && lites[n].Au[1] == 0.f && lites[n].Au[2] == 1.f;
+    }
     h->n_em = n_emitters;
     h->st_dirty = h->st_set;   // cached static keys depend on the emitters
     h->n_sin = (int)sins.size();
@@ -1497,7 +1502,7 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     h->kf_smem = kfused_smem_bytes(n_emitters, h->n_sin, use_lut);
     int b2 = 0, b2b = 0, b4s = 0, b4 = 0;
     if (n_emitters <= kFixedEm && use_lut) {   // the fixed kernel relies on the LUT (gamma <= 255)
-        const void *fn = k2_fixed_fn(n_emitters);
+        const void *fn = k2_fixed_fn(n_emitters, false);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, fn, K2_THREADS, h->k2f_smem));
     } else {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_cull, K2_THREADS, h->k2_smem));
@@ -1593,7 +1598,7 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
         const long long grid = std::min<long long>(tiles, (long long)h->num_sms * h->k2_blocks_per_sm);
         if (h->n_em <= kFixedEm && h->use_lut) {
             void *args[] = {(void *)&P, (void *)&h->lite_pack};
-            CK(cudaLaunchKernel(k2_fixed_fn(h->n_em), dim3((unsigned)grid), dim3(K2_THREADS), args, h->k2f_smem,
+            CK(cudaLaunchKernel(k2_fixed_fn(h->n_em, h->all_level && P.pairs_ok), dim3((unsigned)grid), dim3(K2_THREADS), args, h->k2f_smem,
                                 h->stream));
         } else {
             k_cull<<<(unsigned)grid, K2_THREADS, h->k2_smem, h->stream>>>(P);

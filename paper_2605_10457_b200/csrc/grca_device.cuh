@@ -650,7 +650,10 @@ struct EmPair {
     float2 u[3];    // Au_x, Au_y, Au_z
 };
 
-// two emitters at once; returns bits (keep0, keep1) | (range0, range1) << 2
+// two emitters at once; returns bits (keep0, keep1) | (range0, range1) << 2.  kLevel: both frames
+// level (up row of M^-1 exactly (0, 0, 1), checked on the host), so x_u = a_z -- the same value
+// the general dot product gives for that row, bit for bit.
+template <bool kLevel = false>
 __device__ __forceinline__ unsigned quick_pair_lut(const f3 v[3], float emax, const EmPair &PR, const EmLite &L0,
                                                    const EmLite &L1, const float *sinT0, const float *sinT1,
                                                    const unsigned char *lut0, const unsigned char *lut1) {
@@ -661,7 +664,7 @@ __device__ __forceinline__ unsigned quick_pair_lut(const f3 v[3], float emax, co
         const float2 ay = __fadd2_rn(f2(v[k].y, v[k].y), PR.no[1]);
         const float2 az = __fadd2_rn(f2(v[k].z, v[k].z), PR.no[2]);
         const float2 w2 = __ffma2_rn(az, az, __ffma2_rn(ay, ay, __fmul2_rn(ax, ax)));
-        const float2 xu = __ffma2_rn(PR.u[2], az, __ffma2_rn(PR.u[1], ay, __fmul2_rn(PR.u[0], ax)));
+        const float2 xu = kLevel ? az : __ffma2_rn(PR.u[2], az, __ffma2_rn(PR.u[1], ay, __fmul2_rn(PR.u[0], ax)));
         const float2 iw = f2(rsqrtf(w2.x), rsqrtf(w2.y));
         const float2 ss = __fmul2_rn(xu, iw);
         s0[k] = ss.x;
