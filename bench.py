@@ -295,6 +295,9 @@ def main():
     ap.add_argument("--split-refine", action="store_true", help="K2b and K4s as two kernels (A/B)")
     ap.add_argument("--l2-persist", action="store_true", help="A/B: persisting L2 window (opt-in)")
     ap.add_argument("--no-packed", action="store_true", help="A/B: K2 without packed fp32x2 math")
+    ap.add_argument("--merge", choices=["allreduce", "nvls"], default="allreduce",
+                    help="triangle-shard merge: NCCL all-reduce(MIN) of the packed keys, or the fused NVLS "
+                         "multimem.red.min in the intersection kernels (NEXT-f3; needs NVLS multicast)")
     ap.add_argument("--soup", action="store_true", help="triangle-soup scene (float4 triplets) instead of the indexed "
                     "car meshes (same triangles; the e2e upload is then every dynamic triangle's vertices)")
     ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters"])
@@ -373,6 +376,14 @@ def main():
     tri_out = torch.empty(n_rays, dtype=torch.int32, device=device)
 
     merge = world > 1 and shard == "triangles"
+    nvls = None
+    if args.merge == "nvls" and (merge or world == 1):
+        # NEXT-f3: hits reduced in-switch by the intersection kernels (multimem.red.min); no all-reduce
+        nvls = D.NvlsBuffer(g.nvls_status()["bytes_needed"], dev_index)
+        g.set_nvls(nvls.uc_ptr, nvls.mc_ptr, world)
+        if world > 1:
+            dist.barrier()
+        merge = False
 
     def cast_once(dout=dist_out, tout=tri_out):
         if merge:   # triangle shards: exact merge = all-reduce(MIN) of the packed (t, id) keys
@@ -546,7 +557,8 @@ def main():
                        "deformation": args.deformation, "max_range_m": float(ems[0].max_range),
                        "subdiv": args.subdiv, "car_scale": list(scene.scale), "mesh": scene.mesh,
                        "sharding": ("none" if world == 1 else
-                                    f"triangles block-interleaved ({D.BLOCK}) + all-reduce(MIN) x {world}"
+                                    f"triangles block-interleaved ({D.BLOCK}) + "
+                                    f"{'fused NVLS multimem.red.min' if nvls else 'all-reduce(MIN)'} x {world}"
                                     if shard == "triangles" else f"emitters (n mod P) x {world}, no reduction"),
                        "l2": "inputs > L2: 4 resident ~1 GB frame buffers cycled"},
             "frame_ms": ms_step, "rtic_culled_frac": culled,

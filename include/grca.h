@@ -185,6 +185,26 @@ grca_status grca_cast_packed(grca_t h);
 grca_status grca_hits_packed(grca_t h, uint64_t **d_hits, int64_t *n_rays);
 grca_status grca_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri);
 
+/* NEXT-f3: fused NVLS min-merge for triangle-sharded multi-GPU casts (the merge
+ * of PAPER.md's per-ray closest hit over shards, P:2340-2356 f_sort).  d_uc is this rank's unicast
+ * view and d_mc the multicast view (cuMulticastCreate/BindMem/cuMemMap, every rank's memory bound)
+ * of one NVLS buffer of at least grca_nvls_status(..., bytes_needed) bytes: the per-ray packed keys
+ * (n_rays u64, padded to 128 B) followed by a 128-byte barrier word.  Both views 128-byte aligned,
+ * owned by the caller, valid until grca_set_nvls(h, NULL, NULL, 0) or grca_destroy.
+ * After it, every grca_cast / grca_cast_packed on every rank: K0 initialises the rank's own keys,
+ * a device-side barrier (multimem add + acquire spin on the flag) waits for all n_ranks, the
+ * intersection kernels record hits with multimem.red.min.u64 on d_mc (the NVSwitch applies the
+ * min to every rank's copy: no separate all-reduce), a second barrier, then K5 unpacks the merged
+ * keys from d_uc.  Every rank must call grca_set_nvls before any rank casts, and all ranks must
+ * cast the same sequence.  A barrier whose peers never arrive gives up after ~20 s and sets the
+ * timed_out flag of grca_nvls_status (the result is then incomplete).  Errors: GRCA_E_INVALID
+ * (one view missing, n_ranks < 1, misaligned), GRCA_E_STATE (before grca_set_emitters, with
+ * GRCA_DEBUG_COUNT_ALL_HITS; casting with cached static triangles).  NULL, NULL -> merge off. */
+grca_status grca_set_nvls(grca_t h, void *d_uc, void *d_mc, int32_t n_ranks);
+/* Bytes the NVLS buffer needs for the current emitters; timed_out (synchronizes) = 1 if any
+ * barrier of this handle gave up waiting.  Either pointer may be NULL. */
+grca_status grca_nvls_status(grca_t h, int64_t *bytes_needed, int32_t *timed_out);
+
 /* Distance noise (noise model: "a post-processing perturbation added after output
  * conversion"): K5 adds sigma * N(0,1) to every hit distance (clamped at 0; misses stay +inf), the
  * normal drawn from a counter-based generator keyed by (seed, cast index, ray).  sigma <= 0 -> off. */

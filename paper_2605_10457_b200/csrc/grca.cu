@@ -78,6 +78,7 @@ struct KParams {
     unsigned long long *surv;    // dense K2 survivor list: tri << 8 | emitter
     unsigned *n_surv;
     unsigned long long *desc;    // split path: per survivor, small-rectangle descriptor (0 = none)
+    unsigned long long *mc_hits; // NEXT-f3: multicast view of the ranks' hit buffers (NULL = local RED.MIN)
 };
 
 // slot fields (SoA per warp in shared memory) for the inline small-pair expansion
@@ -122,7 +123,25 @@ __global__ void k_init(unsigned long long *hits, unsigned *allhits, long long n,
     if (allhits)
         for (long long i = tid; i < n; i += stride) allhits[i] = src_allhits ? src_allhits[i] : 0u;
     if (tid < ST_COUNT) stats[tid] = 0ull;
-    if (tid < 8) ctrl[tid] = 0u;
+    if (tid < 7) ctrl[tid] = 0u;   // (ctrl[7]: sticky NVLS barrier timeout flag)
+}
+
+// NEXT-f3 device-side barrier over the NVLS group (one thread): every rank adds 1 to every rank's
+// flag through the multicast address (release), then waits until its own copy reaches
+// target = epoch * n_ranks (acquire).  A peer that never arrives trips the timeout (~20 s), which
+// sets err[0] instead of hanging the GPU.
+__global__ void k_nvls_barrier(unsigned *flag_uc, unsigned *flag_mc, unsigned target, unsigned *err) {
+    __threadfence_system();
+    asm volatile("multimem.red.release.sys.global.add.u32 [%0], %1;" ::"l"(flag_mc), "r"(1u) : "memory");
+    const long long t0 = clock64();
+    unsigned v;
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag_uc) : "memory");
+        if ((int)(v - target) >= 0) break;
+        if (clock64() - t0 > 40000000000ll) { atomicExch(err, 1u); break; }
+        __nanosleep(64);
+    }
+    __threadfence_system();
 }
 
 // ------------------------------------------------------- K2 cull (phase A) --
@@ -555,7 +574,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KP
                     }
                     if (r == 1) {
                         cnt[ST_HITS]++;
-                        record_hit(P.hits, P.allhits, g, th, __float_as_uint(sl[SF_ID * 32]));
+                        record_hit(P.hits, P.mc_hits, P.allhits, g, th, __float_as_uint(sl[SF_ID * 32]));
                     }
                 }
             }
@@ -704,7 +723,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             }
             if (r == 1) {
                 hit = true;
-                record_hit(P.hits, P.allhits, g, th, __float_as_uint(r4.y));
+                record_hit(P.hits, P.mc_hits, P.allhits, g, th, __float_as_uint(r4.y));
             }
         }
         // hit / fp64 counts: warp-uniform sums (a per-lane counter live across the loop would be
@@ -814,7 +833,7 @@ __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev
                 ++items;
                 int res = P.force64 ? 2 : test_fast(d, S, E.dmax_lo, E.dmax_hi, th);
                 if (res == 2) { ++fp64; res = test_exact_r(v, em_o(E), d, E.dmax, P.faces, th); }
-                if (res == 1) { ++hits; record_hit(P.hits, P.allhits, g, th, id); }
+                if (res == 1) { ++hits; record_hit(P.hits, P.mc_hits, P.allhits, g, th, id); }
             }
     }
     atomicAdd(P.stats + ST_ITEMS_LARGE, (unsigned long long)items);
@@ -968,7 +987,7 @@ __global__ void __launch_bounds__(K4_THREADS, K4_MINB) k_isect(const __grid_cons
             }
             if (r == 1) {
                 cnt[ST_HITS]++;
-                record_hit(P.hits, P.allhits, g, th, id);
+                record_hit(P.hits, P.mc_hits, P.allhits, g, th, id);
             }
         }
     }
@@ -1032,6 +1051,11 @@ struct grca_ctx {
     // device buffers
     float4 *d_raytab = nullptr;
     unsigned long long *d_hits = nullptr;
+    // NEXT-f3 fused NVLS merge (grca_set_nvls): this rank's unicast view and the multicast view of
+    // the caller's NVLS-bound buffer [n_rays keys][barrier flag]; nvls_epoch counts barriers
+    unsigned long long *nvls_uc = nullptr, *nvls_mc = nullptr;
+    int nvls_n = 0;
+    unsigned nvls_epoch = 0;
     unsigned *d_allhits = nullptr;
     EmDev *d_em = nullptr;
     float *d_sin = nullptr;
@@ -1130,7 +1154,8 @@ KParams params(grca_t h) {
     P.n_em = h->n_em;
     P.n_sin = h->n_sin;
     P.raytab = h->d_raytab;
-    P.hits = h->d_hits;
+    P.hits = h->nvls_uc ? h->nvls_uc : h->d_hits;
+    P.mc_hits = h->nvls_mc;
     P.allhits = (h->ci.debug_flags & GRCA_DEBUG_COUNT_ALL_HITS) ? h->d_allhits : nullptr;
     P.large = h->d_large;
     P.n_large = h->d_ctrl + 0;
@@ -1637,9 +1662,22 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
     return GRCA_OK;
 }
 
+static size_t nvls_flag_offset(long long n_rays) { return (size_t)((n_rays + 15) / 16) * 16; }   // in u64 words
+
+static cudaError_t nvls_barrier(grca_t h) {
+    ++h->nvls_epoch;
+    const size_t off = nvls_flag_offset(h->n_rays);
+    k_nvls_barrier<<<1, 1, 0, h->stream>>>(reinterpret_cast<unsigned *>(h->nvls_uc + off),
+                                           reinterpret_cast<unsigned *>(h->nvls_mc + off),
+                                           h->nvls_epoch * (unsigned)h->nvls_n, h->d_ctrl + 7);
+    return cudaGetLastError();
+}
+
 static grca_status launch_packed(grca_t h) {
     if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
     if (!h->have_tri && !h->st_set) return fail(h, GRCA_E_STATE, "grca_update_triangles has not been called");
+    if (h->nvls_mc && h->st_set)
+        return fail(h, GRCA_E_STATE, "the fused NVLS merge cannot be combined with cached static triangles");
     DeviceGuard dg(h->device);
     const int slot = (int)(h->n_casts % kRing);
     const bool prof = h->ev_ok;
@@ -1663,15 +1701,19 @@ static grca_status launch_packed(grca_t h) {
     if (prof) CK(cudaEventRecord(h->ev[slot][0], h->stream));
     {   // K0
         const int grid = h->num_sms * 4;
-        k_init<<<grid, 256, 0, h->stream>>>(h->d_hits, P.allhits, h->n_rays, h->d_ctrl, h->d_stats,
+        k_init<<<grid, 256, 0, h->stream>>>(P.hits, P.allhits, h->n_rays, h->d_ctrl, h->d_stats,
                                             h->st_set ? h->d_static_keys : nullptr,
                                             (h->st_set && P.allhits) ? h->d_static_allhits : nullptr);
         CK(cudaGetLastError());
     }
+    // NVLS: no rank may reduce into a peer's copy before the peer has initialised it
+    if (h->nvls_mc) CK(nvls_barrier(h));
     if (prof) CK(cudaEventRecord(h->ev[slot][1], h->stream));
     if (!h->have_tri) P.n_tri = 0;
     grca_status st = launch_core(h, P, P.n_tri, prof, slot);
     if (st != GRCA_OK) return st;
+    // NVLS: every rank's reductions have landed in every copy before anyone unpacks
+    if (h->nvls_mc) CK(nvls_barrier(h));
     if (prof) CK(cudaEventRecord(h->ev[slot][6], h->stream));
     return GRCA_OK;
 }
@@ -1682,7 +1724,7 @@ static grca_status launch_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri
     if (d_out_dist || d_out_tri) {
         const long long blocks = std::min<long long>((h->n_rays + 255) / 256, (long long)h->num_sms * 8);
         k_unpack<<<(unsigned)std::max<long long>(1, blocks), 256, 0, h->stream>>>(
-            h->d_hits, d_out_dist, d_out_tri, h->n_rays, h->noise_sigma, h->noise_seed, (unsigned long long)h->n_casts);
+            h->nvls_uc ? h->nvls_uc : h->d_hits, d_out_dist, d_out_tri, h->n_rays, h->noise_sigma, h->noise_seed, (unsigned long long)h->n_casts);
         CK(cudaGetLastError());
     }
     if (h->ev_ok) CK(cudaEventRecord(h->ev[slot][7], h->stream));
@@ -1754,8 +1796,45 @@ grca_status grca_cast(grca_t h, float *d_out_dist, int32_t *d_out_tri, grca_stat
 
 grca_status grca_hits_packed(grca_t h, uint64_t **d_hits, int64_t *n_rays) {
     if (!h || !d_hits) return GRCA_E_INVALID;
-    *d_hits = reinterpret_cast<uint64_t *>(h->d_hits);
+    *d_hits = reinterpret_cast<uint64_t *>(h->nvls_uc ? h->nvls_uc : h->d_hits);
     if (n_rays) *n_rays = h->n_rays;
+    return GRCA_OK;
+}
+
+grca_status grca_set_nvls(grca_t h, void *d_uc, void *d_mc, int32_t n_ranks) {
+    if (!h) return GRCA_E_INVALID;
+    if (!d_uc && !d_mc) {   // back to the handle's own buffer and local RED.MIN
+        h->nvls_uc = h->nvls_mc = nullptr;
+        h->nvls_n = 0;
+        return GRCA_OK;
+    }
+    if (!d_uc || !d_mc || n_ranks < 1) return fail(h, GRCA_E_INVALID, "need both views and n_ranks >= 1");
+    if ((((uintptr_t)d_uc) | ((uintptr_t)d_mc)) & 127) return fail(h, GRCA_E_INVALID, "views must be 128-byte aligned");
+    if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters first (the buffer holds one key per ray)");
+    if (h->ci.debug_flags & GRCA_DEBUG_COUNT_ALL_HITS)
+        return fail(h, GRCA_E_STATE, "all-hit counting is per rank: not available with the fused NVLS merge");
+    DeviceGuard dg(h->device);
+    h->nvls_uc = reinterpret_cast<unsigned long long *>(d_uc);
+    h->nvls_mc = reinterpret_cast<unsigned long long *>(d_mc);
+    h->nvls_n = n_ranks;
+    h->nvls_epoch = 0;
+    // this rank's barrier flag starts at 0 (callers barrier on the host after every rank set it)
+    CK(cudaMemsetAsync(h->nvls_uc + nvls_flag_offset(h->n_rays), 0, 128, h->stream));
+    CK(cudaMemsetAsync(h->d_ctrl + 7, 0, sizeof(unsigned), h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return GRCA_OK;
+}
+
+grca_status grca_nvls_status(grca_t h, int64_t *bytes_needed, int32_t *timed_out) {
+    if (!h) return GRCA_E_INVALID;
+    if (bytes_needed) *bytes_needed = (int64_t)(nvls_flag_offset(h->n_rays) * 8 + 128);
+    if (timed_out) {
+        DeviceGuard dg(h->device);
+        unsigned v = 0;
+        CK(cudaStreamSynchronize(h->stream));
+        CK(cudaMemcpy(&v, h->d_ctrl + 7, sizeof(unsigned), cudaMemcpyDeviceToHost));
+        *timed_out = (int32_t)v;
+    }
     return GRCA_OK;
 }
 

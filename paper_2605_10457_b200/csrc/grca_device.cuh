@@ -883,10 +883,17 @@ __device__ __forceinline__ int test_exact_r(const f3 v[3], f3 o, float4 d4, doub
 
 // Closest-hit update on the packed key (fp32 t bits << 32 | id).  t > 0 so the raw bits
 // order like the value (PAPER.md:2343-2356 f_sort, widened with the id as tie-break).
-__device__ __forceinline__ void record_hit(unsigned long long *hits, unsigned *allhits, int g, float t, uint32_t id) {
+// mc != NULL (NEXT-f3 fused NVLS merge): the key goes to the multicast address of the ranks' hit
+// buffers, and the NVSwitch applies the min to every rank's copy (multimem.red: no separate
+// all-reduce).  Otherwise a local RED.MIN.
+__device__ __forceinline__ void record_hit(unsigned long long *hits, unsigned long long *mc, unsigned *allhits, int g,
+                                           float t, uint32_t id) {
     const unsigned long long key = ((unsigned long long)__float_as_uint(t) << 32) | id;
     if (allhits) atomicAdd(allhits + g, 1u);
-    atomicMin(hits + g, key);   // result unused -> RED.MIN: fire-and-forget, no L2 round trip
+    if (mc)
+        asm volatile("multimem.red.relaxed.sys.global.min.u64 [%0], %1;" ::"l"(mc + g), "l"(key) : "memory");
+    else
+        atomicMin(hits + g, key);   // result unused -> RED.MIN: fire-and-forget, no L2 round trip
 }
 
 }  // namespace grca

@@ -100,3 +100,96 @@ class ShardedCaster:
         merge_packed(self.g.hits_packed(), self.group)
         self.g.unpack(out_dist, out_tri)
         return out_dist, out_tri
+
+
+# ----------------------------------------------------------- NEXT-f3 NVLS buffer --
+def _ck(res):
+    """cuda.bindings returns (err, *values); raise on error, return the value(s)."""
+    from cuda.bindings import driver as cu
+
+    err = res[0]
+    if err != cu.CUresult.CUDA_SUCCESS:
+        raise RuntimeError(f"CUDA driver error {err}")
+    return res[1] if len(res) == 2 else res[1:]
+
+
+class NvlsBuffer:
+    """Host plumbing of the fused NVLS merge (NEXT-f3; grca_set_nvls): one buffer of >= nbytes
+    bound to a multicast object over the ranks of `group` (or a single-device multicast object
+    when torch.distributed is not initialised), mapped twice on this rank:
+      uc_ptr -- this rank's own copy (unicast), read by K0 / K5;
+      mc_ptr -- the multicast view: a multimem reduction there lands in every rank's copy.
+    Rank 0 creates the object and shares it as a fabric handle (broadcast over `group`); every
+    rank adds its device, then binds its own physical memory, then maps both views.  Nothing
+    here computes any part of the method."""
+
+    def __init__(self, nbytes: int, device_index: int, group=None):
+        import torch.distributed as dist
+        from cuda.bindings import driver as cu
+
+        self._cu = cu
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        _ck(cu.cuInit(0))
+        dev = _ck(cu.cuDeviceGet(int(device_index)))
+        if not _ck(cu.cuDeviceGetAttribute(cu.CUdevice_attribute.CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev)):
+            raise RuntimeError("multicast (NVLS) not supported on this device")
+        fabric = cu.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_FABRIC
+        prop = cu.CUmulticastObjectProp()
+        prop.numDevices = self.world
+        prop.handleTypes = fabric if self.world > 1 else cu.CUmemAllocationHandleType.CU_MEM_HANDLE_TYPE_NONE
+        prop.size = int(nbytes)
+        gran = int(_ck(cu.cuMulticastGetGranularity(
+            prop, cu.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED)))
+        aprop = cu.CUmemAllocationProp()
+        aprop.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+        aprop.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        aprop.location.id = int(device_index)
+        agran = int(_ck(cu.cuMemGetAllocationGranularity(
+            aprop, cu.CUmemAllocationGranularity_flags.CU_MEM_ALLOC_GRANULARITY_RECOMMENDED)))
+        align = max(gran, agran)
+        self.size = (int(nbytes) + align - 1) // align * align
+        prop.size = self.size
+        if self.rank == 0:
+            self.mc = _ck(cu.cuMulticastCreate(prop))
+        if self.world > 1:   # share the object: fabric handle bytes over the process group
+            payload = [bytes(_ck(cu.cuMemExportToShareableHandle(self.mc, fabric, 0)).data) if self.rank == 0
+                       else None]
+            dist.broadcast_object_list(payload, src=0, group=group)
+            if self.rank != 0:
+                fh = cu.CUmemFabricHandle()
+                fh.data = payload[0]
+                self.mc = _ck(cu.cuMemImportFromShareableHandle(fh, fabric))
+        _ck(cu.cuMulticastAddDevice(self.mc, dev))
+        if self.world > 1:
+            dist.barrier(group)   # every device added before any memory is bound
+        self.mem = _ck(cu.cuMemCreate(self.size, aprop, 0))
+        _ck(cu.cuMulticastBindMem(self.mc, 0, self.mem, 0, self.size, 0))
+        if self.world > 1:
+            dist.barrier(group)
+        acc = cu.CUmemAccessDesc()
+        acc.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        acc.location.id = int(device_index)
+        acc.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+        self.uc_ptr = int(_ck(cu.cuMemAddressReserve(self.size, align, 0, 0)))
+        _ck(cu.cuMemMap(self.uc_ptr, self.size, 0, self.mem, 0))
+        _ck(cu.cuMemSetAccess(self.uc_ptr, self.size, [acc], 1))
+        self.mc_ptr = int(_ck(cu.cuMemAddressReserve(self.size, align, 0, 0)))
+        _ck(cu.cuMemMap(self.mc_ptr, self.size, 0, self.mc, 0))
+        _ck(cu.cuMemSetAccess(self.mc_ptr, self.size, [acc], 1))
+        _ck(cu.cuMemsetD8(self.uc_ptr, 0, self.size))
+        _ck(cu.cuCtxSynchronize())
+        self._dev = dev
+
+    def close(self):
+        cu = self._cu
+        if getattr(self, "mc_ptr", 0):
+            cu.cuCtxSynchronize()
+            cu.cuMemUnmap(self.mc_ptr, self.size)
+            cu.cuMemAddressFree(self.mc_ptr, self.size)
+            cu.cuMemUnmap(self.uc_ptr, self.size)
+            cu.cuMemAddressFree(self.uc_ptr, self.size)
+            cu.cuMulticastUnbind(self.mc, self._dev, 0, self.size)
+            cu.cuMemRelease(self.mem)
+            cu.cuMemRelease(self.mc)
+            self.mc_ptr = self.uc_ptr = 0

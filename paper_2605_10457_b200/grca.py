@@ -26,6 +26,7 @@ EXPORTS = [
     "grca_create", "grca_destroy", "grca_set_emitters", "grca_update_triangles", "grca_cast",
     "grca_cast_packed", "grca_hits_packed", "grca_set_static_triangles", "grca_clear_static", "grca_unpack", "grca_get_stats", "grca_kernel_times", "grca_set_distance_noise",
     "grca_debug_all_hits", "grca_debug_large_list", "grca_debug_fast_atan2", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
+    "grca_set_nvls", "grca_nvls_status",
 ]
 
 
@@ -97,6 +98,8 @@ def load(path: str = LIB_PATH):
         "grca_debug_fast_atan2": ([vp, vp, vp, i64], C.c_int),
         "grca_get_layout": ([vp, C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "grca_debug_ray_table": ([vp, vp], C.c_int),
+        "grca_set_nvls": ([vp, vp, vp, i32], C.c_int),
+        "grca_nvls_status": ([vp, C.POINTER(i64), C.POINTER(i32)], C.c_int),
         "grca_last_error": ([vp], C.c_char_p),
         "grca_version": ([], C.c_char_p),
     }
@@ -239,6 +242,16 @@ class Grca:
         self._tri_refs = (vertices, indices, tri_ids)
         self.n_triangles = ntri
         return self
+
+    # -- grca_set_nvls / grca_nvls_status (NEXT-f3 fused NVLS merge; plumbing in dist.NvlsBuffer)
+    def set_nvls(self, uc_ptr, mc_ptr, n_ranks: int):
+        self._check(self._L.grca_set_nvls(self._h, C.c_void_p(uc_ptr or None), C.c_void_p(mc_ptr or None),
+                                          int(n_ranks)))
+
+    def nvls_status(self) -> dict:
+        need, to = C.c_int64(), C.c_int32()
+        self._check(self._L.grca_nvls_status(self._h, C.byref(need), C.byref(to)))
+        return {"bytes_needed": need.value, "timed_out": bool(to.value)}
 
     # -- grca_set_static_triangles / grca_clear_static (hybrid static/dynamic, NEXT-f2)
     def set_static_triangles(self, vertices, indices=None, tri_ids=None, tri_id_base: int = 0, n_triangles=None):

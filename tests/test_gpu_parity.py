@@ -540,3 +540,35 @@ def test_distance_noise():
     g2.set_distance_noise(sigma, seed=123)
     d3, _ = [x.cpu().numpy() for x in g2.cast()]
     assert np.array_equal(d3.view(np.uint32), d1.view(np.uint32))   # same seed, same cast index
+
+
+def test_nvls_fused_merge_single_device():
+    """NEXT-f3: with a 1-device multicast (NVLS) object, every hit goes through
+    multimem.red.min.u64 and both device-side barriers run: bit-identical to the local path,
+    over several casts (barrier epochs advance); then back to the local buffer."""
+    from paper_2605_10457_b200 import dist as D
+
+    ems, tris = sg.random_scene(61, n_tris=3000, n_emitters=2, gamma=16, chi=256, extent=10.0)
+    a_d, a_t, _, g = run(ems, tris)
+    need = g.nvls_status()["bytes_needed"]
+    assert need >= 8 * sg.n_rays_total(ems) + 128
+    try:
+        buf = D.NvlsBuffer(need, device_index=0)
+    except RuntimeError as e:  # pragma: no cover - depends on the box
+        pytest.skip(f"no NVLS multicast here: {e}")
+    try:
+        with pytest.raises(GrcaError):
+            g.set_nvls(buf.uc_ptr, None, 1)
+        g.set_nvls(buf.uc_ptr, buf.mc_ptr, 1)
+        for _ in range(3):
+            d, t = g.cast()
+            torch.cuda.synchronize()
+            assert np.array_equal(t.cpu().numpy(), a_t)
+            assert np.array_equal(d.cpu().numpy().view(np.uint32), a_d.view(np.uint32))
+        assert not g.nvls_status()["timed_out"]
+        g.set_nvls(None, None, 0)
+        d, t = g.cast()
+        torch.cuda.synchronize()
+        assert np.array_equal(t.cpu().numpy(), a_t)
+    finally:
+        buf.close()
