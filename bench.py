@@ -560,7 +560,9 @@ def main():
                                     f"triangles block-interleaved ({D.BLOCK}) + "
                                     f"{'fused NVLS multimem.red.min' if nvls else 'all-reduce(MIN)'} x {world}"
                                     if shard == "triangles" else f"emitters (n mod P) x {world}, no reduction"),
-                       "l2": "inputs > L2: 4 resident ~1 GB frame buffers cycled"},
+                       "l2": f"inputs > L2: {N_FRAMES} resident frame buffers of "
+                             f"{scene.frames[0].numel() * 4 / 1e9:.2f} GB (+ {0 if scene.indices is None else scene.indices.numel() * 4 / 1e9:.2f} GB "
+                             "shared indices) cycled"},
             "frame_ms": ms_step, "rtic_culled_frac": culled,
             "rtic_tested_per_frame": stats["rtic_tested"], "rtic_brute_per_frame": stats["rtic_brute"],
             "rtic_per_s": stats["rtic_tested"] / (ms_step / 1e3),
