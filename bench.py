@@ -532,6 +532,9 @@ def main():
                           "only the dynamic ones -- exact (min-lattice); context, not the headline (PAPER.md:2077-2085)"}
         gh.close()
 
+    # our kernels per cast (cf. the ncu launch list): K0, K2, fused K2b+K4s (split: K2b and K4s),
+    # K3, K4, K5; the fused NVLS merge adds its two barrier kernels
+    launches_per_cast = 6 + (1 if args.split_refine else 0) + (2 if nvls is not None else 0)
     # ---- per-kernel roofline (per-kernel CUDA events on the launch stream, last <= 64 steps)
     kernel_ms = {n: kms[i] for i, n in enumerate(KERNELS)}
     roof = kernel_rooflines(kernel_ms, stats, n_rays, scene.n_tri, len(ems), clk, device, split=args.split_refine,
@@ -573,7 +576,7 @@ def main():
             "stats": {k: stats[k] for k in ("prefilter_survivors", "rtic_small",
                 "pairs", "range_culled", "channel_culled", "azimuth_culled", "survivors", "small_pairs", "large_pairs",
                 "chunks", "fp64_fallbacks", "hits_recorded", "overflow")},
-            "roofline": roofline, "gpu_launches": 7 * args.steps, "clocks": clk,
+            "roofline": roofline, "gpu_launches": launches_per_cast * args.steps, "clocks": clk,
             "e2e": e2e, "cpu_baseline": cpu, "hybrid_static_cache": hybrid,
             "context": "paper (PAPER.md:1758-1762): GRCA_GPU 10.7 ms/frame on RTX 5090 for PP30 Omega=8 "
                        "(3.9e8 rays/s), 1.98x OptiX 9.1; other hardware, not a target",
