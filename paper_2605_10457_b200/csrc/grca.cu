@@ -738,6 +738,13 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
     __syncwarp();
 }
 
+// lane-0 atomic add without the compiler's warp-aggregation wrapper (a single issuing lane)
+__device__ __forceinline__ unsigned atom_add_u32(unsigned *p, unsigned v) {
+    unsigned old;
+    asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
 __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4 *sSlot = reinterpret_cast<float4 *>(smem);   // [warp][6][32]
@@ -764,14 +771,14 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
     const unsigned nr = (ns + 31) >> 5;   // dense rounds of 32 survivors
     // dynamic round fetching (one global atomic per warp per round): no tail imbalance
     unsigned w = 0;
-    if (lane == 0) w = atomicAdd(P.n_surv + 2, 1u);
+    if (lane == 0) w = atom_add_u32(P.n_surv + 2, 1u);
     w = __shfl_sync(FULL, w, 0);
     for (; w < nr;) {
         unsigned wn = 0;
-        if (lane == 0) wn = atomicAdd(P.n_surv + 2, 1u);   // next round, fetched early (latency hidden)
-        const bool valid = (int)(w * 32u) + lane < (int)ns;
-        refine_round(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, lane, valid,
-                     valid ? __ldcs(P.surv + (int)(w * 32u) + lane) : 0ull);
+        if (lane == 0) wn = atom_add_u32(P.n_surv + 2, 1u);   // next round, fetched early (latency hidden)
+        const unsigned idx = w * 32u + (unsigned)lane;
+        const bool valid = idx < ns;
+        refine_round(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, lane, valid, valid ? __ldcs(P.surv + idx) : 0ull);
         w = __shfl_sync(FULL, wn, 0);
     }
     __syncthreads();

@@ -238,7 +238,12 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
     f3 a[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) a[k] = subf(v[k], o);
-    if (!(finite3(a[0]) && finite3(a[1]) && finite3(a[2]))) return CULL_DEGENERATE;
+    {   // non-finite input (inf / NaN coordinates) -> degenerate: inf and NaN propagate through the
+        // sum (inf - inf = NaN), so one test covers all nine values (finite sums cannot reach inf
+        // below |coordinates| ~ 3.8e37)
+        const float sum = ((a[0].x + a[0].y) + (a[0].z + a[1].x)) + ((a[1].y + a[1].z) + (a[2].x + a[2].y)) + a[2].z;
+        if (!(fabsf(sum) < CUDART_INF_F)) return CULL_DEGENERATE;
+    }
     if (nocull) {
         R.c_from = 0; R.c_to = E.gamma - 1; R.r_lo = 0; R.r_len = E.chi; R.pole_rows = 0;
         return CULL_KEEP;
