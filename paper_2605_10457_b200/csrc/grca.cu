@@ -399,6 +399,11 @@ __global__ void __launch_bounds__(K2_THREADS) k_refine(const __grid_constant__ K
     // work = rounds of 32 survivor entries, interleaved over all warps (balanced: no tile tails)
     const unsigned ns = *P.n_surv;
     const unsigned nr = (ns + 31) >> 5;   // dense rounds of 32 survivors
+    // Small-rectangle cap scaled to the load: with few rounds per warp the longest round is the
+    // kernel's tail, so big rectangles go to the chunk-balanced K3/K4 path instead (same results:
+    // both paths run the same certified test).  C4: ~56 rounds/warp -> small_max; C2: ~1 -> 64.
+    const unsigned rpw = nr / (gridDim.x * (KF_THREADS / 32));
+    const int smax = min(P.small_max, (int)max(64u, min(rpw, 1024u) * 16u));
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
     for (unsigned w = wid; w < nr; w += nwarps) {
@@ -481,6 +486,11 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KP
     unsigned setup64 = 0;
     const unsigned ns = *P.n_surv;
     const unsigned nr = (ns + 31) >> 5;   // dense rounds of 32 survivors
+    // Small-rectangle cap scaled to the load: with few rounds per warp the longest round is the
+    // kernel's tail, so big rectangles go to the chunk-balanced K3/K4 path instead (same results:
+    // both paths run the same certified test).  C4: ~56 rounds/warp -> small_max; C2: ~1 -> 64.
+    const unsigned rpw = nr / (gridDim.x * (KF_THREADS / 32));
+    const int smax = min(P.small_max, (int)max(64u, min(rpw, 1024u) * 16u));
     const unsigned wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const unsigned nwarps = (gridDim.x * blockDim.x) >> 5;
     for (unsigned w = wid; w < nr; w += nwarps) {
@@ -596,7 +606,8 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KP
 // list.  Warp-collective; slot / excl are this warp's shared-memory staging areas.
 __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, const float *sSin,
                                              const unsigned char *sLut, float4 *slot, int *excl,
-                                             unsigned long long *wc, int lane, bool valid, unsigned long long ent) {
+                                             unsigned long long *wc, int smax, int lane, bool valid,
+                                             unsigned long long ent) {
     // per-lane category = the stat it counts (warp-private counters wc[], no atomics)
     enum { C_NONE = -1, C_SMALL = ST_SMALL, C_LARGE = ST_LARGE, C_OVF = ST_OVF_LARGE, C_RANGE = ST_RANGE,
            C_CHAN = ST_CHANNEL, C_AZI = ST_AZIMUTH, C_DEGEN = ST_DEGEN };
@@ -619,7 +630,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             sat = !wraps && (R.c_to - R.c_from + 1) <= 64 && R.r_len <= 64;
             bat = !sat;
             const long long items = rect_items(R, E);
-            if (items <= P.small_max && !R.pole_rows) {
+            if (items <= smax && !R.pole_rows) {
                 if (setup_to_slot(v, em_o(E), P.faces, slot + lane, tri_id(P.tri, t), (int)t, e)) {
                     my = (int)items;
                     cat = C_SMALL;
@@ -769,6 +780,11 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
     int *excl = sExcl + wib * 32;
     const unsigned ns = *P.n_surv;
     const unsigned nr = (ns + 31) >> 5;   // dense rounds of 32 survivors
+    // Small-rectangle cap scaled to the load: with few rounds per warp the longest round is the
+    // kernel's tail, so big rectangles go to the chunk-balanced K3/K4 path instead (same results:
+    // both paths run the same certified test).  C4: ~56 rounds/warp -> small_max; C2: ~1 -> 64.
+    const unsigned rpw = nr / (gridDim.x * (KF_THREADS / 32));
+    const int smax = min(P.small_max, (int)max(64u, min(rpw, 1024u) * 16u));
     // dynamic round fetching (one global atomic per warp per round): no tail imbalance
     unsigned w = 0;
     if (lane == 0) w = atom_add_u32(P.n_surv + 2, 1u);
@@ -778,7 +794,8 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
         if (lane == 0) wn = atom_add_u32(P.n_surv + 2, 1u);   // next round, fetched early (latency hidden)
         const unsigned idx = w * 32u + (unsigned)lane;
         const bool valid = idx < ns;
-        refine_round(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, lane, valid, valid ? __ldcs(P.surv + idx) : 0ull);
+        refine_round(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
+                     valid ? __ldcs(P.surv + idx) : 0ull);
         w = __shfl_sync(FULL, wn, 0);
     }
     __syncthreads();

@@ -375,8 +375,11 @@ def test_split_refine_path_identical():
     a = run(ems, tris)
     b = run(ems, tris, flags=G.DEBUG_SPLIT_REFINE)
     assert np.array_equal(a[1], b[1]) and np.array_equal(a[0].view(np.uint32), b[0].view(np.uint32))
-    for k in ("survivors", "small_pairs", "large_pairs", "rtic_tested", "hits_recorded"):
+    # the fused path scales its small-rectangle cap to the load (more pairs may take K3/K4, whose
+    # per-channel refinement trims candidates): compare the invariants
+    for k in ("survivors", "hits_recorded"):
         assert a[2][k] == b[2][k], k
+    assert a[2]["small_pairs"] + a[2]["large_pairs"] == b[2]["small_pairs"] + b[2]["large_pairs"]
     check(ems, tris, a[0], a[1])
 
 
