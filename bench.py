@@ -141,9 +141,9 @@ class Scene:
             self.indices = torch.cat([torch.arange(self.ns3, dtype=torch.int32, device=device),
                                       self.idx_dyn + self.ns3]).contiguous()
             self.n_dyn_vert = self.n_cars * nv_car
-            # algorithmic K2 read per cast: static 48 B vertices + 12 B indices; cars 12 B indices
-            # per triangle + 16 B per shared vertex
-            self.tri_bytes = self.n_static_local * 60 + len(self.own_dyn) * 12 + self.n_dyn_vert * 16
+            # packed float3 vertices (grca_update_triangles_f3).  Algorithmic K2 read per cast:
+            # static 36 B vertices + 12 B indices; cars 12 B indices per triangle + 12 B per shared vertex
+            self.tri_bytes = self.n_static_local * 48 + len(self.own_dyn) * 12 + self.n_dyn_vert * 12
         else:
             self.car = torch.as_tensor(w["car_local"], dtype=torch.float32, device=device)   # (m, 3, 3)
             self.own_dyn_t = torch.as_tensor(self.own_dyn, device=device)
@@ -151,7 +151,7 @@ class Scene:
         self.frames = []
         for fr in range(N_FRAMES):
             nd = self.n_dyn_vert if self.indexed else 3 * (self.n_tri - self.n_static_local)
-            buf = torch.zeros((self.ns3 + nd, 4), dtype=torch.float32, device=device)
+            buf = torch.zeros((self.ns3 + nd, 3 if self.indexed else 4), dtype=torch.float32, device=device)
             buf[: self.ns3, :3] = static
             buf[self.ns3:, :3] = self.dynamic(fr)
             self.frames.append(buf)
@@ -345,7 +345,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2605_10457_b200 import Grca
+    from paper_2605_10457_b200 import Grca, tris_to_float4
     from paper_2605_10457_b200 import dist as D
     from paper_2605_10457_b200 import grca as G
 
@@ -437,7 +437,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         ns3 = scene.ns3
-        n_dyn_vals = scene.frames[0].shape[0] - ns3   # float4 vertices uploaded per step
+        n_dyn_vals = scene.frames[0].shape[0] - ns3   # vertices uploaded per step (float3 / float4)
         host_dyn = [scene.frames[f][ns3:].cpu().pin_memory() for f in range(N_FRAMES)]
         dev_bufs = [scene.frames[0].clone() for _ in range(2)]   # static part resident; dynamic part uploaded
         outs = [(torch.empty(n_rays, dtype=torch.float32, device=device),
@@ -496,7 +496,8 @@ def main():
         # the host results are the cast's (checked on the last step)
         assert torch.equal(host_out[(k_e2e - 1) % 2][1], outs[(k_e2e - 1) % 2][1].cpu())
         e2e = {"value": n_rays_job * k_e2e / (ems_e2e / 1e3), "unit": "rays/s", "ms_per_step": ems_e2e / k_e2e,
-               "h2d_bytes_per_step": int(n_dyn_vals * 16), "d2h_bytes_per_step": int(n_rays * 8), "steps": k_e2e,
+               "h2d_bytes_per_step": int(n_dyn_vals * scene.frames[0].shape[1] * 4), "d2h_bytes_per_step": int(n_rays * 8),
+               "steps": k_e2e,
                "what": f"pinned H2D of this frame's dynamic vertices ({scene.mesh} mesh) + grca_cast + D2H of "
                        "(dist, id) per ray; pipelined over frames (double buffers, H2D/D2H on two copy "
                        "streams overlap the previous/next cast)"}
@@ -508,7 +509,8 @@ def main():
         gh = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays)
         gh.set_emitters(ems)
         ns3 = 3 * scene.n_static_local
-        gh.set_static_triangles(scene.frames[0][:ns3], tri_ids=scene.ids[: scene.n_static_local])
+        st4 = tris_to_float4(scene.frames[0][:ns3])   # set_static_triangles takes float4 vertices
+        gh.set_static_triangles(st4, tri_ids=scene.ids[: scene.n_static_local])
         dyn_ids = scene.ids[scene.n_static_local:]
 
         def hstep(k):

@@ -155,6 +155,11 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
 grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_vertices,
                                   const uint32_t *d_indices, int64_t n_triangles,
                                   const int32_t *d_tri_ids, int32_t tri_id_base);
+/* Same as grca_update_triangles with the vertices as packed float3 (x, y, z: 12 bytes each, 4-byte
+ * aligned) instead of float4 -- a quarter fewer bytes to upload per frame.  Same ownership,
+ * layout of indices / ids and errors (alignment: 4 bytes). */
+grca_status grca_update_triangles_f3(grca_t h, const float *d_xyz, int64_t n_vertices, const uint32_t *d_indices,
+                                     int64_t n_triangles, const int32_t *d_tri_ids, int32_t tri_id_base);
 
 /* Hybrid static/dynamic mode (NEXT-f2; "GRCA on dynamic, static BVH on static,
  * per-ray min merge", here without any BVH): borrow a static triangle set (same conventions as

@@ -1570,14 +1570,17 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
 }
 
 static grca_status check_tri_args(grca_t h, const float *d_vertices, int64_t n_vertices, const uint32_t *d_indices,
-                                  int64_t n_triangles, const int32_t *d_tri_ids, int32_t tri_id_base) {
+                                  int64_t n_triangles, const int32_t *d_tri_ids, int32_t tri_id_base,
+                                  bool packed3 = false) {
     if (n_triangles < 0) return fail(h, GRCA_E_INVALID, "n_triangles < 0");
     if (n_triangles > h->ci.max_triangles) return fail(h, GRCA_E_CAPACITY, "n_triangles exceeds max_triangles");
     if (n_triangles > 0 && !d_vertices) return fail(h, GRCA_E_INVALID, "null vertex buffer");
     if (n_triangles > 0 && d_indices && n_vertices < 1) return fail(h, GRCA_E_INVALID, "indexed mesh with no vertices");
     if (n_triangles > 0 && !d_indices && n_vertices < 3 * n_triangles)
         return fail(h, GRCA_E_INVALID, "non-indexed: n_vertices must be >= 3 * n_triangles");
-    if (((uintptr_t)d_vertices & 15) != 0) return fail(h, GRCA_E_INVALID, "vertex buffer must be 16-byte aligned");
+    if (((uintptr_t)d_vertices & (packed3 ? 3 : 15)) != 0)
+        return fail(h, GRCA_E_INVALID, packed3 ? "float3 vertex buffer must be 4-byte aligned"
+                                               : "vertex buffer must be 16-byte aligned");
     if (tri_id_base < 0 || (!d_tri_ids && (long long)tri_id_base + n_triangles > 0x7fffffffll))
         return fail(h, GRCA_E_INVALID, "triangle ids must be in [0, 2^31)");
     return GRCA_OK;
@@ -1589,6 +1592,22 @@ grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_v
     grca_status st = check_tri_args(h, d_vertices, n_vertices, d_indices, n_triangles, d_tri_ids, tri_id_base);
     if (st != GRCA_OK) return st;
     h->tri.v = reinterpret_cast<const float4 *>(d_vertices);
+    h->tri.v3 = nullptr;
+    h->tri.idx = d_indices;
+    h->tri.ids = d_tri_ids;
+    h->tri.id_base = tri_id_base;
+    h->n_tri = n_triangles;
+    h->have_tri = true;
+    return GRCA_OK;
+}
+
+grca_status grca_update_triangles_f3(grca_t h, const float *d_xyz, int64_t n_vertices, const uint32_t *d_indices,
+                                     int64_t n_triangles, const int32_t *d_tri_ids, int32_t tri_id_base) {
+    if (!h) return GRCA_E_INVALID;
+    grca_status st = check_tri_args(h, d_xyz, n_vertices, d_indices, n_triangles, d_tri_ids, tri_id_base, true);
+    if (st != GRCA_OK) return st;
+    h->tri.v = nullptr;
+    h->tri.v3 = d_xyz;
     h->tri.idx = d_indices;
     h->tri.ids = d_tri_ids;
     h->tri.id_base = tri_id_base;
@@ -1603,6 +1622,7 @@ grca_status grca_set_static_triangles(grca_t h, const float *d_vertices, int64_t
     grca_status st = check_tri_args(h, d_vertices, n_vertices, d_indices, n_triangles, d_tri_ids, tri_id_base);
     if (st != GRCA_OK) return st;
     h->st_tri.v = reinterpret_cast<const float4 *>(d_vertices);
+    h->st_tri.v3 = nullptr;
     h->st_tri.idx = d_indices;
     h->st_tri.ids = d_tri_ids;
     h->st_tri.id_base = tri_id_base;

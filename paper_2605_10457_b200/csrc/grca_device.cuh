@@ -132,19 +132,31 @@ __host__ __device__ __forceinline__ float poly_atan(float z) {
 
 // ----------------------------------------------------------------- A1 load --
 struct TriSrc {
-    const float4 *v;
+    const float4 *v;       // float4 vertices (w ignored), or
+    const float *v3;       // non-NULL: packed float3 vertices (12 B each; grca_update_triangles_f3)
     const uint32_t *idx;   // NULL -> non-indexed triplets
     const int32_t *ids;    // NULL -> id_base + local
     int32_t id_base;
 };
+__device__ __forceinline__ f3 ldcs3(const float *p) { return {__ldcs(p), __ldcs(p + 1), __ldcs(p + 2)}; }
 // Streaming (evict-first) loads: the ~1 GB triangle stream must not evict the L2-resident ray
 // table (67 MB at C4) and hit buffer (33.5 MB) that the intersection kernels gather from.
 __device__ __forceinline__ void load_tri(const TriSrc &T, long long t, f3 v[3]) {
     if (T.idx) {
         const uint32_t i0 = __ldcs(T.idx + 3 * t), i1 = __ldcs(T.idx + 3 * t + 1), i2 = __ldcs(T.idx + 3 * t + 2);
-        v[0] = mk(__ldcs(T.v + i0));
-        v[1] = mk(__ldcs(T.v + i1));
-        v[2] = mk(__ldcs(T.v + i2));
+        if (T.v3) {
+            v[0] = ldcs3(T.v3 + 3ll * i0);
+            v[1] = ldcs3(T.v3 + 3ll * i1);
+            v[2] = ldcs3(T.v3 + 3ll * i2);
+        } else {
+            v[0] = mk(__ldcs(T.v + i0));
+            v[1] = mk(__ldcs(T.v + i1));
+            v[2] = mk(__ldcs(T.v + i2));
+        }
+    } else if (T.v3) {
+        v[0] = ldcs3(T.v3 + 9 * t);
+        v[1] = ldcs3(T.v3 + 9 * t + 3);
+        v[2] = ldcs3(T.v3 + 9 * t + 6);
     } else {
         v[0] = mk(__ldcs(T.v + 3 * t));
         v[1] = mk(__ldcs(T.v + 3 * t + 1));

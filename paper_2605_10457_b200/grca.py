@@ -26,7 +26,7 @@ EXPORTS = [
     "grca_create", "grca_destroy", "grca_set_emitters", "grca_update_triangles", "grca_cast",
     "grca_cast_packed", "grca_hits_packed", "grca_set_static_triangles", "grca_clear_static", "grca_unpack", "grca_get_stats", "grca_kernel_times", "grca_set_distance_noise",
     "grca_debug_all_hits", "grca_debug_large_list", "grca_debug_fast_atan2", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
-    "grca_set_nvls", "grca_nvls_status",
+    "grca_set_nvls", "grca_nvls_status", "grca_update_triangles_f3",
 ]
 
 
@@ -84,6 +84,7 @@ def load(path: str = LIB_PATH):
         "grca_destroy": ([vp], C.c_int),
         "grca_set_emitters": ([vp, C.POINTER(EmitterC), i32], C.c_int),
         "grca_update_triangles": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
+        "grca_update_triangles_f3": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
         "grca_cast": ([vp, vp, vp, C.POINTER(Stats)], C.c_int),
         "grca_cast_packed": ([vp], C.c_int),
         "grca_set_static_triangles": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
@@ -225,9 +226,11 @@ class Grca:
     def update_triangles(self, vertices, indices=None, tri_ids=None, tri_id_base: int = 0, n_triangles=None):
         import torch
 
-        assert vertices.is_cuda and vertices.dtype == torch.float32 and vertices.shape[-1] == 4
+        # (n, 4) float4 vertices -> grca_update_triangles; (n, 3) packed float3 -> grca_update_triangles_f3
+        assert vertices.is_cuda and vertices.dtype == torch.float32 and vertices.shape[-1] in (3, 4)
         assert vertices.is_contiguous()
-        nv = vertices.numel() // 4
+        comps = vertices.shape[-1]
+        nv = vertices.numel() // comps
         if indices is not None:
             assert indices.is_cuda and indices.dtype in (torch.int32, torch.uint32) and indices.is_contiguous()
             ntri = indices.numel() // 3
@@ -237,8 +240,8 @@ class Grca:
             ntri = int(n_triangles)
         if tri_ids is not None:
             assert tri_ids.is_cuda and tri_ids.dtype == torch.int32 and tri_ids.is_contiguous()
-        self._check(self._L.grca_update_triangles(self._h, _ptr(vertices), nv, _ptr(indices), ntri, _ptr(tri_ids),
-                                                  int(tri_id_base)))
+        fn = self._L.grca_update_triangles_f3 if comps == 3 else self._L.grca_update_triangles
+        self._check(fn(self._h, _ptr(vertices), nv, _ptr(indices), ntri, _ptr(tri_ids), int(tri_id_base)))
         self._tri_refs = (vertices, indices, tri_ids)
         self.n_triangles = ntri
         return self

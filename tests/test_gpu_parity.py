@@ -343,9 +343,8 @@ def test_c4_full_size_sampled():
 
 
 def run_indexed_frame(w, g):
-    v, idx = sg.indexed_frame(w)
-    g.update_triangles(tris_to_float4(v),   # (V, 3) vertices -> (V, 4)
-                       indices=torch.as_tensor(idx, device="cuda"))
+    v, idx = sg.indexed_frame(w)   # as bench.py passes it: packed float3 vertices + indices
+    g.update_triangles(torch.as_tensor(v, device="cuda"), indices=torch.as_tensor(idx, device="cuda"))
     d, t = g.cast()
     torch.cuda.synchronize()
     return d.cpu().numpy(), t.cpu().numpy()
@@ -575,3 +574,21 @@ def test_nvls_fused_merge_single_device():
         assert np.array_equal(t.cpu().numpy(), a_t)
     finally:
         buf.close()
+
+
+def test_float3_vertices_identical():
+    """grca_update_triangles_f3 (packed float3 vertices) == float4, soup and indexed, bit for bit."""
+    ems, tris = sg.random_scene(71, n_tris=2500, n_emitters=2, gamma=16, chi=300, extent=9.0)
+    a_d, a_t, _, g = run(ems, tris)
+    v3 = torch.as_tensor(np.ascontiguousarray(tris.reshape(-1, 3)), device="cuda")
+    g.update_triangles(v3)
+    d, t = g.cast()
+    torch.cuda.synchronize()
+    assert np.array_equal(t.cpu().numpy(), a_t) and np.array_equal(d.cpu().numpy().view(np.uint32), a_d.view(np.uint32))
+    flat = np.asarray(tris, np.float32).reshape(-1, 3)
+    uniq, inv = np.unique(flat, axis=0, return_inverse=True)
+    g.update_triangles(torch.as_tensor(np.ascontiguousarray(uniq), device="cuda"),
+                       indices=torch.as_tensor(inv.astype(np.int32).reshape(-1), device="cuda"))
+    d, t = g.cast()
+    torch.cuda.synchronize()
+    assert np.array_equal(t.cpu().numpy(), a_t) and np.array_equal(d.cpu().numpy().view(np.uint32), a_d.view(np.uint32))
