@@ -27,7 +27,10 @@ namespace grca {
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr unsigned long long kMiss = 0x7F800000FFFFFFFFull;
-constexpr int K2_THREADS = 256;   // K2 tile = 256 triangles
+constexpr int K2_THREADS = 256;
+#ifndef K2_TILE
+#define K2_TILE 1024   // triangles per K2 block tile (K2_TILE / K2_THREADS = 4 per thread; measured: 256 -> 0.578, 512 -> 0.543, 1024 -> 0.525 ms)
+#endif
 constexpr int K4_THREADS = 256;
 // fused refine+small: 512 threads x 2 blocks (64 registers) measured best on B200 (occupancy vs spills)
 #ifndef KF_THREADS
@@ -312,18 +315,25 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid
     __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned c_pairs = 0, c_range = 0, c_chan = 0, c_surv = 0, c_area = 0;
-    const long long ntiles = (P.n_tri + K2_THREADS - 1) / K2_THREADS;
+    const long long ntiles = (P.n_tri + K2_TILE - 1) / K2_TILE;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const long long t = tile * K2_THREADS + threadIdx.x;
-        unsigned keep = 0u, rng = 0u;
-        if (t < P.n_tri) {
-            unsigned chan = 0u;
-            k2_tri<NE, kLevel>(P, EL, sSin, sLut, t, keep, rng, chan, c_area);
-            c_pairs += NE;
-            c_chan += chan;
+        // K2_TILE / K2_THREADS triangles per thread (one block scan, barrier pair and atomic for all)
+        unsigned keeps[K2_TILE / K2_THREADS];
+        int cntk = 0;
+#pragma unroll
+        for (int h = 0; h < K2_TILE / K2_THREADS; ++h) {
+            const long long t = tile * K2_TILE + h * K2_THREADS + threadIdx.x;
+            unsigned keep = 0u, rng = 0u;
+            if (t < P.n_tri) {
+                unsigned chan = 0u;
+                k2_tri<NE, kLevel>(P, EL, sSin, sLut, t, keep, rng, chan, c_area);
+                c_pairs += NE;
+                c_chan += chan;
+            }
+            keeps[h] = keep;
+            cntk += __popc(keep);
+            c_range += __popc(rng);
         }
-        const int cntk = __popc(keep);
-        c_range += __popc(rng);
         c_surv += cntk;
         // block-wide exclusive scan of the per-thread survivor counts
         int incl = cntk;
@@ -344,10 +354,15 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid
         if (threadIdx.x == 0) qbase = total ? atomicAdd(P.n_surv, (unsigned)total) : 0u;   // one atomic per tile
         __syncthreads();
         unsigned long long *dst = P.surv + qbase + wbase + incl - cntk;
-        while (keep) {
-            const int e = __ffs(keep) - 1;
-            keep &= keep - 1u;
-            *dst++ = ((unsigned long long)t << 8) | (unsigned)e;
+#pragma unroll
+        for (int h = 0; h < K2_TILE / K2_THREADS; ++h) {
+            const long long t = tile * K2_TILE + h * K2_THREADS + threadIdx.x;
+            unsigned keep = keeps[h];
+            while (keep) {
+                const int e = __ffs(keep) - 1;
+                keep &= keep - 1u;
+                *dst++ = ((unsigned long long)t << 8) | (unsigned)e;
+            }
         }
         __syncthreads();   // wsum / qbase reuse
     }
