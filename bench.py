@@ -280,7 +280,7 @@ def kernel_rooflines(kernel_ms, st, n_rays, n_tri, n_em, clk, device, split=Fals
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--steps", type=int, default=1500)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="C4")
     ap.add_argument("--deformation", default="ND", choices=["ND", "SWD"])
