@@ -448,14 +448,37 @@ def main():
     # are inside the timed region (which starts before the first H2D and ends after the last D2H).
     e2e = None
     if not args.no_e2e:
+        # N > 1: each rank uploads 1/N of the dynamic vertices over its own PCIe link and an
+        # all-gather over NVLink assembles the rest (inside the timed region); each rank reads back
+        # only its own results (sensor shards: its emitters' rays; triangle shards: 1/N of the rays)
         ns3 = scene.ns3
-        n_dyn_vals = scene.frames[0].shape[0] - ns3   # vertices uploaded per step (float3 / float4)
-        host_dyn = [scene.frames[f][ns3:].cpu().pin_memory() for f in range(N_FRAMES)]
-        dev_bufs = [scene.frames[0].clone() for _ in range(2)]   # static part resident; dynamic part uploaded
+        comps = scene.frames[0].shape[1]
+        n_dyn = scene.frames[0].shape[0] - ns3          # dynamic vertices per frame
+        # split only when every rank needs the same dynamic data (indexed scene: all car vertices;
+        # sensor shards: all triangles); a triangle-sharded soup holds per-rank data
+        split = world > 1 and (scene.indexed or shard != "triangles")
+        nsplit = world if split else 1
+        chunk = -(-n_dyn // nsplit)                     # per-rank upload slice (padded)
+        lo_v = (rank if split else 0) * chunk
+        n_mine = max(0, min(chunk, n_dyn - lo_v))
+        host_dyn = []
+        for f in range(N_FRAMES):
+            hs = torch.zeros((chunk, comps), dtype=torch.float32)
+            hs[:n_mine] = scene.frames[f][ns3 + lo_v: ns3 + lo_v + n_mine].cpu()
+            host_dyn.append(hs.pin_memory())
+        dev_bufs = []
+        for _ in range(2):   # static part resident; dynamic part (padded to world * chunk) uploaded
+            db = torch.zeros((ns3 + chunk * nsplit, comps), dtype=torch.float32, device=device)
+            db[:ns3] = scene.frames[0][:ns3]
+            dev_bufs.append(db)
         outs = [(torch.empty(n_rays, dtype=torch.float32, device=device),
                  torch.empty(n_rays, dtype=torch.int32, device=device)) for _ in range(2)]
-        host_out = [(torch.empty(n_rays, dtype=torch.float32).pin_memory(),
-                     torch.empty(n_rays, dtype=torch.int32).pin_memory()) for _ in range(2)]
+        r_lo, r_n = 0, n_rays                           # rays this rank reads back
+        if merge:
+            rch = -(-n_rays // world)
+            r_lo, r_n = rank * rch, max(0, min(rch, n_rays - rank * rch))
+        host_out = [(torch.empty(r_n, dtype=torch.float32).pin_memory(),
+                     torch.empty(r_n, dtype=torch.int32).pin_memory()) for _ in range(2)]
         cs, ds = torch.cuda.Stream(device), torch.cuda.Stream(device)
         ev_h2d = [torch.cuda.Event() for _ in range(2)]
         ev_cast = [torch.cuda.Event() for _ in range(2)]
@@ -467,7 +490,11 @@ def main():
             with torch.cuda.stream(cs):
                 if k >= 2:
                     cs.wait_event(ev_cast[b])   # cast k-2 has released buffer b
-                dev_bufs[b][ns3:].copy_(host_dyn[k % N_FRAMES], non_blocking=True)
+                dyn = dev_bufs[b][ns3:]
+                mine = dyn[lo_v: lo_v + chunk]
+                mine.copy_(host_dyn[k % N_FRAMES], non_blocking=True)
+                if split:   # in place: this rank's slice sits at rank * chunk of the output
+                    dist.all_gather_into_tensor(dyn, mine)
                 ev_h2d[b].record(cs)
 
         def run_e2e(n):
@@ -478,15 +505,15 @@ def main():
                 stream.wait_event(ev_h2d[b])
                 if k >= 2:
                     stream.wait_event(ev_d2h[b])   # host copy of step k-2 done with outs[b]
-                g.update_triangles(dev_bufs[b], indices=scene.indices, tri_ids=scene.ids)
+                g.update_triangles(dev_bufs[b], indices=scene.indices, tri_ids=scene.ids, n_triangles=scene.n_tri)
                 cast_once(*outs[b])
                 ev_cast[b].record(stream)
                 if k + 1 < n:
                     issue_h2d(k + 1)
                 with torch.cuda.stream(ds):
                     ds.wait_event(ev_cast[b])
-                    host_out[b][0].copy_(outs[b][0], non_blocking=True)
-                    host_out[b][1].copy_(outs[b][1], non_blocking=True)
+                    host_out[b][0].copy_(outs[b][0][r_lo: r_lo + r_n], non_blocking=True)
+                    host_out[b][1].copy_(outs[b][1][r_lo: r_lo + r_n], non_blocking=True)
                     ev_d2h[b].record(ds)
             stream.wait_stream(cs)
             stream.wait_stream(ds)
@@ -505,12 +532,17 @@ def main():
             t = torch.tensor([ems_e2e], device=device)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems_e2e = float(t.item())
-        # the host results are the cast's (checked on the last step)
-        assert torch.equal(host_out[(k_e2e - 1) % 2][1], outs[(k_e2e - 1) % 2][1].cpu())
+        # the host results are the cast's (checked on the last step), and the gathered frame equals
+        # the resident one
+        last = (k_e2e - 1) % 2
+        assert torch.equal(host_out[last][1], outs[last][1][r_lo: r_lo + r_n].cpu())
+        fr = (k_e2e - 1) % N_FRAMES
+        assert torch.equal(dev_bufs[last][ns3: ns3 + n_dyn], scene.frames[fr][ns3:])
         e2e = {"value": n_rays_job * k_e2e / (ems_e2e / 1e3), "unit": "rays/s", "ms_per_step": ems_e2e / k_e2e,
-               "h2d_bytes_per_step": int(n_dyn_vals * scene.frames[0].shape[1] * 4), "d2h_bytes_per_step": int(n_rays * 8),
-               "steps": k_e2e,
-               "what": f"pinned H2D of this frame's dynamic vertices ({scene.mesh} mesh) + grca_cast + D2H of "
+               "h2d_bytes_per_step": int(chunk * comps * 4), "d2h_bytes_per_step": int(r_n * 8), "steps": k_e2e,
+               "bytes_scope": "per rank" if world > 1 else "job",
+               "what": f"pinned H2D of this frame's dynamic vertices ({scene.mesh} mesh"
+                       f"{', 1/N per rank + NVLink all-gather' if split else ''}) + grca_cast + D2H of "
                        "(dist, id) per ray; pipelined over frames (double buffers, H2D/D2H on two copy "
                        "streams overlap the previous/next cast)"}
         del dev_bufs
