@@ -345,6 +345,14 @@ def main():
     import torch
     import torch.distributed as dist
 
+    from paper_2605_10457_b200 import build as B
+    if local_rank == 0:
+        B.build()   # no-op when libgrca.so is up to date; a fresh checkout compiles it (nvcc, sm_100a)
+    else:
+        for _ in range(600):   # the other local ranks wait for rank 0's build
+            if os.path.exists(B.LIB):
+                break
+            time.sleep(1.0)
     from paper_2605_10457_b200 import Grca, tris_to_float4
     from paper_2605_10457_b200 import dist as D
     from paper_2605_10457_b200 import grca as G
