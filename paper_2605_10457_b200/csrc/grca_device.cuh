@@ -734,73 +734,17 @@ __device__ __noinline__ double exact_vol(const f3 v[3], f3 o) {
     return dotd(crossd(e1, e2), subd(V0, tod(o)));
 }
 
-// Returns false when the pair can never hit (Vol == 0: origin in the plane / degenerate
-// triangle) or is rejected by the face mode.  setup64 counts fp64 plane-side decisions.
-__device__ __forceinline__ bool make_setup(const f3 v[3], f3 o, int faces, Setup &S, unsigned &setup64) {
-    f3 n[3];
-    float B[3], sg[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        f3 P = v[k], Q = v[(k + 1) % 3];
-        const bool sw = lexless(Q, P);
-        if (sw) { f3 t = P; P = Q; Q = t; }
-        sg[k] = sw ? -1.f : 1.f;
-        f3 aP = subf(P, o), e = subf(Q, P);
-        n[k] = crossf(aP, e);
-        const float pe = __fmul_rn(dotf(aP, aP), dotf(e, e));
-        B[k] = __fmul_rn(16.1f * kU, pe > 0.f ? __fmul_rn(pe, rsqrtf(pe)) : 0.f);   // 16u|a||e| (+ rsqrt slack)
-    }
-    // plane (N, h) in fp64 from the exact fp64 edges, rounded: t = h / d.N is then certified to
-    // 4.5e-6 for all but |cos(view)| < ~0.05.
-    const d3 V0 = tod(v[0]);
-    const d3 E1 = subd(tod(v[1]), V0), E2 = subd(tod(v[2]), V0);
-    const d3 N64 = crossd(E1, E2);
-    const d3 A0 = subd(V0, tod(o));
-    const double h64 = dotd(N64, A0);
-    if (!(h64 > 0.0 || h64 < 0.0)) return false;   // origin in the plane / degenerate: no hits
-    const float s = h64 > 0.0 ? 1.f : -1.f;
-    if ((faces == 1 && s < 0.f) || (faces == 2 && s > 0.f)) return false;
-    const f3 N = {(float)N64.x, (float)N64.y, (float)N64.z};
-    const float habs = (float)fabs(h64);
-    // generous bound of the fp64 error of h64 (2^-48 relative to its L1 magnitudes)
-    // (explicit _rn intrinsics: thresholds must be bit-identical in every kernel that inlines this)
-    const float sE1 = __fadd_rn(__fadd_rn(fabsf((float)E1.x), fabsf((float)E1.y)), fabsf((float)E1.z));
-    const float sE2 = __fadd_rn(__fadd_rn(fabsf((float)E2.x), fabsf((float)E2.y)), fabsf((float)E2.z));
-    const float sN = __fadd_rn(__fadd_rn(fabsf(N.x), fabsf(N.y)), fabsf(N.z));
-    const float l1 = __fadd_rn(__fmul_rn(sE1, sE2), sN);
-    const float la = __fadd_rn(__fadd_rn(fabsf((float)A0.x), fabsf((float)A0.y)), fabsf((float)A0.z));
-    const float err64 = __fmul_rn(__fmul_rn(3.64e-15f, l1), la);
-    const bool sign_ok = habs > 2.f * err64;
-    S.n0 = scalef(n[0], s * sg[0]);
-    S.n1 = scalef(n[1], s * sg[1]);
-    S.n2 = scalef(n[2], s * sg[2]);
-    S.B0 = sign_ok ? B[0] : CUDART_INF_F;   // unsure side of the plane: every candidate -> fp64
-    S.B1 = sign_ok ? B[1] : CUDART_INF_F;
-    S.B2 = sign_ok ? B[2] : CUDART_INF_F;
-    S.N = scalef(N, s);
-    S.habs = habs;
-    const float rh = __fadd_rn(1.01f * kU, __fmul_rn(__fdividef(err64, habs), 1.02f));
-    const float nn = dotf(N, N);
-    const float Bn = __fmul_rn(3.11f * kU, nn > 0.f ? __fmul_rn(nn, rsqrtf(nn)) : 0.f);
-    (void)setup64;
-    // budget: kTRel = rel(d.N) + rh + 6u, where 6u covers the rounding of N and h and the approximate
-    // division in test_fast (rcp.approx then multiply: <= 2 ulp = 4u)
-    S.TN = (!sign_ok || !(rh < 2e-6f)) ? CUDART_INF_F : __fmul_rn(__fdividef(Bn, __fsub_rn(kTRel - 6.f * kU, rh)), 1.0002f);
-    return true;
-}
-
-__device__ __forceinline__ float rcp_approx(float x) {   // rcp.approx.ftz.f32 (MUFU.RCP, <= 1 ulp)
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-
-// make_setup written straight into a lane's slot column (fused kernel): same values, bit for bit,
-// computed plane first and one edge at a time so that fewer values are live at once (the fused
-// kernel runs at the 64-register cap).  slot[k * 32] = (n_k, B_k) for k < 3, slot[3 * 32] = (N, |h|),
-// slot[4 * 32] = (TN, id, tri, emitter).  Returns false like make_setup.
-__device__ __forceinline__ bool setup_to_slot(const f3 v[3], f3 o, int faces, float4 *slot, uint32_t id, int tri,
-                                              int em) {
+// A6 setup of one (triangle, emitter) pair, computed once into the five values every kernel stores
+// or reads (so K4, the split path and the fused kernel use bit-identical thresholds):
+//   out[k] = (sigma_k s n_k, B_k) for the three canonical edges (hit <=> all d.n_k >= 0; B_k certified
+//            bound of d.n_k), out[3] = (s N, |h|), out[4].x = TN (fp32 t certified iff d.N >= TN).
+// The plane (N, h) is computed in fp64 from the exact fp64 edges and rounded: t = h / d.N is then
+// certified to 4.5e-6 for all but |cos(view)| < ~0.05.  Computed plane
+// first and one edge at a time (fewer live values: the fused kernel runs at the register cap).
+// Returns false when the pair can never hit (Vol == 0: origin in the plane / degenerate triangle)
+// or is rejected by the face mode.  Explicit _rn intrinsics: no contraction freedom.
+template <typename Store>
+__device__ __forceinline__ bool setup_core(const f3 v[3], f3 o, int faces, Store &&store) {
     const d3 V0 = tod(v[0]);
     const d3 E1 = subd(tod(v[1]), V0), E2 = subd(tod(v[2]), V0);
     const d3 N64 = crossd(E1, E2);
@@ -811,33 +755,70 @@ __device__ __forceinline__ bool setup_to_slot(const f3 v[3], f3 o, int faces, fl
     if ((faces == 1 && s < 0.f) || (faces == 2 && s > 0.f)) return false;
     const f3 N = {(float)N64.x, (float)N64.y, (float)N64.z};
     const float habs = (float)fabs(h64);
+    // generous bound of the fp64 error of h64 (2^-48 relative to its L1 magnitudes)
     const float sE1 = __fadd_rn(__fadd_rn(fabsf((float)E1.x), fabsf((float)E1.y)), fabsf((float)E1.z));
     const float sE2 = __fadd_rn(__fadd_rn(fabsf((float)E2.x), fabsf((float)E2.y)), fabsf((float)E2.z));
     const float sN = __fadd_rn(__fadd_rn(fabsf(N.x), fabsf(N.y)), fabsf(N.z));
     const float l1 = __fadd_rn(__fmul_rn(sE1, sE2), sN);
     const float la = __fadd_rn(__fadd_rn(fabsf((float)A0.x), fabsf((float)A0.y)), fabsf((float)A0.z));
     const float err64 = __fmul_rn(__fmul_rn(3.64e-15f, l1), la);
-    const bool sign_ok = habs > 2.f * err64;
+    const bool sign_ok = habs > 2.f * err64;   // else every candidate goes to fp64 (B = inf)
     const float rh = __fadd_rn(1.01f * kU, __fmul_rn(__fdividef(err64, habs), 1.02f));
     const float nn = dotf(N, N);
     const float Bn = __fmul_rn(3.11f * kU, nn > 0.f ? __fmul_rn(nn, rsqrtf(nn)) : 0.f);
+    // budget: kTRel = rel(d.N) + rh + 6u, where 6u covers the rounding of N and h and the approximate
+    // division in test_fast (rcp.approx then multiply: <= 2 ulp = 4u)
     const float TN = (!sign_ok || !(rh < 2e-6f)) ? CUDART_INF_F
                                                  : __fmul_rn(__fdividef(Bn, __fsub_rn(kTRel - 6.f * kU, rh)), 1.0002f);
     const f3 SN = scalef(N, s);
-    slot[3 * 32] = make_float4(SN.x, SN.y, SN.z, habs);
-    slot[4 * 32] = make_float4(TN, __uint_as_float(id), __int_as_float(tri), __int_as_float(em));
+    store(3, make_float4(SN.x, SN.y, SN.z, habs));
+    store(4, make_float4(TN, 0.f, 0.f, 0.f));
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         f3 Pp = v[k], Qq = v[(k + 1) % 3];
-        const bool sw = lexless(Qq, Pp);
+        const bool sw = lexless(Qq, Pp);   // canonical direction: adjacent triangles share bits
         if (sw) { f3 t = Pp; Pp = Qq; Qq = t; }
         const f3 aP = subf(Pp, o), e = subf(Qq, Pp);
         const f3 n = scalef(crossf(aP, e), s * (sw ? -1.f : 1.f));
         const float pe = __fmul_rn(dotf(aP, aP), dotf(e, e));
-        const float B = __fmul_rn(16.1f * kU, pe > 0.f ? __fmul_rn(pe, rsqrtf(pe)) : 0.f);
-        slot[k * 32] = make_float4(n.x, n.y, n.z, sign_ok ? B : CUDART_INF_F);
+        const float B = __fmul_rn(16.1f * kU, pe > 0.f ? __fmul_rn(pe, rsqrtf(pe)) : 0.f);   // 16u|a||e|
+        store(k, make_float4(n.x, n.y, n.z, sign_ok ? B : CUDART_INF_F));
     }
     return true;
+}
+
+// The setup as a Setup struct (K4, split path, serial fallback).
+__device__ __forceinline__ bool make_setup(const f3 v[3], f3 o, int faces, Setup &S, unsigned &setup64) {
+    (void)setup64;
+    return setup_core(v, o, faces, [&](int k, float4 q) {
+        if (k < 3) {
+            const f3 n = {q.x, q.y, q.z};
+            if (k == 0) { S.n0 = n; S.B0 = q.w; }
+            if (k == 1) { S.n1 = n; S.B1 = q.w; }
+            if (k == 2) { S.n2 = n; S.B2 = q.w; }
+        } else if (k == 3) {
+            S.N = {q.x, q.y, q.z};
+            S.habs = q.w;
+        } else {
+            S.TN = q.x;
+        }
+    });
+}
+
+// The setup written straight into a lane's slot column (fused kernel): slot[k * 32] for k < 4,
+// slot[4 * 32] = (TN, id, tri, emitter).
+__device__ __forceinline__ bool setup_to_slot(const f3 v[3], f3 o, int faces, float4 *slot, uint32_t id, int tri,
+                                              int em) {
+    return setup_core(v, o, faces, [&](int k, float4 q) {
+        if (k == 4) q = make_float4(q.x, __uint_as_float(id), __int_as_float(tri), __int_as_float(em));
+        slot[k * 32] = q;
+    });
+}
+
+__device__ __forceinline__ float rcp_approx(float x) {   // rcp.approx.ftz.f32 (MUFU.RCP, <= 1 ulp)
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
 }
 
 // 0 = certified miss, 1 = certified hit (t set), 2 = uncertain -> fp64
