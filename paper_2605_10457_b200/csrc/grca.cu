@@ -39,6 +39,9 @@ constexpr int K4_THREADS = 256;
 #ifndef KF_MINB
 #define KF_MINB 2
 #endif
+#ifndef K3_MINB
+#define K3_MINB 2   // 128 registers (without a bound the compiler took 145: K3 0.028 -> 0.041 ms)
+#endif
 #ifndef K4_MINB
 #define K4_MINB 3   // 80 registers: 3 blocks of 256 per SM (measured best; 1 block = 95+ regs, 25 % occupancy)
 #endif
@@ -880,7 +883,7 @@ __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev
     atomicAdd(P.stats + ST_HITS, (unsigned long long)hits);
 }
 
-__global__ void __launch_bounds__(256) k_bin(const __grid_constant__ KParams P) {
+__global__ void __launch_bounds__(256, K3_MINB) k_bin(const __grid_constant__ KParams P) {
     // one warp per large rectangle; lanes = channel rows.  A7 refines each non-pole row of a
     // partial-arc rectangle to its exact (padded) ray range; rows become chunks of <= kColMax rays.
     __shared__ unsigned long long acc[ST_COUNT];
