@@ -1435,6 +1435,7 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
         D.pole_lo = plo;
         D.pole_hi = phi;
         D.noisy = E.ray_azimuth_rad ? 1 : 0;
+        D.level = (D.A[2] == 0.f && D.A[5] == 0.f && D.A[6] == 0.f && D.A[7] == 0.f && D.A[8] == 1.f) ? 1 : 0;
         if (E.ray_azimuth_rad) {   // noise model: |theta*_i - theta_i| < dtheta, strictly ascending
             const double th0 = -(double)(E.rays_per_channel / 2) * dth;
             for (int i = 0; i < E.rays_per_channel; ++i) {

@@ -39,6 +39,7 @@ struct EmDev {
     float dmax_lo, dmax_hi;   // certified accept / reject bounds around D_max (+inf if none)
     double dmax;              // fp64 D_max for the fallback (+inf if none)
     int gamma, chi, hfov, ray_base, sin_base, pole_lo, pole_hi, noisy;   // noisy: perturbed theta*_i
+    int level;                // A = [[a0 a1 0] [a3 a4 0] [0 0 1]] exactly (level frame): x_u = a_z
 };
 
 // Phase-A (K2) view of an emitter: just what the elevation pre-test needs.
@@ -269,12 +270,22 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
     // sensor coordinates x = A a  (x = (x_f, x_r, x_u))
     f3 x[3];
     float r2[3], inv[3], s[3];
+    if (E.level) {   // level frame: the zero / unit entries of A dropped (same values up to the sign of 0)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        x[k].x = E.A[0] * a[k].x + E.A[1] * a[k].y + E.A[2] * a[k].z;
-        x[k].y = E.A[3] * a[k].x + E.A[4] * a[k].y + E.A[5] * a[k].z;
-        x[k].z = E.A[6] * a[k].x + E.A[7] * a[k].y + E.A[8] * a[k].z;
-        r2[k] = x[k].x * x[k].x + x[k].y * x[k].y + x[k].z * x[k].z;
+        for (int k = 0; k < 3; ++k) {
+            x[k].x = E.A[0] * a[k].x + E.A[1] * a[k].y;
+            x[k].y = E.A[3] * a[k].x + E.A[4] * a[k].y;
+            x[k].z = a[k].z;
+            r2[k] = x[k].x * x[k].x + x[k].y * x[k].y + x[k].z * x[k].z;
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            x[k].x = E.A[0] * a[k].x + E.A[1] * a[k].y + E.A[2] * a[k].z;
+            x[k].y = E.A[3] * a[k].x + E.A[4] * a[k].y + E.A[5] * a[k].z;
+            x[k].z = E.A[6] * a[k].x + E.A[7] * a[k].y + E.A[8] * a[k].z;
+            r2[k] = x[k].x * x[k].x + x[k].y * x[k].y + x[k].z * x[k].z;
+        }
     }
     if (!(r2[0] > 0.f && r2[1] > 0.f && r2[2] > 0.f)) return CULL_DEGENERATE;   // o is a vertex: Vol = 0
     float xn[3];   // |x_k|
