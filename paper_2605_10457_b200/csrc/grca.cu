@@ -32,9 +32,9 @@ constexpr int K2_THREADS = 256;
 #define K2_TILE 1024   // triangles per K2 block tile (K2_TILE / K2_THREADS = 4 per thread; measured: 256 -> 0.578, 512 -> 0.543, 1024 -> 0.525 ms)
 #endif
 constexpr int K4_THREADS = 256;
-// fused refine+small: 512 threads x 2 blocks (64 registers) measured best on B200 (occupancy vs spills)
+// fused refine+small: 576 threads x 2 blocks (56 registers) measured best on B200 (occupancy vs spills)
 #ifndef KF_THREADS
-#define KF_THREADS 512
+#define KF_THREADS 576   // 18 warps x 2 blocks at 56 registers (measured: 512 -> 0.561 ms, 576 -> 0.558, 640 -> 0.585)
 #endif
 #ifndef KF_MINB
 #define KF_MINB 2
