@@ -342,6 +342,41 @@ def test_c4_full_size_sampled():
     assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
 
 
+@pytest.mark.slow
+def test_c4_full_size_large_rectangle_frame():
+    """C4 frame 2 (the bench cycles frames 0-3; frames with huge scaled cars send many large
+    rectangles through K3/K4), full size, in the indexed float3 layout bench.py times: sampled
+    parity against the oracle, plus soup == indexed bit for bit."""
+    w = sg.workload("C4", frame=2)
+    dist, tri, st, g = run(w["emitters"], w["tris"])
+    assert st["large_pairs"] > 1000 and st["chunks"] > 10000
+    di, ti = run_indexed_frame(w, g)
+    assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
+    rep, _ = check(w["emitters"], w["tris"], di, ti, rays=_sampled(w["emitters"], 24, 19))
+    assert rep["oracle_hits"] > 20
+
+
+def test_c2_tilted_frames():
+    """C2 at full size with every emitter's frame rolled 25 deg and pitched 10 deg (not level: the
+    general K2 pre-test and sensor transform), indexed float3 layout; sampled parity."""
+    w = sg.workload("C2", frame=1)
+    ca, sa, cb, sb = math.cos(0.436), math.sin(0.436), math.cos(0.175), math.sin(0.175)
+    roll = np.array([[1, 0, 0], [0, ca, -sa], [0, sa, ca]])
+    pitch = np.array([[cb, 0, sb], [0, 1, 0], [-sb, 0, cb]])
+    R = pitch @ roll
+    ems = []
+    for e in w["emitters"]:
+        f, r, u = (R @ np.asarray(x, np.float64) for x in (e.forward, e.right, e.up))
+        ems.append(sg.Emitter(origin=e.origin, forward=f, right=r, up=u, elev=e.elev,
+                              rays_per_channel=e.rays_per_channel, hfov_deg=e.hfov_deg, max_range=e.max_range))
+    w = dict(w, emitters=ems)
+    dist, tri, st, g = run(ems, w["tris"])
+    di, ti = run_indexed_frame(w, g)
+    assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
+    rep, _ = check(ems, w["tris"], di, ti, rays=_sampled(ems, 1024, 23))
+    assert rep["oracle_hits"] > 100
+
+
 def run_indexed_frame(w, g):
     v, idx = sg.indexed_frame(w)   # as bench.py passes it: packed float3 vertices + indices
     g.update_triangles(torch.as_tensor(v, device="cuda"), indices=torch.as_tensor(idx, device="cuda"))
