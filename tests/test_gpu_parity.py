@@ -356,6 +356,27 @@ def test_c4_full_size_large_rectangle_frame():
     assert rep["oracle_hits"] > 20
 
 
+def test_c2_hybrid_indexed_dynamic():
+    """The bench's hybrid line: static triangles (float4 soup) cached, the cars' posed vertices
+    (indexed float3) cast each frame -- bit-identical to the full indexed cast."""
+    w = sg.workload("C2", frame=2)
+    v, idx = sg.indexed_frame(w)
+    ns3 = 3 * w["n_static"]
+    g = Grca(device=0, max_triangles=len(w["tris"]), max_rays=sg.n_rays_total(w["emitters"]))
+    g.set_emitters(w["emitters"])
+    g.update_triangles(torch.as_tensor(v, device="cuda"), indices=torch.as_tensor(idx, device="cuda"))
+    d_f, t_f = g.cast()
+    gh = Grca(device=0, max_triangles=len(w["tris"]), max_rays=sg.n_rays_total(w["emitters"]))
+    gh.set_emitters(w["emitters"])
+    gh.set_static_triangles(tris_to_float4(v[:ns3]), tri_id_base=0)
+    dyn_idx = torch.as_tensor(idx[ns3:] - ns3, device="cuda")
+    gh.update_triangles(torch.as_tensor(v[ns3:], device="cuda"), indices=dyn_idx, tri_id_base=w["n_static"])
+    d_h, t_h = gh.cast()
+    torch.cuda.synchronize()
+    assert np.array_equal(t_h.cpu().numpy(), t_f.cpu().numpy())
+    assert np.array_equal(d_h.cpu().numpy().view(np.uint32), d_f.cpu().numpy().view(np.uint32))
+
+
 def test_c2_tilted_frames():
     """C2 at full size with every emitter's frame rolled 25 deg and pitched 10 deg (not level: the
     general K2 pre-test and sensor transform), indexed float3 layout; sampled parity."""
