@@ -109,7 +109,11 @@ class Scene:
         n_static, n_dyn = w["n_static"], w["n_dynamic"]
         self.n_tri_global = n_static + n_dyn
         own = np.zeros(self.n_tri_global, dtype=bool)
-        if shard == "triangles":
+        if shard.startswith("mixed"):   # emitter groups x triangle shards (D.mixed_partition)
+            g, t, T = D.mixed_partition(rank, world, int(shard.split(":")[1]))
+            own[D.shard_triangles(self.n_tri_global, t, T)] = True
+            self.emitters = [self.emitters[n] for n in D.shard_emitters(len(self.emitters), g, world // T)]
+        elif shard == "triangles":
             own[D.shard_triangles(self.n_tri_global, rank, world)] = True
         else:   # sensor sharding: every rank holds all triangles, casts its own emitters
             own[:] = True
@@ -295,12 +299,17 @@ def main():
     ap.add_argument("--split-refine", action="store_true", help="K2b and K4s as two kernels (A/B)")
     ap.add_argument("--l2-persist", action="store_true", help="A/B: persisting L2 window (opt-in)")
     ap.add_argument("--no-packed", action="store_true", help="A/B: K2 without packed fp32x2 math")
+    ap.add_argument("--emulate-world", type=int, default=0, help="do rank --emulate-rank's share of a W-rank run "
+                    "on this one GPU (sensor shards: ranks never wait on one another); see tools/emulate_ranks.py")
+    ap.add_argument("--emulate-rank", type=int, default=0)
     ap.add_argument("--merge", choices=["allreduce", "nvls"], default="allreduce",
                     help="triangle-shard merge: NCCL all-reduce(MIN) of the packed keys, or the fused NVLS "
                          "multimem.red.min in the intersection kernels (NEXT-f3; needs NVLS multicast)")
     ap.add_argument("--soup", action="store_true", help="triangle-soup scene (float4 triplets) instead of the indexed "
                     "car meshes (same triangles; the e2e upload is then every dynamic triangle's vertices)")
-    ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters"])
+    ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters", "mixed"])
+    ap.add_argument("--emitter-groups", type=int, default=2, help="--shard mixed: emitter groups (each split "
+                    "into world / groups triangle shards merged within the group)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the N>1 logic with several ranks on one GPU")
     args = ap.parse_args()
@@ -366,11 +375,22 @@ def main():
             dist.init_process_group("gloo")
     device = torch.device(f"cuda:{dev_index}")
     torch.cuda.set_device(device)
+    if args.merge == "nvls" and world > max(1, torch.cuda.device_count()):
+        # the NVLS barrier spins on flags the other ranks write: never several ranks on one GPU
+        raise SystemExit("--merge nvls needs one GPU per rank")
+    # --emulate-world W --emulate-rank R: this process does exactly rank R's share of a W-rank run
+    # (its shard of the scene, no process group).  Valid for sensor shards, whose ranks never wait on
+    # one another; tools/emulate_ranks.py runs every rank and takes the slowest (projected frame).
+    s_rank, s_world = (args.emulate_rank, args.emulate_world) if args.emulate_world > 1 else (rank, world)
+    if args.emulate_world > 1:
+        args.no_e2e = args.no_hybrid = args.no_cpu_baseline = True
     n_em_total = len(sg.workload(args.config)["emitters"]) if args.config == "C1" else sg.WORKLOADS[args.config][0]
-    shard = args.shard if args.shard != "auto" else (D.choose_mode(n_em_total, world) if world > 1 else "triangles")
+    shard = args.shard if args.shard != "auto" else (D.choose_mode(n_em_total, s_world) if s_world > 1 else "triangles")
+    if shard == "mixed":
+        shard = f"mixed:{args.emitter_groups}"
 
     car_scale = tuple(float(x) for x in args.car_scale.split(",")) if args.car_scale else None
-    scene = Scene(args.config, rank, world, device, args.deformation, shard=shard,
+    scene = Scene(args.config, s_rank, s_world, device, args.deformation, shard=shard,
                   max_range=(None if args.max_range == 0 else args.max_range), subdiv=args.subdiv, car_scale=car_scale,
                   mesh="soup" if args.soup else "indexed")
     ems = scene.emitters
@@ -386,7 +406,13 @@ def main():
     dist_out = torch.empty(n_rays, dtype=torch.float32, device=device)
     tri_out = torch.empty(n_rays, dtype=torch.int32, device=device)
 
-    merge = world > 1 and shard == "triangles"
+    merge = world > 1 and (shard == "triangles" or shard.startswith("mixed"))
+    merge_group = None
+    if world > 1 and shard.startswith("mixed"):   # merge only within this rank's emitter group
+        n_groups = int(shard.split(":")[1])
+        _, _, T = D.mixed_partition(rank, world, n_groups)
+        subs = [dist.new_group(ranks=[gg * T + t for t in range(T)]) for gg in range(n_groups)]
+        merge_group = subs[rank // T]
     nvls = None
     if args.merge == "nvls" and (merge or world == 1):
         # NEXT-f3: hits reduced in-switch by the intersection kernels (multimem.red.min); no all-reduce
@@ -399,7 +425,7 @@ def main():
     def cast_once(dout=dist_out, tout=tri_out):
         if merge:   # triangle shards: exact merge = all-reduce(MIN) of the packed (t, id) keys
             g.cast_packed()
-            D.merge_packed(g.hits_packed())
+            D.merge_packed(g.hits_packed(), group=merge_group)
             g.unpack(dout, tout)
         else:       # single GPU, or sensor shards (disjoint ray slices, no reduction)
             g.cast(dout, tout)
@@ -464,7 +490,7 @@ def main():
         n_dyn = scene.frames[0].shape[0] - ns3          # dynamic vertices per frame
         # split only when every rank needs the same dynamic data (indexed scene: all car vertices;
         # sensor shards: all triangles); a triangle-sharded soup holds per-rank data
-        split = world > 1 and (scene.indexed or shard != "triangles")
+        split = world > 1 and (scene.indexed or shard == "emitters")
         nsplit = world if split else 1
         chunk = -(-n_dyn // nsplit)                     # per-rank upload slice (padded)
         lo_v = (rank if split else 0) * chunk
@@ -482,9 +508,12 @@ def main():
         outs = [(torch.empty(n_rays, dtype=torch.float32, device=device),
                  torch.empty(n_rays, dtype=torch.int32, device=device)) for _ in range(2)]
         r_lo, r_n = 0, n_rays                           # rays this rank reads back
-        if merge:
-            rch = -(-n_rays // world)
-            r_lo, r_n = rank * rch, max(0, min(rch, n_rays - rank * rch))
+        if merge:   # the merged keys are on every rank of the merge group: each reads 1/T of them
+            m_rank, m_size = (rank % D.mixed_partition(rank, world, int(shard.split(":")[1]))[2],
+                              D.mixed_partition(rank, world, int(shard.split(":")[1]))[2]) \
+                if shard.startswith("mixed") else (rank, world)
+            rch = -(-n_rays // m_size)
+            r_lo, r_n = m_rank * rch, max(0, min(rch, n_rays - m_rank * rch))
         host_out = [(torch.empty(r_n, dtype=torch.float32).pin_memory(),
                      torch.empty(r_n, dtype=torch.int32).pin_memory()) for _ in range(2)]
         cs, ds = torch.cuda.Stream(device), torch.cuda.Stream(device)
@@ -616,7 +645,10 @@ def main():
                        "sharding": ("none" if world == 1 else
                                     f"triangles block-interleaved ({D.BLOCK}) + "
                                     f"{'fused NVLS multimem.red.min' if nvls else 'all-reduce(MIN)'} x {world}"
-                                    if shard == "triangles" else f"emitters (n mod P) x {world}, no reduction"),
+                                    if shard == "triangles" else
+                                    f"{shard.split(':')[1]} emitter groups x {world // int(shard.split(':')[1])} "
+                                    f"triangle shards, all-reduce(MIN) within a group"
+                                    if shard.startswith("mixed") else f"emitters (n mod P) x {world}, no reduction"),
                        "l2": f"inputs > L2: {N_FRAMES} resident frame buffers of "
                              f"{scene.frames[0].numel() * 4 / 1e9:.2f} GB (+ {0 if scene.indices is None else scene.indices.numel() * 4 / 1e9:.2f} GB "
                              "shared indices) cycled"},
@@ -632,6 +664,9 @@ def main():
                 "chunks", "fp64_fallbacks", "hits_recorded", "overflow")},
             "roofline": roofline, "gpu_launches": launches_per_cast * args.steps, "clocks": clk,
             "e2e": e2e, "cpu_baseline": cpu, "hybrid_static_cache": hybrid,
+            "emulated": ({"rank": s_rank, "world": s_world, "shard": shard, "rank_rays": n_rays,
+                          "note": "this rank's share of a W-rank run on one GPU (no merge timed)"}
+                         if args.emulate_world > 1 else None),
             "context": "paper (PAPER.md:1758-1762): GRCA_GPU 10.7 ms/frame on RTX 5090 for PP30 Omega=8 "
                        "(3.9e8 rays/s), 1.98x OptiX 9.1; other hardware, not a target",
         }

@@ -43,6 +43,15 @@ def choose_mode(n_emitters: int, world: int) -> str:
     return "triangles"
 
 
+def mixed_partition(rank: int, world: int, groups: int):
+    """2-D partition for `world` ranks: `groups` emitter groups x (world / groups) triangle shards.
+    Rank r -> (emitter group g = r // T, triangle shard t = r mod T); ranks of one emitter group
+    merge their packed keys (all-reduce MIN over a T-rank subgroup), different groups never talk."""
+    assert groups >= 1 and world % groups == 0, (world, groups)
+    T = world // groups
+    return rank // T, rank % T, T
+
+
 def merge_packed(hits, group=None):
     """In-place exact merge of per-shard packed hit buffers: all-reduce(MIN) over ranks.
 

@@ -74,6 +74,46 @@ def test_two_rank_triangle_and_sensor_sharding():
     assert np.array_equal(t_full, ref["id"]) and np.array_equal(d_full.view(np.uint32), ref["t"].view(np.uint32))
 
 
+def _worker_mixed(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ems, tris = sg.random_scene(78, n_tris=6000, n_emitters=2, gamma=8, chi=64, extent=8.0)
+        G = 2
+        g, t, T = D.mixed_partition(rank, world, G)
+        subs = [dist.new_group(ranks=[gg * T + tt for tt in range(T)]) for gg in range(G)]
+        mine_em = D.shard_emitters(len(ems), g, G)
+        own = D.shard_triangles(len(tris), t, T, block=512)
+        res = oracle.cast([ems[n] for n in mine_em], tris[own], ids=own.astype(np.int32), threads=2)
+        hits = torch.as_tensor(_packed(res))
+        D.merge_packed(hits, group=subs[g])   # merge only within this emitter group
+        q.put((rank, mine_em, hits.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_four_rank_mixed_partition():
+    """2 emitter groups x 2 triangle shards (D.mixed_partition): each group's in-group min-merge
+    equals the unsharded oracle for that group's emitters."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_mixed, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(4)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ems, tris = sg.random_scene(78, n_tris=6000, n_emitters=2, gamma=8, chi=64, extent=8.0)
+    for rank, mine_em, hits in got:
+        ref = _packed(oracle.cast([ems[n] for n in mine_em], tris, want_t64=True))
+        same = hits == ref
+        tie = (hits >> 32) == (ref >> 32)   # fp32-equal distances: fp64 order vs id order
+        assert np.all(same | tie) and same.mean() > 0.999, rank
+
+
 def test_partition_helpers():
     n, world = 100_000, 4
     parts = [D.shard_triangles(n, r, world) for r in range(world)]
@@ -84,3 +124,4 @@ def test_partition_helpers():
     assert D.shard_emitters(8, 1, 4) == [1, 5]
     assert D.choose_mode(8, 8) == "emitters" and D.choose_mode(2, 8) == "triangles" and D.choose_mode(8, 1) == "triangles"
     assert D.MISS_KEY == 0x7F800000FFFFFFFF and D.MISS_KEY < 2**63   # positive as int64: signed min works
+    assert [D.mixed_partition(r, 8, 2) for r in (0, 3, 4, 7)] == [(0, 0, 4), (0, 3, 4), (1, 0, 4), (1, 3, 4)]
