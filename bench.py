@@ -91,16 +91,18 @@ class Scene:
     """Resident C-config frames on the GPU (harness: input generation, not the hot path).
 
     mesh="indexed" (default when the cars are plain meshes, i.e. ND motion and no subdivision):
-    one vertex buffer per frame = [static triangles' own vertices (3 per triangle)] + [posed car
-    vertices (shared grid vertices)], and one index buffer shared by all frames (static: 0..3n-1;
-    cars: their faces).  Same triangles, same order and ids as the soup; a frame's per-step input
-    is then only the car vertices.  mesh="soup": float4 triplets per triangle."""
+    grca_update_scene's two parts -- the static triangles as one resident float4-triplet soup
+    shared by all frames, then the cars as one packed-float3 vertex buffer per frame (shared grid
+    vertices) with one index buffer shared by all frames (their faces).  Same triangles, same order
+    and ids as the soup; a frame's per-step input is then only the car vertices.  mesh="soup":
+    float4 triplets per triangle, one buffer per frame (static part copied into each)."""
 
     def __init__(self, config: str, rank: int, world: int, device, deformation: str = "ND", shard: str = "triangles",
                  max_range=-1.0, subdiv: int = 0, car_scale=None, mesh: str = "indexed"):
         import torch
 
         from paper_2605_10457_b200 import dist as D
+        from paper_2605_10457_b200 import tris_to_float4
 
         w = sg.workload(config, frame=0, deformation=deformation, max_range=max_range, subdiv=subdiv)
         self.w = w
@@ -134,7 +136,7 @@ class Scene:
         cm = w.get("car_mesh")
         self.indexed = mesh == "indexed" and cm is not None and deformation == "ND" and n_dyn > 0
         self.mesh = "indexed" if self.indexed else "soup"
-        self.indices = self.idx_dyn = None
+        self.idx_dyn = self.static_soup = None
         if self.indexed:
             car_v, car_f = cm
             nv_car, nf_car = len(car_v), len(car_f)
@@ -142,25 +144,33 @@ class Scene:
             inst, f = self.own_dyn // nf_car, self.own_dyn % nf_car
             rel = (inst.astype(np.int64) * nv_car)[:, None] + car_f[f].astype(np.int64)
             self.idx_dyn = torch.as_tensor(rel.astype(np.int32).reshape(-1), device=device)
-            self.indices = torch.cat([torch.arange(self.ns3, dtype=torch.int32, device=device),
-                                      self.idx_dyn + self.ns3]).contiguous()
             self.n_dyn_vert = self.n_cars * nv_car
-            # packed float3 vertices (grca_update_triangles_f3).  Algorithmic K2 read per cast:
-            # static 36 B vertices + 12 B indices; cars 12 B indices per triangle + 12 B per shared vertex
+            self.static_soup = tris_to_float4(static, device=device)   # part A of grca_update_scene (resident)
+            # Algorithmic K2 read per cast: static 48 B (3 float4); cars 12 B indices per triangle +
+            # 12 B per shared float3 vertex
             self.tri_bytes = self.n_static_local * 48 + len(self.own_dyn) * 12 + self.n_dyn_vert * 12
         else:
             self.car = torch.as_tensor(w["car_local"], dtype=torch.float32, device=device)   # (m, 3, 3)
             self.own_dyn_t = torch.as_tensor(self.own_dyn, device=device)
             self.tri_bytes = self.n_tri * 48
+        # frame buffers: soup = [static | dynamic] float4 rows; indexed = the car vertices only
+        self.fs = 0 if self.indexed else self.ns3   # static rows at the head of a frame buffer
         self.frames = []
         for fr in range(N_FRAMES):
             nd = self.n_dyn_vert if self.indexed else 3 * (self.n_tri - self.n_static_local)
-            buf = torch.zeros((self.ns3 + nd, 3 if self.indexed else 4), dtype=torch.float32, device=device)
-            buf[: self.ns3, :3] = static
-            buf[self.ns3:, :3] = self.dynamic(fr)
+            buf = torch.zeros((self.fs + nd, 3 if self.indexed else 4), dtype=torch.float32, device=device)
+            buf[: self.fs, :3] = static[: self.fs]
+            buf[self.fs:, :3] = self.dynamic(fr)
             self.frames.append(buf)
         del static
         torch.cuda.synchronize()
+
+    def bind(self, g, buf, n_triangles=None):
+        """Point handle g at one frame buffer (public API: grca_update_scene / grca_update_triangles)."""
+        if self.indexed:
+            g.update_scene(soup=self.static_soup, mesh_xyz=buf, mesh_indices=self.idx_dyn, tri_ids=self.ids)
+        else:
+            g.update_triangles(buf, tri_ids=self.ids, n_triangles=n_triangles)
 
     def dynamic(self, frame: int):
         """Motion f.i: per-frame random pose/scale of every car instance; world
@@ -431,7 +441,7 @@ def main():
             g.cast(dout, tout)
 
     def step(k):
-        g.update_triangles(scene.frames[k % N_FRAMES], indices=scene.indices, tri_ids=scene.ids)
+        scene.bind(g, scene.frames[k % N_FRAMES])
         cast_once()
 
     stream = torch.cuda.current_stream(device)
@@ -463,7 +473,7 @@ def main():
     gp.set_emitters(ems)
     n_last = min(max(args.steps, 8), 64)
     for k in range(n_last + 2):
-        gp.update_triangles(scene.frames[k % N_FRAMES], indices=scene.indices, tri_ids=scene.ids)
+        scene.bind(gp, scene.frames[k % N_FRAMES])
         gp.cast(dist_out, tri_out)
     torch.cuda.synchronize()
     kt = gp.kernel_times(n_last)
@@ -485,7 +495,7 @@ def main():
         # N > 1: each rank uploads 1/N of the dynamic vertices over its own PCIe link and an
         # all-gather over NVLink assembles the rest (inside the timed region); each rank reads back
         # only its own results (sensor shards: its emitters' rays; triangle shards: 1/N of the rays)
-        ns3 = scene.ns3
+        ns3 = scene.fs                                  # static rows carried in a frame buffer
         comps = scene.frames[0].shape[1]
         n_dyn = scene.frames[0].shape[0] - ns3          # dynamic vertices per frame
         # split only when every rank needs the same dynamic data (indexed scene: all car vertices;
@@ -542,7 +552,7 @@ def main():
                 stream.wait_event(ev_h2d[b])
                 if k >= 2:
                     stream.wait_event(ev_d2h[b])   # host copy of step k-2 done with outs[b]
-                g.update_triangles(dev_bufs[b], indices=scene.indices, tri_ids=scene.ids, n_triangles=scene.n_tri)
+                scene.bind(g, dev_bufs[b], n_triangles=scene.n_tri)
                 cast_once(*outs[b])
                 ev_cast[b].record(stream)
                 if k + 1 < n:
@@ -589,8 +599,8 @@ def main():
     if world == 1 and not args.no_hybrid and scene.n_static_local > 0:
         gh = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays)
         gh.set_emitters(ems)
-        ns3 = 3 * scene.n_static_local
-        st4 = tris_to_float4(scene.frames[0][:ns3])   # set_static_triangles takes float4 vertices
+        ns3 = scene.fs
+        st4 = scene.static_soup if scene.indexed else scene.frames[0][:ns3]   # float4 triplets
         gh.set_static_triangles(st4, tri_ids=scene.ids[: scene.n_static_local])
         dyn_ids = scene.ids[scene.n_static_local:]
 
@@ -649,9 +659,12 @@ def main():
                                     f"{shard.split(':')[1]} emitter groups x {world // int(shard.split(':')[1])} "
                                     f"triangle shards, all-reduce(MIN) within a group"
                                     if shard.startswith("mixed") else f"emitters (n mod P) x {world}, no reduction"),
-                       "l2": f"inputs > L2: {N_FRAMES} resident frame buffers of "
-                             f"{scene.frames[0].numel() * 4 / 1e9:.2f} GB (+ {0 if scene.indices is None else scene.indices.numel() * 4 / 1e9:.2f} GB "
-                             "shared indices) cycled"},
+                       "l2": (f"inputs > L2: every cast streams the resident {scene.static_soup.numel() * 4 / 1e9:.2f} GB "
+                              f"static float4 soup + {scene.idx_dyn.numel() * 4 / 1e9:.3f} GB car indices + one of "
+                              f"{N_FRAMES} cycled {scene.frames[0].numel() * 4 / 1e9:.3f} GB car-vertex frames"
+                              if scene.indexed else
+                              f"inputs > L2: {N_FRAMES} resident frame buffers of "
+                              f"{scene.frames[0].numel() * 4 / 1e9:.2f} GB cycled")},
             "frame_ms": ms_step, "rtic_culled_frac": culled,
             "rtic_tested_per_frame": stats["rtic_tested"], "rtic_brute_per_frame": stats["rtic_brute"],
             "rtic_per_s": stats["rtic_tested"] / (ms_step / 1e3),

@@ -160,6 +160,19 @@ grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_v
  * layout of indices / ids and errors (alignment: 4 bytes). */
 grca_status grca_update_triangles_f3(grca_t h, const float *d_xyz, int64_t n_vertices, const uint32_t *d_indices,
                                      int64_t n_triangles, const int32_t *d_tri_ids, int32_t tri_id_base);
+/* Two-part triangle set in one call (same role as grca_update_triangles; PAPER.md:146-157 casts every
+ * triangle of the frame, the split is only a storage layout): triangles [0, n_soup_triangles) are
+ * non-indexed float4 triplets d_soup (vertex 3k..3k+2 = triangle k; 16-byte aligned; w ignored) --
+ * scenery that needs no index indirection -- and triangles [n_soup_triangles, n_soup + n_mesh) are
+ * the indexed packed-float3 mesh d_mesh_xyz (n_mesh_vertices x 12 bytes, 4-byte aligned) with
+ * d_mesh_indices (uint32[3 * n_mesh_triangles], local to d_mesh_xyz).  Either part may be empty
+ * (its pointers are then ignored).  Triangle k of the concatenation has id d_tri_ids[k] or
+ * tri_id_base + k.  Ownership as grca_update_triangles.  Errors: GRCA_E_INVALID (negative counts,
+ * misaligned or missing buffers of a non-empty part), GRCA_E_CAPACITY (n_soup + n_mesh >
+ * max_triangles). */
+grca_status grca_update_scene(grca_t h, const float *d_soup, int64_t n_soup_triangles, const float *d_mesh_xyz,
+                              int64_t n_mesh_vertices, const uint32_t *d_mesh_indices, int64_t n_mesh_triangles,
+                              const int32_t *d_tri_ids, int32_t tri_id_base);
 
 /* Hybrid static/dynamic mode (NEXT-f2; "GRCA on dynamic, static BVH on static,
  * per-ray min merge", here without any BVH): borrow a static triangle set (same conventions as

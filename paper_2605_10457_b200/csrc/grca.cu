@@ -1613,6 +1613,8 @@ grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_v
     if (st != GRCA_OK) return st;
     h->tri.v = reinterpret_cast<const float4 *>(d_vertices);
     h->tri.v3 = nullptr;
+    h->tri.va = nullptr;
+    h->tri.n_a = 0;
     h->tri.idx = d_indices;
     h->tri.ids = d_tri_ids;
     h->tri.id_base = tri_id_base;
@@ -1628,10 +1630,38 @@ grca_status grca_update_triangles_f3(grca_t h, const float *d_xyz, int64_t n_ver
     if (st != GRCA_OK) return st;
     h->tri.v = nullptr;
     h->tri.v3 = d_xyz;
+    h->tri.va = nullptr;
+    h->tri.n_a = 0;
     h->tri.idx = d_indices;
     h->tri.ids = d_tri_ids;
     h->tri.id_base = tri_id_base;
     h->n_tri = n_triangles;
+    h->have_tri = true;
+    return GRCA_OK;
+}
+
+grca_status grca_update_scene(grca_t h, const float *d_soup, int64_t n_soup_triangles, const float *d_mesh_xyz,
+                              int64_t n_mesh_vertices, const uint32_t *d_mesh_indices, int64_t n_mesh_triangles,
+                              const int32_t *d_tri_ids, int32_t tri_id_base) {
+    if (!h) return GRCA_E_INVALID;
+    if (n_soup_triangles < 0 || n_mesh_triangles < 0) return fail(h, GRCA_E_INVALID, "negative triangle count");
+    if (n_soup_triangles > 0 && (!d_soup || ((uintptr_t)d_soup & 15)))
+        return fail(h, GRCA_E_INVALID, "soup part: 16-byte aligned float4 vertices required");
+    if (n_mesh_triangles > 0 && (!d_mesh_indices || n_mesh_vertices < 1))
+        return fail(h, GRCA_E_INVALID, "mesh part: indices and vertices required");
+    grca_status st = check_tri_args(h, n_mesh_triangles > 0 ? d_mesh_xyz : d_soup,
+                                    n_mesh_triangles > 0 ? n_mesh_vertices : 3 * (n_soup_triangles + n_mesh_triangles),
+                                    n_mesh_triangles > 0 ? d_mesh_indices : nullptr, n_soup_triangles + n_mesh_triangles,
+                                    d_tri_ids, tri_id_base, n_mesh_triangles > 0);
+    if (st != GRCA_OK) return st;
+    h->tri.va = reinterpret_cast<const float4 *>(d_soup);
+    h->tri.n_a = n_soup_triangles;
+    h->tri.v = nullptr;
+    h->tri.v3 = d_mesh_xyz;
+    h->tri.idx = d_mesh_indices;
+    h->tri.ids = d_tri_ids;
+    h->tri.id_base = tri_id_base;
+    h->n_tri = n_soup_triangles + n_mesh_triangles;
     h->have_tri = true;
     return GRCA_OK;
 }
@@ -1643,6 +1673,8 @@ grca_status grca_set_static_triangles(grca_t h, const float *d_vertices, int64_t
     if (st != GRCA_OK) return st;
     h->st_tri.v = reinterpret_cast<const float4 *>(d_vertices);
     h->st_tri.v3 = nullptr;
+    h->st_tri.va = nullptr;
+    h->st_tri.n_a = 0;
     h->st_tri.idx = d_indices;
     h->st_tri.ids = d_tri_ids;
     h->st_tri.id_base = tri_id_base;

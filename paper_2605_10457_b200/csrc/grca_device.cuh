@@ -133,16 +133,25 @@ __host__ __device__ __forceinline__ float poly_atan(float z) {
 
 // ----------------------------------------------------------------- A1 load --
 struct TriSrc {
+    const float4 *va;      // part A (grca_update_scene): triangles [0, n_a) as float4 triplets, then
+    long long n_a;         // part B = the source below for triangles [n_a, n) (n_a = 0: B only)
     const float4 *v;       // float4 vertices (w ignored), or
     const float *v3;       // non-NULL: packed float3 vertices (12 B each; grca_update_triangles_f3)
     const uint32_t *idx;   // NULL -> non-indexed triplets
-    const int32_t *ids;    // NULL -> id_base + local
+    const int32_t *ids;    // NULL -> id_base + local (global triangle index, parts A and B alike)
     int32_t id_base;
 };
 __device__ __forceinline__ f3 ldcs3(const float *p) { return {__ldcs(p), __ldcs(p + 1), __ldcs(p + 2)}; }
 // Streaming (evict-first) loads: the ~1 GB triangle stream must not evict the L2-resident ray
 // table (67 MB at C4) and hit buffer (33.5 MB) that the intersection kernels gather from.
 __device__ __forceinline__ void load_tri(const TriSrc &T, long long t, f3 v[3]) {
+    if (t < T.n_a) {   // part A: float4 triplets, no indirection (static scenery)
+        v[0] = mk(__ldcs(T.va + 3 * t));
+        v[1] = mk(__ldcs(T.va + 3 * t + 1));
+        v[2] = mk(__ldcs(T.va + 3 * t + 2));
+        return;
+    }
+    t -= T.n_a;
     if (T.idx) {
         const uint32_t i0 = __ldcs(T.idx + 3 * t), i1 = __ldcs(T.idx + 3 * t + 1), i2 = __ldcs(T.idx + 3 * t + 2);
         if (T.v3) {

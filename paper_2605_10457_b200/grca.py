@@ -26,7 +26,7 @@ EXPORTS = [
     "grca_create", "grca_destroy", "grca_set_emitters", "grca_update_triangles", "grca_cast",
     "grca_cast_packed", "grca_hits_packed", "grca_set_static_triangles", "grca_clear_static", "grca_unpack", "grca_get_stats", "grca_kernel_times", "grca_set_distance_noise",
     "grca_debug_all_hits", "grca_debug_large_list", "grca_debug_fast_atan2", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
-    "grca_set_nvls", "grca_nvls_status", "grca_update_triangles_f3",
+    "grca_set_nvls", "grca_nvls_status", "grca_update_triangles_f3", "grca_update_scene",
 ]
 
 
@@ -85,6 +85,7 @@ def load(path: str = LIB_PATH):
         "grca_set_emitters": ([vp, C.POINTER(EmitterC), i32], C.c_int),
         "grca_update_triangles": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
         "grca_update_triangles_f3": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
+        "grca_update_scene": ([vp, vp, i64, vp, i64, vp, i64, vp, i32], C.c_int),
         "grca_cast": ([vp, vp, vp, C.POINTER(Stats)], C.c_int),
         "grca_cast_packed": ([vp], C.c_int),
         "grca_set_static_triangles": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
@@ -244,6 +245,32 @@ class Grca:
         self._check(fn(self._h, _ptr(vertices), nv, _ptr(indices), ntri, _ptr(tri_ids), int(tri_id_base)))
         self._tri_refs = (vertices, indices, tri_ids)
         self.n_triangles = ntri
+        return self
+
+    # -- grca_update_scene: soup = float32 CUDA [3 * n_soup, 4] (float4 triplets, triangles first),
+    #    mesh_xyz = float32 CUDA [n_vertices, 3] with indices int32/uint32 [n_mesh, 3] (triangles after)
+    def update_scene(self, soup=None, mesh_xyz=None, mesh_indices=None, tri_ids=None, tri_id_base: int = 0,
+                     n_soup=None):
+        import torch
+
+        ns = 0
+        if soup is not None:
+            assert soup.is_cuda and soup.dtype == torch.float32 and soup.shape[-1] == 4 and soup.is_contiguous()
+            ns = soup.numel() // 12 if n_soup is None else int(n_soup)
+        nv = nm = 0
+        if mesh_indices is not None:
+            assert mesh_xyz is not None and mesh_xyz.is_cuda and mesh_xyz.dtype == torch.float32
+            assert mesh_xyz.shape[-1] == 3 and mesh_xyz.is_contiguous()
+            assert mesh_indices.is_cuda and mesh_indices.dtype in (torch.int32, torch.uint32)
+            assert mesh_indices.is_contiguous()
+            nv = mesh_xyz.numel() // 3
+            nm = mesh_indices.numel() // 3
+        if tri_ids is not None:
+            assert tri_ids.is_cuda and tri_ids.dtype == torch.int32 and tri_ids.is_contiguous()
+        self._check(self._L.grca_update_scene(self._h, _ptr(soup), ns, _ptr(mesh_xyz), nv, _ptr(mesh_indices), nm,
+                                              _ptr(tri_ids), int(tri_id_base)))
+        self._tri_refs = (soup, mesh_xyz, mesh_indices, tri_ids)
+        self.n_triangles = ns + nm
         return self
 
     # -- grca_set_nvls / grca_nvls_status (NEXT-f3 fused NVLS merge; plumbing in dist.NvlsBuffer)

@@ -336,8 +336,8 @@ def test_c4_full_size_sampled():
     rep, _ = check(w["emitters"], w["tris"], dist, tri, rays=rays)
     assert st["pairs"] == len(w["tris"]) * 8
     assert rep["oracle_hits"] > 20
-    # bench.py's default representation of the same frame (indexed: trivial static indices +
-    # shared car vertices) gives the bit-identical result
+    # bench.py's default representation of the same frame (grca_update_scene: static float4 soup +
+    # indexed float3 cars) gives the bit-identical result
     di, ti = run_indexed_frame(w, g)
     assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
 
@@ -345,7 +345,7 @@ def test_c4_full_size_sampled():
 @pytest.mark.slow
 def test_c4_full_size_large_rectangle_frame():
     """C4 frame 2 (the bench cycles frames 0-3; frames with huge scaled cars send many large
-    rectangles through K3/K4), full size, in the indexed float3 layout bench.py times: sampled
+    rectangles through K3/K4), full size, in the scene layout bench.py times: sampled
     parity against the oracle, plus soup == indexed bit for bit."""
     w = sg.workload("C4", frame=2)
     dist, tri, st, g = run(w["emitters"], w["tris"])
@@ -398,9 +398,16 @@ def test_c2_tilted_frames():
     assert rep["oracle_hits"] > 100
 
 
-def run_indexed_frame(w, g):
-    v, idx = sg.indexed_frame(w)   # as bench.py passes it: packed float3 vertices + indices
-    g.update_triangles(torch.as_tensor(v, device="cuda"), indices=torch.as_tensor(idx, device="cuda"))
+def run_indexed_frame(w, g, layout="scene"):
+    """layout "scene" (bench.py's default): grca_update_scene with the static triangles as a float4
+    soup and the cars as indexed packed float3; "f3": everything indexed packed float3."""
+    v, idx = sg.indexed_frame(w)
+    if layout == "scene":
+        ns3 = 3 * w["n_static"]
+        g.update_scene(soup=tris_to_float4(w["tris"][: w["n_static"]]), mesh_xyz=torch.as_tensor(v[ns3:], device="cuda"),
+                       mesh_indices=torch.as_tensor(idx[ns3:] - ns3, device="cuda"))
+    else:
+        g.update_triangles(torch.as_tensor(v, device="cuda"), indices=torch.as_tensor(idx, device="cuda"))
     d, t = g.cast()
     torch.cuda.synchronize()
     return d.cpu().numpy(), t.cpu().numpy()
@@ -410,9 +417,50 @@ def test_c2_indexed_layout():
     """C2 at full size in bench.py's indexed layout: bit-identical to the soup, parity on sampled rays."""
     w = sg.workload("C2", frame=3)
     dist, tri, st, g = run(w["emitters"], w["tris"])
-    di, ti = run_indexed_frame(w, g)
-    assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
+    for layout in ("scene", "f3"):
+        di, ti = run_indexed_frame(w, g, layout)
+        assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
     check(w["emitters"], w["tris"], di, ti, rays=_sampled(w["emitters"], 1024, 11))
+
+
+def test_update_scene_parts_and_errors():
+    """grca_update_scene: any split point of a soup into [float4 part | indexed float3 part] gives
+    the soup's bit-identical result (ids = global triangle index, or the explicit id array);
+    empty parts; argument errors."""
+    ems, tris = sg.random_scene(91, n_tris=3000, n_emitters=3, gamma=16, chi=240, extent=8.0)
+    d0, t0, st0, g = run(ems, tris)
+    check(ems, tris, d0, t0)
+    n = len(tris)
+    rng = np.random.default_rng(5)
+    for na in (0, 1, 777, n - 1, n):
+        # the mesh part as a vertex-deduplicated indexed float3 mesh with shuffled vertex order
+        mv = tris[na:].reshape(-1, 3)
+        perm = rng.permutation(len(mv))
+        xyz = np.ascontiguousarray(mv[perm])
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(len(perm))
+        g.update_scene(soup=tris_to_float4(tris[:na]) if na else None,
+                       mesh_xyz=torch.as_tensor(xyz, device="cuda") if na < n else None,
+                       mesh_indices=torch.as_tensor(inv.astype(np.int32), device="cuda") if na < n else None)
+        d, t = g.cast()
+        assert np.array_equal(t.cpu().numpy(), t0) and np.array_equal(d.cpu().numpy().view(np.uint32), d0.view(np.uint32))
+    # explicit ids index the concatenation
+    ids = rng.permutation(n).astype(np.int32)
+    g.update_scene(soup=tris_to_float4(tris[:1000]), mesh_xyz=torch.as_tensor(tris[1000:].reshape(-1, 3), device="cuda"),
+                   mesh_indices=torch.arange(3 * (n - 1000), dtype=torch.int32, device="cuda"),
+                   tri_ids=torch.as_tensor(ids, device="cuda"))
+    d, t = g.cast()
+    t = t.cpu().numpy()
+    hit = t0 >= 0
+    assert np.array_equal(t[hit], ids[t0[hit]]) and np.array_equal(t[~hit], t0[~hit])
+    # errors: misaligned soup, negative count, capacity
+    v4 = tris_to_float4(tris)
+    L, h = g._L, g._h
+    E_INVALID, E_CAPACITY = 1, 3   # include/grca.h
+    assert L.grca_update_scene(h, v4.data_ptr() + 4, 10, None, 0, None, 0, None, 0) == E_INVALID
+    assert L.grca_update_scene(h, v4.data_ptr(), -1, None, 0, None, 0, None, 0) == E_INVALID
+    assert L.grca_update_scene(h, v4.data_ptr(), n, v4.data_ptr(), 3, None, 1, None, 0) == E_INVALID  # no indices
+    assert L.grca_update_scene(h, v4.data_ptr(), n + 1, None, 0, None, 0, None, 0) == E_CAPACITY      # > max_triangles
 
 
 @pytest.mark.parametrize("n_em", [9, 17])
