@@ -1,0 +1,5 @@
+timeout 600 python -m pytest tests -m gpu -x -q -k near_axis 2>&1 | tail -3
+GRCA_LIB=abtest/lib_base.so timeout 600 python -m pytest tests -m gpu -x -q -k near_axis 2>&1 | tail -3
+bash abtest/run.sh; bash abtest/run.sh
+for L in abtest/lib_base.so abtest/lib_axis.so; do GRCA_LIB=$L timeout 300 python bench.py --steps 600 --warmup 10 --no-cpu-baseline --no-hybrid --no-e2e --emulate-world 8 --emulate-rank 7 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('N8r7 $L', round(d['ms_per_step'],4), {k: round(v,4) for k,v in d['kernel_ms'].items()})"; done
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3

@@ -23,7 +23,8 @@ namespace grca {
 constexpr float kU = 5.9604644775390625e-8f;   // 2^-24, unit roundoff of fp32
 constexpr float kPadS = 4e-6f;                 // sin(elevation) padding (>> 3u ray rounding)
 constexpr float kPadTheta = 5e-5f;             // azimuth padding in radians
-constexpr float kNearAxis2 = 1e-3f;            // |x_h|^2 < 1e-3 |x|^2 -> full azimuth
+constexpr float kNearAxis2 = 1e-3f;            // |x_h|^2 < 1e-3 |x|^2 -> full azimuth (general frames)
+constexpr float kNearAxisLevel2 = 1e-10f;      // level frames: x_h has no cancellation (cull_pair)
 constexpr float kChordSmall2 = 4e-2f;          // chord^2 below which the L^2/8 edge pad is used
 constexpr float kTRel = 4.5e-6f;               // certified relative error of fp32 t
 constexpr int kChunkItems = 1024;              // target items per load-balanced chunk
@@ -305,9 +306,19 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
         xn[k] = r2[k] * inv[k];
     }
     float slo = fminf(s[0], fminf(s[1], s[2])), shi = fmaxf(s[0], fmaxf(s[1], s[2]));
+    // Near the spin axis the azimuths (and the pole test below) need x_h = (x_f, x_r) accurate
+    // relative to |x_h|.  In a general frame x_h carries absolute errors ~u|x| from the cancellation
+    // of the a_z terms, so within ~1.8 deg of the axis the row is taken whole.  In a level frame x_h
+    // is a 2-D rotation of (a_x, a_y) alone (errors <= 4.25u |x_h| per component, no cancellation):
+    // azimuth error <= 6u + the 2e-6 of fast_atan2, inside kPadTheta, at any |x_h| > 0, so only a
+    // vertex on the axis itself (|x_h| < 1e-5 |x|) forces the full row.
     bool near_axis = false;
+    float h2[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) near_axis |= (x[k].x * x[k].x + x[k].y * x[k].y) < kNearAxis2 * r2[k];
+    for (int k = 0; k < 3; ++k) {
+        h2[k] = x[k].x * x[k].x + x[k].y * x[k].y;
+        near_axis |= h2[k] < (E.level ? kNearAxisLevel2 : kNearAxis2) * r2[k];
+    }
     // Fast path (most survivors: far, small triangles).  In sensor coordinates every point of T is
     // within diam of each vertex, so with rlb = max|x_k| - diam > 2 diam every chord subtends <= q =
     // diam / rlb: edge interiors exceed the vertex elevations by <= q^2/8 and a pole inside T would
@@ -334,12 +345,15 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
         pad_e = 0.13f * q2f;
     } else {
     // pole containment: does the spin axis pass through T?  (2-D winding in the x_f x_r plane)
+    // Bound of the computed winding's error: general frames 9u |x_k||x_k1| (x_h errors ~u|x|);
+    // level frames 16u |x_h,k||x_h,k1| (x_h errors <= 4.25u|x_h| each + 2u for the cross product
+    // = 10.5u, margin 1.5x), so a near-axis triangle still gets a decided pole test.
     bool pos = false, neg = false;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         const int k1 = (k + 1) % 3;
         float w = x[k].x * x[k1].y - x[k].y * x[k1].x;
-        float eps = 9.f * kU * xn[k] * xn[k1];
+        float eps = E.level ? 16.f * kU * (sqrt_approx(h2[k]) * sqrt_approx(h2[k1])) : 9.f * kU * xn[k] * xn[k1];
         pos |= (w > eps);
         neg |= (w < -eps);
     }

@@ -423,6 +423,52 @@ def test_c2_indexed_layout():
     check(w["emitters"], w["tris"], di, ti, rays=_sampled(w["emitters"], 1024, 11))
 
 
+def _near_axis_scene(seed, n=1500):
+    """Triangles within 5 deg of a level emitter's spin axis, above and below: random far / near,
+    tiny / large, 10 % centred on the axis (pole inside), 5 % with a vertex exactly on it."""
+    rng = np.random.default_rng(seed)
+    o = np.array([0.3, -0.2, 1.0])
+    out, off_axis = [], []
+    for i in range(n):
+        sgn = 1.0 if rng.random() < 0.5 else -1.0
+        R = float(np.exp(rng.uniform(np.log(3.0), np.log(300.0))))
+        alpha = 0.0 if i % 10 == 0 else rng.uniform(0.0, np.radians(5.0))
+        beta = rng.uniform(0.0, 2 * np.pi)
+        c = o + R * np.array([np.sin(alpha) * np.cos(beta), np.sin(alpha) * np.sin(beta), sgn * np.cos(alpha)])
+        size = R * float(np.exp(rng.uniform(np.log(1e-4), np.log(0.05))))
+        u = rng.normal(size=(3, 3))
+        T = c + size * u / np.linalg.norm(u, axis=1, keepdims=True)
+        if i % 20 == 1:
+            T[0] = o + np.array([0.0, 0.0, sgn * R])
+        T = T.astype(np.float32)
+        out.append(T)
+        rel = T.astype(np.float64) - o
+        ang = np.arctan2(np.hypot(rel[:, 0], rel[:, 1]), np.abs(rel[:, 2]))
+        # off the axis: every vertex > 0.5 deg from it and an azimuth span < 3 rad (so the axis is
+        # outside T and the arc is not near pi, where a full row is the designed answer)
+        th = np.sort(np.arctan2(rel[:, 1], rel[:, 0]))
+        gaps = np.diff(np.concatenate([th, th[:1] + 2 * np.pi]))
+        off_axis.append(bool(ang.min() > np.radians(0.5)) and 2 * np.pi - gaps.max() < 3.0)
+    return o, np.stack(out), np.array(off_axis)
+
+
+@pytest.mark.parametrize("yaw_deg", [0.0, 37.0])
+def test_near_axis_level_frames(yaw_deg):
+    """Level frames near the spin axis (zenith / nadir of a full-sphere LiDAR, 64 x 1024 rays):
+    full brute-force parity, and triangles off the axis get partial-azimuth rectangles (the
+    general-frame near-axis guard would take all 1024 rays of every row)."""
+    o, tris, off_axis = _near_axis_scene(7 + int(yaw_deg))
+    a = np.radians(yaw_deg)
+    em = sg.Emitter(origin=o, forward=(np.cos(a), np.sin(a), 0.0), right=(np.sin(a), -np.cos(a), 0.0), up=(0, 0, 1),
+                    elev=sg.full_sphere_elev(64), rays_per_channel=1024)
+    dist, tri, st, g = run([em], tris, small_max=64)
+    check([em], tris, dist, tri)
+    L = g.debug_large_list()
+    full = ((L[:, 3] >> 16) & 0xFFFF) >= 1024
+    assert not off_axis[L[full, 0]].any(), "off-axis triangle with a full-azimuth rectangle"
+    assert len(L) > 20 and (~full).sum() > 0
+
+
 def test_update_scene_parts_and_errors():
     """grca_update_scene: any split point of a soup into [float4 part | indexed float3 part] gives
     the soup's bit-identical result (ids = global triangle index, or the explicit id array);
