@@ -71,7 +71,8 @@ struct KParams {
     int4 *large;
     unsigned *n_large;
     long long cap_large;
-    int4 *chunks;
+    int4 *chunks;                // K3 -> K4: {large-pair index, e | row << 8, 1 | lo << 16, len}
+    float4 *large_setup;         // K3 -> K4: per large pair the 5-float4 setup (slot layout of setup_to_slot)
     unsigned *n_chunks;
     long long cap_chunks;
     unsigned long long *stats;
@@ -904,11 +905,21 @@ __global__ void __launch_bounds__(256, K3_MINB) k_bin(const __grid_constant__ KP
         const int r_lo = D.w & 0xffff, r_len = (int)((unsigned)D.w >> 16);
         const EmDev &E = P.em[e];
         const bool full = r_len >= E.chi;
+        f3 v[3];
+        load_tri(P.tri, tri, v);
+        {   // the pair's certified setup, once for all its chunks (K4 reads it; slot layout of
+            // setup_to_slot).  Every lane computes the same values; lane k stores float4 k.
+            float4 *Sd = P.large_setup + 5 * w;
+            const uint32_t id = tri_id(P.tri, tri);
+            const bool ok = setup_core(v, em_o(E), P.faces, [&](int k, float4 q) {
+                if (k == 4) q = make_float4(q.x, __uint_as_float(id), __int_as_float((int)tri), __int_as_float(e));
+                if (lane == k) Sd[k] = q;
+            });
+            if (!ok) continue;   // Vol = 0 or face-culled: the pair can never hit
+        }
         d3 x[3];
         float th_ref = 0.f;
         if (!full && !P.norefine) {
-            f3 v[3];
-            load_tri(P.tri, tri, v);
             const d3 O = {(double)E.o[0], (double)E.o[1], (double)E.o[2]};
 #pragma unroll
             for (int k = 0; k < 3; ++k) {
@@ -967,7 +978,7 @@ __global__ void __launch_bounds__(256, K3_MINB) k_bin(const __grid_constant__ KP
             for (int c0 = 0; c0 < len; c0 += kColMax) {
                 int l0 = lo + c0;
                 if (l0 >= E.chi) l0 -= E.chi;
-                P.chunks[pos++] = make_int4((int)tri, e | (j << 8), (int)(1u | ((unsigned)l0 << 16)),
+                P.chunks[pos++] = make_int4((int)w, e | (j << 8), (int)(1u | ((unsigned)l0 << 16)),
                                             min(kColMax, len - c0));
             }
         }
@@ -999,33 +1010,51 @@ __global__ void __launch_bounds__(K4_THREADS, K4_MINB) k_isect(const __grid_cons
     const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
     for (long long c = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < n; c += nw) {
         const int4 ch = P.chunks[c];
-        const long long tri = ch.x;
         const EmDev &E = sE[ch.y & 255];
         const int row0 = (unsigned)ch.y >> 8;
         const int nrows = ch.z & 0xffff;
         const int lo = (unsigned)ch.z >> 16;
         const int len = ch.w;
-        f3 v[3];
-        load_tri(P.tri, tri, v);
-        const uint32_t id = tri_id(P.tri, tri);
+        // the pair's setup, computed once by K3 (same address in every lane: broadcast loads)
+        const float4 *Sp = P.large_setup + 5 * (long long)ch.x;
+        const float4 s0 = __ldcg(Sp), s1 = __ldcg(Sp + 1), s2 = __ldcg(Sp + 2), s3 = __ldcg(Sp + 3),
+                     s4 = __ldcg(Sp + 4);
         Setup S;
-        if (!make_setup(v, em_o(E), P.faces, S, setup64)) continue;
+        S.n0 = {s0.x, s0.y, s0.z}; S.B0 = s0.w;
+        S.n1 = {s1.x, s1.y, s1.z}; S.B1 = s1.w;
+        S.n2 = {s2.x, s2.y, s2.z}; S.B2 = s2.w;
+        S.N = {s3.x, s3.y, s3.z}; S.habs = s3.w;
+        S.TN = s4.x;
+        const uint32_t id = __float_as_uint(s4.y);
+        const long long tri = __float_as_int(s4.z);
         const int items = nrows * len;
         const float invl = __fdividef(1.f, (float)len);   // row guess, corrected by +-1
         if (lane == 0) cnt[ST_ITEMS_LARGE] += items;
-        for (int q = lane; q < items; q += 32) {
+        auto ray_of = [&](int q) {
             int row = (int)(((float)q + 0.5f) * invl);
             int col = q - row * len;
             if (col < 0) { --row; col += len; }
             if (col >= len) { ++row; col -= len; }
             int i = lo + col;
             if (i >= E.chi) i -= E.chi;
-            const int g = E.ray_base + (row0 + row) * E.chi + i;
-            const float4 d = __ldg(P.raytab + g);
+            return E.ray_base + (row0 + row) * E.chi + i;
+        };
+        // software-pipelined: the next item's ray is in flight while this one is tested
+        int gn = lane < items ? ray_of(lane) : 0;
+        float4 dn = lane < items ? __ldg(P.raytab + gn) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = lane; q < items; q += 32) {
+            const int g = gn;
+            const float4 d = dn;
+            if (q + 32 < items) {
+                gn = ray_of(q + 32);
+                dn = __ldg(P.raytab + gn);
+            }
             float th = 0.f;
             int r = P.force64 ? 2 : test_fast(d, S, E.dmax_lo, E.dmax_hi, th);
-            if (r == 2) {
+            if (r == 2) {   // rare: the vertices for the fp64 decision
                 cnt[ST_FP64]++;
+                f3 v[3];
+                load_tri(P.tri, tri, v);
                 r = test_exact_r(v, em_o(E), d, E.dmax, P.faces, th);
             }
             if (r == 1) {
@@ -1118,6 +1147,7 @@ struct grca_ctx {
     size_t k2f_smem = 0;
     int4 *d_large = nullptr;
     int4 *d_chunks = nullptr;
+    float4 *d_large_setup = nullptr;
     unsigned *d_ctrl = nullptr;
     unsigned long long *d_stats = nullptr;
     long long cap_large = 0, cap_chunks = 0;
@@ -1180,6 +1210,7 @@ void free_all(grca_t h) {
     cudaFree(h->d_desc);
     cudaFree(h->d_large);
     cudaFree(h->d_chunks);
+    cudaFree(h->d_large_setup);
     cudaFree(h->d_ctrl);
     cudaFree(h->d_stats);
     if (h->ev_ok)
@@ -1204,6 +1235,7 @@ KParams params(grca_t h) {
     P.n_large = h->d_ctrl + 0;
     P.cap_large = h->cap_large;
     P.chunks = h->d_chunks;
+    P.large_setup = h->d_large_setup;
     P.n_chunks = h->d_ctrl + 1;
     P.n_surv = h->d_ctrl + 2;
     P.cap_chunks = h->cap_chunks;
@@ -1298,6 +1330,7 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     alloc((void **)&h->d_lut, sizeof(unsigned char) * kLutMaxEm * kLutBins);
     alloc((void **)&h->d_large, sizeof(int4) * h->cap_large);
     alloc((void **)&h->d_chunks, sizeof(int4) * h->cap_chunks);
+    alloc((void **)&h->d_large_setup, sizeof(float4) * 5 * h->cap_large);
     alloc((void **)&h->d_ctrl, sizeof(unsigned) * 8);
     alloc((void **)&h->d_stats, sizeof(unsigned long long) * 32);
     if (!ok) {
