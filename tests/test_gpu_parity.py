@@ -499,6 +499,18 @@ def test_update_scene_parts_and_errors():
     t = t.cpu().numpy()
     hit = t0 >= 0
     assert np.array_equal(t[hit], ids[t0[hit]]) and np.array_equal(t[~hit], t0[~hit])
+    # hybrid: the first 1200 triangles as the cached static set, the rest through grca_update_scene
+    # (a soup part and an indexed part, ids continuing the static ones) == the plain soup cast
+    gh = Grca(device=0, max_triangles=n, max_rays=sg.n_rays_total(ems))
+    gh.set_emitters(ems)
+    gh.set_static_triangles(tris_to_float4(tris[:1200]), tri_id_base=0)
+    gh.update_scene(soup=tris_to_float4(tris[1200:2000]),
+                    mesh_xyz=torch.as_tensor(tris[2000:].reshape(-1, 3), device="cuda"),
+                    mesh_indices=torch.arange(3 * (n - 2000), dtype=torch.int32, device="cuda"), tri_id_base=1200)
+    for _ in range(2):   # first cast fills the static cache, the second starts from it
+        d, t = gh.cast()
+        assert np.array_equal(t.cpu().numpy(), t0) and np.array_equal(d.cpu().numpy().view(np.uint32), d0.view(np.uint32))
+    gh.close()
     # errors: misaligned soup, negative count, capacity
     v4 = tris_to_float4(tris)
     L, h = g._L, g._h
