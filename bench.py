@@ -312,8 +312,9 @@ def main():
     ap.add_argument("--emulate-world", type=int, default=0, help="do rank --emulate-rank's share of a W-rank run "
                     "on this one GPU (sensor shards: ranks never wait on one another); see tools/emulate_ranks.py")
     ap.add_argument("--emulate-rank", type=int, default=0)
-    ap.add_argument("--merge", choices=["allreduce", "nvls"], default="allreduce",
-                    help="triangle-shard merge: NCCL all-reduce(MIN) of the packed keys, or the fused NVLS "
+    ap.add_argument("--merge", choices=["allreduce", "reduce_scatter", "nvls"], default="allreduce",
+                    help="triangle-shard merge: NCCL all-reduce(MIN) of the packed keys, reduce-scatter(MIN) "
+                         "(each rank keeps its ray slice; half the traffic), or the fused NVLS "
                          "multimem.red.min in the intersection kernels (NEXT-f3; needs NVLS multicast)")
     ap.add_argument("--soup", action="store_true", help="triangle-soup scene (float4 triplets) instead of the indexed "
                     "car meshes (same triangles; the e2e upload is then every dynamic triangle's vertices)")
@@ -433,7 +434,11 @@ def main():
         merge = False
 
     def cast_once(dout=dist_out, tout=tri_out):
-        if merge:   # triangle shards: exact merge = all-reduce(MIN) of the packed (t, id) keys
+        if merge and args.merge == "reduce_scatter":   # ray-sharded result: this rank's slice only
+            g.cast_packed()
+            sl, first = D.merge_packed_scatter(g.hits_packed(), group=merge_group)
+            g.unpack_range(sl, first, dout[first: first + sl.numel()], tout[first: first + sl.numel()])
+        elif merge:   # triangle shards: exact merge = all-reduce(MIN) of the packed (t, id) keys
             g.cast_packed()
             D.merge_packed(g.hits_packed(), group=merge_group)
             g.unpack(dout, tout)
@@ -654,7 +659,7 @@ def main():
                        "subdiv": args.subdiv, "car_scale": list(scene.scale), "mesh": scene.mesh,
                        "sharding": ("none" if world == 1 else
                                     f"triangles block-interleaved ({D.BLOCK}) + "
-                                    f"{'fused NVLS multimem.red.min' if nvls else 'all-reduce(MIN)'} x {world}"
+                                    f"{'fused NVLS multimem.red.min' if nvls else 'reduce-scatter(MIN), ray-sharded output' if args.merge == 'reduce_scatter' else 'all-reduce(MIN)'} x {world}"
                                     if shard == "triangles" else
                                     f"{shard.split(':')[1]} emitter groups x {world // int(shard.split(':')[1])} "
                                     f"triangle shards, all-reduce(MIN) within a group"

@@ -202,6 +202,16 @@ grca_status grca_cast(grca_t h, float *d_out_dist, int32_t *d_out_tri, grca_stat
 grca_status grca_cast_packed(grca_t h);
 grca_status grca_hits_packed(grca_t h, uint64_t **d_hits, int64_t *n_rays);
 grca_status grca_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri);
+/* K5 over a slice of the rays, for ray-sharded merges (a reduce-scatter(MIN) leaves
+ * each rank the merged keys of its own ray slice).  d_keys: device uint64[n] holding the packed keys
+ * of global rays [first_ray, first_ray + n), or NULL for the handle's own buffer at first_ray.
+ * d_out_dist / d_out_tri: device float[n] / int32[n] (slice-local), either may be NULL.  The distance
+ * noise model (grca_set_distance_noise) keys its draws by the global ray index, so a slice gives
+ * exactly the values the full unpack gives for those rays.  Counts as the cast's unpack (advances
+ * the cast counter, like grca_unpack).  Errors: GRCA_E_INVALID (range outside [0, n_rays)),
+ * GRCA_E_STATE (no emitters), GRCA_E_CUDA. */
+grca_status grca_unpack_range(grca_t h, const uint64_t *d_keys, int64_t first_ray, int64_t n, float *d_out_dist,
+                              int32_t *d_out_tri);
 
 /* NEXT-f3: fused NVLS min-merge for triangle-sharded multi-GPU casts (the merge
  * of PAPER.md's per-ray closest hit over shards, P:2340-2356 f_sort).  d_uc is this rank's unicast

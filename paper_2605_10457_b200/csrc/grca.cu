@@ -1083,14 +1083,15 @@ __device__ __forceinline__ float gauss01(unsigned long long key) {
 }
 
 __global__ void k_unpack(const unsigned long long *__restrict__ hits, float *__restrict__ dist,
-                         int32_t *__restrict__ tri, long long n, float sigma, unsigned long long seed,
+                         int32_t *__restrict__ tri, long long n, long long first, float sigma, unsigned long long seed,
                          unsigned long long cast_idx) {
+    // hits[i] / dist[i] / tri[i] belong to global ray first + i (the noise model's counter key)
     const long long stride = (long long)gridDim.x * blockDim.x;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
         const unsigned long long k = __ldcs(hits + i);
         float dv = __uint_as_float((unsigned)(k >> 32));
         if (sigma > 0.f && dv < CUDART_INF_F)   // noise model: range noise after output conversion
-            dv = fmaxf(0.f, dv + sigma * gauss01(splitmix64(seed ^ (cast_idx << 40)) ^ (unsigned long long)i));
+            dv = fmaxf(0.f, dv + sigma * gauss01(splitmix64(seed ^ (cast_idx << 40)) ^ (unsigned long long)(first + i)));
         if (dist) __stcs(dist + i, dv);
         if (tri) __stcs(tri + i, (int32_t)(unsigned)(k & 0xffffffffull));
     }
@@ -1847,13 +1848,16 @@ static grca_status launch_packed(grca_t h) {
     return GRCA_OK;
 }
 
-static grca_status launch_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri) {
+static grca_status launch_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri,
+                                 const unsigned long long *keys = nullptr, long long first = 0, long long n = -1) {
     DeviceGuard dg(h->device);
     const int slot = (int)(h->n_casts % kRing);
-    if (d_out_dist || d_out_tri) {
-        const long long blocks = std::min<long long>((h->n_rays + 255) / 256, (long long)h->num_sms * 8);
+    if (!keys) keys = (h->nvls_uc ? h->nvls_uc : h->d_hits) + first;
+    if (n < 0) n = h->n_rays;
+    if ((d_out_dist || d_out_tri) && n > 0) {
+        const long long blocks = std::min<long long>((n + 255) / 256, (long long)h->num_sms * 8);
         k_unpack<<<(unsigned)std::max<long long>(1, blocks), 256, 0, h->stream>>>(
-            h->nvls_uc ? h->nvls_uc : h->d_hits, d_out_dist, d_out_tri, h->n_rays, h->noise_sigma, h->noise_seed, (unsigned long long)h->n_casts);
+            keys, d_out_dist, d_out_tri, n, first, h->noise_sigma, h->noise_seed, (unsigned long long)h->n_casts);
         CK(cudaGetLastError());
     }
     if (h->ev_ok) CK(cudaEventRecord(h->ev[slot][7], h->stream));
@@ -1908,6 +1912,18 @@ grca_status grca_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri) {
     if (!h) return GRCA_E_INVALID;
     if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
     grca_status s = launch_unpack(h, d_out_dist, d_out_tri);
+    ++h->n_casts;
+    return s;
+}
+
+grca_status grca_unpack_range(grca_t h, const uint64_t *d_keys, int64_t first_ray, int64_t n, float *d_out_dist,
+                              int32_t *d_out_tri) {
+    if (!h) return GRCA_E_INVALID;
+    if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
+    if (first_ray < 0 || n < 0 || first_ray + n > h->n_rays)
+        return fail(h, GRCA_E_INVALID, "ray range outside [0, n_rays)");
+    grca_status s = launch_unpack(h, d_out_dist, d_out_tri, reinterpret_cast<const unsigned long long *>(d_keys),
+                                  first_ray, n);
     ++h->n_casts;
     return s;
 }

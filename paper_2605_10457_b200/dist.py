@@ -64,6 +64,32 @@ def merge_packed(hits, group=None):
     return hits
 
 
+def merge_packed_scatter(hits, group=None):
+    """Exact merge with a ray-sharded result: rank r of the group receives the min over
+    ranks of the keys of rays [r c, (r + 1) c), c = ceil(n / P) -- a reduce-scatter(MIN), half the
+    traffic of the all-reduce.  Returns (keys slice, first ray); unpack it with Grca.unpack_range.
+    NCCL: reduce_scatter_tensor; other backends (gloo tests): all-reduce then slice."""
+    import torch
+    import torch.distributed as dist
+
+    assert hits.dtype == torch.int64
+    P, r = dist.get_world_size(group), dist.get_rank(group)
+    n = hits.numel()
+    c = -(-n // P)
+    src = hits if n == c * P else torch.cat([hits, torch.full((c * P - n,), MISS_KEY, dtype=hits.dtype,
+                                                              device=hits.device)])
+    first = r * c
+    n_mine = max(0, min(c, n - first))
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty(c, dtype=hits.dtype, device=hits.device)
+        dist.reduce_scatter_tensor(out, src, op=dist.ReduceOp.MIN, group=group)
+    else:
+        tmp = src.clone()
+        dist.all_reduce(tmp, op=dist.ReduceOp.MIN, group=group)
+        out = tmp[first: first + c].clone()
+    return out[:n_mine], first
+
+
 def gather_emitter_slices(dist_slice, tri_slice, rank_emitters_rays: Sequence[Sequence[int]], offsets, group=None):
     """Assemble the full (dist, tri) layout from per-rank emitter slices (sensor sharding).
 

@@ -27,6 +27,7 @@ EXPORTS = [
     "grca_cast_packed", "grca_hits_packed", "grca_set_static_triangles", "grca_clear_static", "grca_unpack", "grca_get_stats", "grca_kernel_times", "grca_set_distance_noise",
     "grca_debug_all_hits", "grca_debug_large_list", "grca_debug_fast_atan2", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
     "grca_set_nvls", "grca_nvls_status", "grca_update_triangles_f3", "grca_update_scene",
+    "grca_unpack_range",
 ]
 
 
@@ -92,6 +93,7 @@ def load(path: str = LIB_PATH):
         "grca_clear_static": ([vp], C.c_int),
         "grca_hits_packed": ([vp, C.POINTER(vp), C.POINTER(i64)], C.c_int),
         "grca_unpack": ([vp, vp, vp], C.c_int),
+        "grca_unpack_range": ([vp, vp, i64, i64, vp, vp], C.c_int),
         "grca_get_stats": ([vp, C.POINTER(Stats)], C.c_int),
         "grca_set_distance_noise": ([vp, C.c_float, C.c_uint64], C.c_int),
         "grca_kernel_times": ([vp, i32, C.POINTER(C.c_float)], C.c_int),
@@ -328,6 +330,18 @@ class Grca:
 
     def unpack(self, out_dist, out_tri):
         self._check(self._L.grca_unpack(self._h, _ptr(out_dist), _ptr(out_tri)))
+
+    def unpack_range(self, keys, first_ray: int, out_dist, out_tri):
+        """K5 over rays [first_ray, first_ray + n): keys = int64/uint64 CUDA tensor [n] of packed keys
+        (e.g. this rank's reduce-scatter slice) or None for the handle's buffer (then n =
+        out_dist/out_tri length); outputs are slice-local."""
+        if keys is not None:
+            assert keys.is_cuda and keys.element_size() == 8 and keys.is_contiguous()
+            n = keys.numel()
+        else:
+            n = (out_dist if out_dist is not None else out_tri).numel()
+        self._check(self._L.grca_unpack_range(self._h, _ptr(keys), int(first_ray), int(n), _ptr(out_dist),
+                                              _ptr(out_tri)))
 
     def set_distance_noise(self, sigma: float, seed: int = 0):
         self._check(self._L.grca_set_distance_noise(self._h, float(sigma), int(seed)))

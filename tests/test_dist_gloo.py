@@ -114,6 +114,42 @@ def test_four_rank_mixed_partition():
         assert np.all(same | tie) and same.mean() > 0.999, rank
 
 
+def _worker_scatter(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ems, tris = sg.random_scene(79, n_tris=5000, n_emitters=1, gamma=7, chi=61, extent=8.0)   # 427 rays
+        own = D.shard_triangles(len(tris), rank, world, block=256)
+        res = oracle.cast(ems, tris[own], ids=own.astype(np.int32), threads=2)
+        hits = torch.as_tensor(_packed(res))
+        sl, first = D.merge_packed_scatter(hits)
+        q.put((rank, first, sl.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_three_rank_reduce_scatter_merge():
+    """Ray-sharded merge (reduce-scatter(MIN)) with a ray count not divisible by the
+    ranks: the slices tile [0, n_rays) in rank order and equal the unsharded oracle's keys."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_scatter, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    got = sorted([q.get(timeout=300) for _ in range(3)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ems, tris = sg.random_scene(79, n_tris=5000, n_emitters=1, gamma=7, chi=61, extent=8.0)
+    ref = _packed(oracle.cast(ems, tris, want_t64=True))
+    assert [f for _, f, _ in got] == [0, 143, 286] and sum(len(s) for _, _, s in got) == len(ref) == 427
+    merged = np.concatenate([s for _, _, s in got])
+    same = merged == ref
+    assert np.all(same | ((merged >> 32) == (ref >> 32))) and same.mean() > 0.999
+
+
 def test_partition_helpers():
     n, world = 100_000, 4
     parts = [D.shard_triangles(n, r, world) for r in range(world)]

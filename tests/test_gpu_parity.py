@@ -706,6 +706,42 @@ def test_distance_noise():
     assert np.array_equal(d3.view(np.uint32), d1.view(np.uint32))   # same seed, same cast index
 
 
+def test_unpack_range_slices():
+    """grca_unpack_range (the reduce-scatter merge's K5): for each ray slice of a 3-way split (ragged),
+    keys passed as a separate slice tensor give exactly the full unpack's values for those rays,
+    distance noise included (keyed by the global ray index, same cast index); bad ranges rejected."""
+    ems, tris = sg.random_scene(512, n_tris=2500, n_emitters=2, gamma=17, chi=301, extent=6.0)
+    n = sg.n_rays_total(ems)
+
+    def handle():
+        g = Grca(device=0, max_triangles=len(tris), max_rays=n)
+        g.set_emitters(ems)
+        g.update_triangles(tris_to_float4(tris))
+        g.set_distance_noise(0.05, seed=9)
+        return g
+
+    g = handle()
+    d_full, t_full = [x.cpu().numpy() for x in g.cast()]
+    assert (t_full >= 0).sum() > 1000
+    c = -(-n // 3)
+    for r in range(3):
+        gr = handle()
+        gr.cast_packed()
+        first = r * c
+        m = min(c, n - first)
+        keys = gr.hits_packed()[first: first + m].clone()
+        d = torch.empty(m, dtype=torch.float32, device="cuda")
+        t = torch.empty(m, dtype=torch.int32, device="cuda")
+        gr.unpack_range(keys, first, d, t)
+        torch.cuda.synchronize()
+        assert np.array_equal(t.cpu().numpy(), t_full[first: first + m])
+        assert np.array_equal(d.cpu().numpy().view(np.uint32), d_full[first: first + m].view(np.uint32))
+        E_INVALID = 1   # include/grca.h
+        assert gr._L.grca_unpack_range(gr._h, None, n - 5, 6, d.data_ptr(), None) == E_INVALID
+        assert gr._L.grca_unpack_range(gr._h, None, -1, 1, d.data_ptr(), None) == E_INVALID
+        gr.close()
+
+
 def test_nvls_fused_merge_single_device():
     """NEXT-f3: with a 1-device multicast (NVLS) object, every hit goes through
     multimem.red.min.u64 and both device-side barriers run: bit-identical to the local path,
