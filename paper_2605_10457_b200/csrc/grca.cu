@@ -98,14 +98,18 @@ __device__ __forceinline__ f3 em_o(const EmDev &E) { return {E.o[0], E.o[1], E.o
 
 __device__ __forceinline__ void block_flush(unsigned long long *acc_smem, unsigned long long *stats,
                                             const unsigned *mine) {
-    // warp reduce then smem then one atomic per block per counter
+    // warp reduce then smem then one atomic per block per counter.  REDUX.SUM on the 16-bit halves
+    // of the per-thread u32 counts (each half-sum < 2^21: exact), and counters that are zero in the
+    // whole warp are skipped (one vote): this runs at the end of every warp's chain (K3/K4 latency).
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) {
-        unsigned long long v = mine[c];   // per-thread u32 counts, summed in 64 bits
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-        if (lane == 0 && v) atomicAdd(acc_smem + c, v);
+        const unsigned v = mine[c];
+        if (__any_sync(FULL, v != 0u)) {
+            const unsigned lo = __reduce_add_sync(FULL, v & 0xffffu);
+            const unsigned hi = __reduce_add_sync(FULL, v >> 16);
+            if (lane == 0) atomicAdd(acc_smem + c, (unsigned long long)lo + ((unsigned long long)hi << 16));
+        }
     }
     __syncthreads();
     if (threadIdx.x < ST_COUNT && acc_smem[threadIdx.x]) atomicAdd(stats + threadIdx.x, acc_smem[threadIdx.x]);
