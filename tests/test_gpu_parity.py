@@ -452,21 +452,28 @@ def _near_axis_scene(seed, n=1500):
     return o, np.stack(out), np.array(off_axis)
 
 
-@pytest.mark.parametrize("yaw_deg", [0.0, 37.0])
-def test_near_axis_level_frames(yaw_deg):
-    """Level frames near the spin axis (zenith / nadir of a full-sphere LiDAR, 64 x 1024 rays):
-    full brute-force parity, and triangles off the axis get partial-azimuth rectangles (the
-    general-frame near-axis guard would take all 1024 rays of every row)."""
+@pytest.mark.parametrize("yaw_deg,tilt_deg", [(0.0, 0.0), (37.0, 0.0), (20.0, 0.5)])
+def test_near_axis_level_frames(yaw_deg, tilt_deg):
+    """Near the spin axis (zenith / nadir of a full-sphere LiDAR, 64 x 1024 rays): full brute-force
+    parity.  Level frames: triangles off the axis get partial-azimuth rectangles (the general-frame
+    near-axis guard would take all 1024 rays of every row).  A frame tilted by 0.5 deg is not level:
+    the guard applies (parity only)."""
     o, tris, off_axis = _near_axis_scene(7 + int(yaw_deg))
-    a = np.radians(yaw_deg)
-    em = sg.Emitter(origin=o, forward=(np.cos(a), np.sin(a), 0.0), right=(np.sin(a), -np.cos(a), 0.0), up=(0, 0, 1),
-                    elev=sg.full_sphere_elev(64), rays_per_channel=1024)
+    a, b = np.radians(yaw_deg), np.radians(tilt_deg)
+    f = np.array([np.cos(a), np.sin(a), 0.0])
+    r = np.array([np.sin(a), -np.cos(a), 0.0])
+    u = np.array([0.0, 0.0, 1.0])
+    if tilt_deg:   # roll about the forward axis
+        r, u = np.cos(b) * r + np.sin(b) * u, -np.sin(b) * r + np.cos(b) * u
+    em = sg.Emitter(origin=o, forward=f, right=r, up=u, elev=sg.full_sphere_elev(64), rays_per_channel=1024)
     dist, tri, st, g = run([em], tris, small_max=64)
     check([em], tris, dist, tri)
     L = g.debug_large_list()
     full = ((L[:, 3] >> 16) & 0xFFFF) >= 1024
-    assert not off_axis[L[full, 0]].any(), "off-axis triangle with a full-azimuth rectangle"
-    assert len(L) > 20 and (~full).sum() > 0
+    assert len(L) > 20
+    if not tilt_deg:
+        assert not off_axis[L[full, 0]].any(), "off-axis triangle with a full-azimuth rectangle"
+        assert (~full).sum() > 0
 
 
 def test_update_scene_parts_and_errors():
