@@ -28,7 +28,10 @@ constexpr float kNearAxisLevel2 = 1e-10f;      // level frames: x_h has no cance
 constexpr float kChordSmall2 = 4e-2f;          // chord^2 below which the L^2/8 edge pad is used
 constexpr float kTRel = 4.5e-6f;               // certified relative error of fp32 t
 constexpr int kChunkItems = 1024;              // target items per load-balanced chunk
-constexpr int kColMax = 1024;                  // max columns per chunk row segment
+#ifndef GRCA_COLMAX
+#define GRCA_COLMAX 128   // K4 chain = one chunk: 128 rays = 4 steps of 32 (measured: 1024 -> 128 took K4 0.046 -> 0.031 ms at C4)
+#endif
+constexpr int kColMax = GRCA_COLMAX;           // max columns per chunk row segment
 
 // Per-emitter record (device + shared memory).  A = M^-1 with M = [f r u] (fp64 inverse,
 // rounded): x = A (p - o) are the coordinates in which ray (j,i) is exactly
