@@ -1086,17 +1086,43 @@ __device__ __forceinline__ float gauss01(unsigned long long key) {
     return sqrtf(-2.f * __logf(u1)) * __cosf(6.283185307f * u2);
 }
 
+__device__ __forceinline__ float unpack_dist(unsigned long long k, long long g, float sigma, unsigned long long base) {
+    float dv = __uint_as_float((unsigned)(k >> 32));
+    if (sigma > 0.f && dv < CUDART_INF_F)   // noise model: range noise after output conversion
+        dv = fmaxf(0.f, dv + sigma * gauss01(base ^ (unsigned long long)g));
+    return dv;
+}
+
 __global__ void k_unpack(const unsigned long long *__restrict__ hits, float *__restrict__ dist,
                          int32_t *__restrict__ tri, long long n, long long first, float sigma, unsigned long long seed,
                          unsigned long long cast_idx) {
-    // hits[i] / dist[i] / tri[i] belong to global ray first + i (the noise model's counter key)
+    // hits[i] / dist[i] / tri[i] belong to global ray first + i (the noise model's counter key).
+    // Two rays per thread step (16-byte key loads, 8-byte stores) when the buffers allow it: a
+    // streaming kernel needs ~6.5 MB in flight to reach HBM bandwidth.
+    const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
-    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const unsigned long long base = splitmix64(seed ^ (cast_idx << 40));
+    const bool vec = ((reinterpret_cast<uintptr_t>(hits) & 15) | (reinterpret_cast<uintptr_t>(dist) & 7) |
+                      (reinterpret_cast<uintptr_t>(tri) & 7)) == 0;
+    long long done = 0;
+    if (vec) {
+        const long long n2 = n >> 1;
+        const ulonglong2 *h2 = reinterpret_cast<const ulonglong2 *>(hits);
+        for (long long i = tid; i < n2; i += stride) {
+            const ulonglong2 k = __ldcs(h2 + i);
+            const long long g = first + 2 * i;
+            if (dist)
+                __stcs(reinterpret_cast<float2 *>(dist) + i,
+                       make_float2(unpack_dist(k.x, g, sigma, base), unpack_dist(k.y, g + 1, sigma, base)));
+            if (tri)
+                __stcs(reinterpret_cast<int2 *>(tri) + i,
+                       make_int2((int32_t)(unsigned)(k.x & 0xffffffffull), (int32_t)(unsigned)(k.y & 0xffffffffull)));
+        }
+        done = 2 * n2;
+    }
+    for (long long i = done + tid; i < n; i += stride) {
         const unsigned long long k = __ldcs(hits + i);
-        float dv = __uint_as_float((unsigned)(k >> 32));
-        if (sigma > 0.f && dv < CUDART_INF_F)   // noise model: range noise after output conversion
-            dv = fmaxf(0.f, dv + sigma * gauss01(splitmix64(seed ^ (cast_idx << 40)) ^ (unsigned long long)(first + i)));
-        if (dist) __stcs(dist + i, dv);
+        if (dist) __stcs(dist + i, unpack_dist(k, first + i, sigma, base));
         if (tri) __stcs(tri + i, (int32_t)(unsigned)(k & 0xffffffffull));
     }
 }
@@ -1834,7 +1860,7 @@ static grca_status launch_packed(grca_t h) {
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][0], h->stream));
     {   // K0
-        const int grid = h->num_sms * 4;
+        const int grid = h->num_sms * 8;   // full occupancy: stores in flight for HBM bandwidth
         k_init<<<grid, 256, 0, h->stream>>>(P.hits, P.allhits, h->n_rays, h->d_ctrl, h->d_stats,
                                             h->st_set ? h->d_static_keys : nullptr,
                                             (h->st_set && P.allhits) ? h->d_static_allhits : nullptr);
