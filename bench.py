@@ -3,14 +3,15 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
 
 One step = one LiDAR frame of BASELINE config C4 (8 LiDARs 128x4096 = 4,194,304 rays,
-~21.8M triangles of which ~9.0M dynamic, 1000 m range): K0 init -> K2 cull (+inline small
-work) -> K3 bin -> K4 intersect -> [N>1: NCCL min-allreduce of the packed hit buffer] -> K5
-unpack.  Inputs are resident in HBM (static scene + per-frame posed dynamic instances, 4 frame
-buffers of ~1 GB cycled, so every step reads > L2).  With N>1 (torchrun) triangles are sharded
-block-interleaved across ranks (strong scaling).  `e2e` repeats the measurement through the
-public API with the frame's dynamic vertices copied from pinned host memory and the outputs
-copied back inside the timed region.  `--impl reference` times the brute-force oracle (the
-reference arm of this tier) on host cores.
+~21.8M triangles of which ~9.0M dynamic, 1000 m range): K0 init -> K2 cull -> fused refine +
+small-rectangle intersection -> K3 bin -> K4 intersect -> K5 unpack.  Inputs are resident in HBM
+(grca_update_scene: the static scenery as one float4 soup, the cars as indexed float3 meshes with
+4 posed frames cycled; every step streams 0.78 GB, > L2).  With N>1 (torchrun) the emitters are
+sharded across ranks (sensor sharding, no reduction; --shard triangles|mixed adds an NCCL
+min-merge of the packed hit keys: all-reduce, reduce-scatter or the fused NVLS path).  `e2e`
+repeats the measurement through the public API with the frame's car vertices copied from pinned
+host memory and the outputs copied back inside the timed region.  `--impl reference` times the
+brute-force oracle (the reference arm of this tier) on host cores.
 """
 from __future__ import annotations
 
