@@ -246,7 +246,7 @@ def ncu_traffic():
     for k, v in d.get("per_kernel", {}).items():
         for ours, nm in NCU_NAME.items():
             if nm in k:
-                out[ours] = v["dram_bytes"]
+                out[ours] = v
     return out, os.path.basename(files[-1])
 
 
@@ -278,9 +278,12 @@ def kernel_rooflines(kernel_ms, st, n_rays, n_tri, n_em, clk, device, split=Fals
             ach, peak, unit = amount / t / 1e9, pk["hbm_gbs"], "GB/s"
         else:
             ach, peak, unit = amount / t / 1e12, alu_peak, "Tops/s"
-        tr = traffic.get(k)
+        tr = traffic.get(k, {})
         out[k] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-                  "traffic": tr, "algorithmic_per_launch": amount,
+                  "traffic": tr.get("dram_bytes"), "algorithmic_per_launch": amount,
+                  # context from the same ncu capture: fraction of cycles an instruction issued
+                  # (a latency-bound kernel sits well below 1 even when its ALU fraction is low)
+                  "ncu_issue_slots_busy": (tr["issue_slots_busy_pct"] / 100.0) if "issue_slots_busy_pct" in tr else None,
                   "peak_src": (pk["src"] + " (MEASURED_PEAKS.json hbm_gbs)") if bound == "hbm" else
                   f"derived: {n_sm} SMs x 128 fp32 lanes x {mhz:.0f} MHz (median SM clock under load)",
                   "traffic_src": src}

@@ -95,6 +95,12 @@ def full(rep, out, traffic_json=None):
         if k in rawd:
             lines.append(f"- DRAM traffic per launch (read + write): {rawd[k]['_bytes'] / 1e6:.1f} MB")
             traffic[k[1]] = {"dram_bytes": rawd[k]["_bytes"]}
+            for name, key in (("Issue Slots Busy", "issue_slots_busy_pct"), ("Executed Ipc Active", "ipc_active")):
+                if name in m:
+                    try:
+                        traffic[k[1]][key] = float(m[name].split()[0].replace(",", ""))
+                    except ValueError:
+                        pass
         lines.append("")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
