@@ -834,33 +834,6 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
 }
 
 // ------------------------------------------------------------------ K3 bin --
-// Row groups of a large rectangle: pole rows (channels with cos(phi) < 0.01) take all chi
-// rays; the rest take [r_lo, r_lo + r_len).  Each group becomes chunks of <= kChunkItems
-// items (rows of <= kColMax columns).
-struct Group {
-    int row0, row1, lo, len;
-};
-__device__ __forceinline__ int make_groups(int c_from, int c_to, int r_lo, int r_len, const EmDev &E, Group g[3]) {
-    if (r_len >= E.chi) {
-        g[0] = {c_from, c_to, 0, E.chi};
-        return 1;
-    }
-    int n = 0;
-    const int a = c_from, b = min(c_to, E.pole_lo - 1);
-    if (a <= b) g[n++] = {a, b, 0, E.chi};
-    const int c = max(c_from, E.pole_lo), d = min(c_to, E.gamma - 1 - E.pole_hi);
-    if (c <= d) g[n++] = {c, d, r_lo, r_len};
-    const int e = max(c_from, E.gamma - E.pole_hi), f = c_to;
-    if (e <= f) g[n++] = {e, f, 0, E.chi};
-    return n;
-}
-__device__ __forceinline__ int group_chunks(const Group &G) {
-    const int rows = G.row1 - G.row0 + 1;
-    if (G.len > kColMax) return rows * ((G.len + kColMax - 1) / kColMax);
-    const int rpc = max(1, kChunkItems / G.len);
-    return (rows + rpc - 1) / rpc;
-}
-
 __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev &E, long long t, int row0, int nrows, int lo,
                                                    int len) {
     // capacity-overflow fallback (rare): one thread tests a whole rectangle; stats via global atomics

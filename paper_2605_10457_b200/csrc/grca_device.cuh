@@ -27,7 +27,6 @@ constexpr float kNearAxis2 = 1e-3f;            // |x_h|^2 < 1e-3 |x|^2 -> full a
 constexpr float kNearAxisLevel2 = 1e-10f;      // level frames: x_h has no cancellation (cull_pair)
 constexpr float kChordSmall2 = 4e-2f;          // chord^2 below which the L^2/8 edge pad is used
 constexpr float kTRel = 4.5e-6f;               // certified relative error of fp32 t
-constexpr int kChunkItems = 1024;              // target items per load-balanced chunk
 #ifndef GRCA_COLMAX
 #define GRCA_COLMAX 128   // K4 chain = one chunk: 128 rays = 4 steps of 32 (measured: 1024 -> 128 took K4 0.046 -> 0.031 ms at C4)
 #endif
@@ -763,13 +762,6 @@ struct Setup {
     float habs;        // |N . a0|
     float TN;          // fp32 t certified iff d.N >= TN
 };
-
-// fp64 Vol = (e1 x e2) . (v0 - o)
-__device__ __noinline__ double exact_vol(const f3 v[3], f3 o) {
-    d3 V0 = tod(v[0]);
-    d3 e1 = subd(tod(v[1]), V0), e2 = subd(tod(v[2]), V0);
-    return dotd(crossd(e1, e2), subd(V0, tod(o)));
-}
 
 // A6 setup of one (triangle, emitter) pair, computed once into the five values every kernel stores
 // or reads (so K4, the split path and the fused kernel use bit-identical thresholds):
