@@ -279,7 +279,7 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
             rb |= (r >> 2) << e;
         }
         if (NE & 1) {
-            const unsigned r = quick_cull_lut(v, emax, EL.e[NE - 1], sSin + EL.e[NE - 1].sin_base,
+            const unsigned r = quick_cull_lut<kLevel>(v, emax, EL.e[NE - 1], sSin + EL.e[NE - 1].sin_base,
                                               sLut + (NE - 1) * kLutBins);
             kb |= (r & 1u) << (NE - 1);
             rb |= (r >> 1) << (NE - 1);
@@ -287,7 +287,7 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
     } else {
 #pragma unroll
         for (int e = 0; e < NE; ++e) {
-            const unsigned r = quick_cull_lut(v, emax, EL.e[e], sSin + EL.e[e].sin_base, sLut + e * kLutBins);
+            const unsigned r = quick_cull_lut<kLevel>(v, emax, EL.e[e], sSin + EL.e[e].sin_base, sLut + e * kLutBins);
             kb |= (r & 1u) << e;
             rb |= (r >> 1) << e;
         }

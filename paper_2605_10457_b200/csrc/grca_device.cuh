@@ -676,7 +676,9 @@ __device__ __forceinline__ unsigned quick_tail_lut(const float s[3], float miw, 
     return range ? 2u : (keep ? 1u : 0u);
 }
 
-// scalar pre-test (any frame) with the fixed-kernel LUT tail; returns 1 = keep, 2 = range-culled
+// scalar pre-test (any frame) with the fixed-kernel LUT tail; returns 1 = keep, 2 = range-culled.
+// kLevel: the frame's up row is exactly (0, 0, 1), so x_u = a_z (bit for bit what the dot gives).
+template <bool kLevel = false>
 __device__ __forceinline__ unsigned quick_cull_lut(const f3 v[3], float emax, const EmLite &L, const float *sinT,
                                                    const unsigned char *lut) {
     float s[3], iw[3];
@@ -684,7 +686,7 @@ __device__ __forceinline__ unsigned quick_cull_lut(const f3 v[3], float emax, co
     for (int k = 0; k < 3; ++k) {
         const f3 a = {v[k].x - L.o[0], v[k].y - L.o[1], v[k].z - L.o[2]};
         const float w2 = a.x * a.x + a.y * a.y + a.z * a.z;
-        const float xu = L.Au[0] * a.x + L.Au[1] * a.y + L.Au[2] * a.z;
+        const float xu = kLevel ? a.z : L.Au[0] * a.x + L.Au[1] * a.y + L.Au[2] * a.z;
         iw[k] = rsqrtf(w2);
         if (L.ortho) {
             s[k] = xu * iw[k];
