@@ -252,7 +252,9 @@ struct EmLitePack {
 
 // K2 per-triangle test (A1 load + A2-A3 pre-test for all NE emitters): keep / range bit masks,
 // channel-culled count; c_area counts paper-mode apparent-area culls.
-template <int NE, bool kLevel>
+// kFast: culling on, packed pairs usable, no apparent-area cull -- the mode flags are then checked
+// once per kernel instead of per triangle (k_cull_fixed picks the instantiation)
+template <int NE, bool kLevel, bool kFast>
 __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, const float *sSin,
                                        const unsigned char *sLut, long long t, unsigned &keep, unsigned &rng,
                                        unsigned &chan, unsigned &c_area) {
@@ -267,9 +269,9 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
     const float m2 = fmaxf(l0, fmaxf(l1, l2));
     const float emax = m2 * rsqrtf(m2) * (1.f + 1e-5f);   // triangle diameter (0 if degenerate)
     unsigned kb = 0u, rb = 0u;
-    if (P.nocull) {
+    if (!kFast && P.nocull) {
         kb = (1u << NE) - 1u;
-    } else if (P.pairs_ok) {   // all frames orthonormal: packed fp32x2 path
+    } else if (kFast || P.pairs_ok) {   // all frames orthonormal: packed fp32x2 path
 #pragma unroll
         for (int e = 0; e + 1 < NE; e += 2) {
             const unsigned r = quick_pair_lut<kLevel>(v, emax, EL.p[e / 2], EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base,
@@ -293,7 +295,7 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
         }
     }
     chan = (unsigned)(NE - __popc(kb) - __popc(rb));
-    if (P.area_eps2 > 0.f) {   // NEXT-f1 paper mode (approximate): apparent-area cull
+    if (!kFast && P.area_eps2 > 0.f) {   // NEXT-f1 paper mode (approximate): apparent-area cull
         for (unsigned m = kb; m; m &= m - 1u) {
             const int e = __ffs(m) - 1;
             const f3 cen = {(v[0].x + v[1].x + v[2].x) * (1.f / 3.f), (v[0].y + v[1].y + v[2].y) * (1.f / 3.f),
@@ -308,21 +310,12 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
     rng = rb;
 }
 
-template <int NE, bool kLevel>
-__global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid_constant__ KParams P, const EmLitePack EL) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    float *sSin = reinterpret_cast<float *>(smem);
-    unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
-    __shared__ int wsum[K2_THREADS / 32];
-    __shared__ unsigned qbase;
-    __shared__ unsigned long long acc[ST_COUNT];
-    for (int i = threadIdx.x; i < P.n_sin; i += blockDim.x) sSin[i] = P.sin[i];
-    if (P.lut)
-        for (int i = threadIdx.x; i < NE * kLutBins; i += blockDim.x) sLut[i] = P.lut[i];
-    if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
-    __syncthreads();
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned c_pairs = 0, c_range = 0, c_chan = 0, c_surv = 0, c_area = 0;
+// The persistent tile loop of k_cull_fixed (one instantiation per mode, see k2_tri).
+template <int NE, bool kLevel, bool kFast>
+__device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL, const float *sSin,
+                                         const unsigned char *sLut, int *wsum, unsigned &qbase, int lane, int wib,
+                                         unsigned &c_pairs, unsigned &c_range, unsigned &c_chan, unsigned &c_surv,
+                                         unsigned &c_area) {
     const long long ntiles = (P.n_tri + K2_TILE - 1) / K2_TILE;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         // K2_TILE / K2_THREADS triangles per thread (one block scan, barrier pair and atomic for all)
@@ -334,7 +327,7 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid
             unsigned keep = 0u, rng = 0u;
             if (t < P.n_tri) {
                 unsigned chan = 0u;
-                k2_tri<NE, kLevel>(P, EL, sSin, sLut, t, keep, rng, chan, c_area);
+                k2_tri<NE, kLevel, kFast>(P, EL, sSin, sLut, t, keep, rng, chan, c_area);
                 c_pairs += NE;
                 c_chan += chan;
             }
@@ -374,6 +367,27 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid
         }
         __syncthreads();   // wsum / qbase reuse
     }
+}
+
+template <int NE, bool kLevel>
+__global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid_constant__ KParams P, const EmLitePack EL) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *sSin = reinterpret_cast<float *>(smem);
+    unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
+    __shared__ int wsum[K2_THREADS / 32];
+    __shared__ unsigned qbase;
+    __shared__ unsigned long long acc[ST_COUNT];
+    for (int i = threadIdx.x; i < P.n_sin; i += blockDim.x) sSin[i] = P.sin[i];
+    if (P.lut)
+        for (int i = threadIdx.x; i < NE * kLutBins; i += blockDim.x) sLut[i] = P.lut[i];
+    if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    unsigned c_pairs = 0, c_range = 0, c_chan = 0, c_surv = 0, c_area = 0;
+    if (!P.nocull && (P.pairs_ok || NE == 1) && !(P.area_eps2 > 0.f))
+        k2_tiles<NE, kLevel, true>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_chan, c_surv, c_area);
+    else
+        k2_tiles<NE, kLevel, false>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_chan, c_surv, c_area);
     unsigned cnt[ST_COUNT];
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0u;
