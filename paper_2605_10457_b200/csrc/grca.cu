@@ -641,6 +641,9 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KP
 // (tri << 8 | emitter, one per lane, valid lanes only): exact rectangle (cull_pair), small
 // rectangles set up and expanded over the warp (prefix scan), large ones appended to the large
 // list.  Warp-collective; slot / excl are this warp's shared-memory staging areas.
+// kFast: no debug / multicast modes (no-cull, forced fp64, all-hit counts, NVLS keys), so the per-
+// candidate checks of those flags compile away (the host launches this instantiation when they are off)
+template <bool kFast>
 __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, const float *sSin,
                                              const unsigned char *sLut, float4 *slot, int *excl,
                                              unsigned long long *wc, int smax, int lane, bool valid,
@@ -660,7 +663,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
         load_tri(P.tri, t, v);
         const EmDev &E = sE[e];
         const int st = cull_pair(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
-                                 P.nocull != 0, R);
+                                 !kFast && P.nocull != 0, R);
         if (st == CULL_KEEP) {
             // Eq. sat_cond with (gamma_T, chi_T) = (64, 64); all-CW = the arc does not wrap the seam
             const bool wraps = R.r_len >= E.chi || R.r_lo + R.r_len > E.chi || R.pole_rows;
@@ -761,7 +764,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             Q.habs = r3.w;
             Q.TN = r4.x;
             float th = 0.f;
-            int r = P.force64 ? 2 : test_fast(d, Q, EO.dmax_lo, EO.dmax_hi, th);
+            int r = (!kFast && P.force64) ? 2 : test_fast(d, Q, EO.dmax_lo, EO.dmax_hi, th);
             fb = r == 2;
             if (r == 2) {   // rare: reload the ray (keeping d live into the fp64 code spills it)
                 f3 wv[3];
@@ -771,7 +774,8 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             }
             if (r == 1) {
                 hit = true;
-                record_hit(P.hits, P.mc_hits, P.allhits, g, th, __float_as_uint(r4.y));
+                record_hit(P.hits, kFast ? nullptr : P.mc_hits, kFast ? nullptr : P.allhits, g, th,
+                           __float_as_uint(r4.y));
             }
         }
         // hit / fp64 counts: warp-uniform sums (a per-lane counter live across the loop would be
@@ -793,6 +797,7 @@ __device__ __forceinline__ unsigned atom_add_u32(unsigned *p, unsigned v) {
     return old;
 }
 
+template <bool kFast>
 __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4 *sSlot = reinterpret_cast<float4 *>(smem);   // [warp][6][32]
@@ -831,7 +836,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
         if (lane == 0) wn = atom_add_u32(P.n_surv + 2, 1u);   // next round, fetched early (latency hidden)
         const unsigned idx = w * 32u + (unsigned)lane;
         const bool valid = idx < ns;
-        refine_round(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
+        refine_round<kFast>(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
                      valid ? __ldcs(P.surv + idx) : 0ull);
         w = __shfl_sync(FULL, wn, 0);
     }
@@ -979,6 +984,7 @@ __global__ void __launch_bounds__(256, K3_MINB) k_bin(const __grid_constant__ KP
 }
 
 // ------------------------------------------------------------ K4 intersect --
+template <bool kFast>   // as refine_round
 __global__ void __launch_bounds__(K4_THREADS, K4_MINB) k_isect(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     EmDev *sE = reinterpret_cast<EmDev *>(smem);
@@ -1041,7 +1047,7 @@ __global__ void __launch_bounds__(K4_THREADS, K4_MINB) k_isect(const __grid_cons
                 dn = __ldg(P.raytab + gn);
             }
             float th = 0.f;
-            int r = P.force64 ? 2 : test_fast(d, S, E.dmax_lo, E.dmax_hi, th);
+            int r = (!kFast && P.force64) ? 2 : test_fast(d, S, E.dmax_lo, E.dmax_hi, th);
             if (r == 2) {   // rare: the vertices for the fp64 decision
                 cnt[ST_FP64]++;
                 f3 v[3];
@@ -1050,7 +1056,7 @@ __global__ void __launch_bounds__(K4_THREADS, K4_MINB) k_isect(const __grid_cons
             }
             if (r == 1) {
                 cnt[ST_HITS]++;
-                record_hit(P.hits, P.mc_hits, P.allhits, g, th, id);
+                record_hit(P.hits, kFast ? nullptr : P.mc_hits, kFast ? nullptr : P.allhits, g, th, id);
             }
         }
     }
@@ -1370,9 +1376,10 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2b_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k4s_smem_bytes(kMaxEmitters));
-    cudaFuncSetAttribute(k_refine_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kfused_smem_bytes(kMaxEmitters, kMaxSin, false));
-    cudaFuncSetAttribute(k_isect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(EmDev) * kMaxEmitters));
+    for (const void *f : {(const void *)k_refine_small<true>, (const void *)k_refine_small<false>})
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kfused_smem_bytes(kMaxEmitters, kMaxSin, false));
+    for (const void *f : {(const void *)k_isect<true>, (const void *)k_isect<false>})
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(EmDev) * kMaxEmitters));
     {   // opt-in persisting L2 window for the ray table + hits (measured: no gain at C4 after the
         // triangle streams were made evict-first, and K0/K5 lose from the carve-out)
         int max_persist = 0;
@@ -1631,9 +1638,9 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4s, k_small, K2_THREADS, h->k4s_smem));
     h->k4s_blocks_per_sm = std::max(1, b4s);
     int bf = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_refine_small, KF_THREADS, h->kf_smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_refine_small<true>, KF_THREADS, h->kf_smem));
     h->kf_blocks_per_sm = std::max(1, bf);
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_isect, K4_THREADS, sizeof(EmDev) * n_emitters));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_isect<true>, K4_THREADS, sizeof(EmDev) * n_emitters));
     h->k2_blocks_per_sm = std::max(1, b2);
     h->k2b_blocks_per_sm = std::max(1, b2b);
     h->k4_blocks_per_sm = std::max(1, b4);
@@ -1763,6 +1770,9 @@ static cudaError_t launch_l2(grca_t h, const void *fn, unsigned grid, unsigned b
 }
 
 // K2 .. K4 for the triangle source in P (events only when prof).
+// the kFast instantiations of the fused kernel and K4: no debug / multicast modes in effect
+static bool fast_modes(const KParams &P) { return !P.nocull && !P.force64 && !P.allhits && !P.mc_hits; }
+
 static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof, int slot) {
     const bool split = (h->ci.debug_flags & GRCA_DEBUG_SPLIT_REFINE) != 0;
     if (n_tri > 0) {   // K2
@@ -1790,7 +1800,8 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
             k_small<<<(unsigned)grid, K2_THREADS, h->k4s_smem, h->stream>>>(P);
         } else {
             const long long grid = (long long)h->num_sms * h->kf_blocks_per_sm;
-            CK(launch_l2(h, (const void *)k_refine_small, (unsigned)grid, KF_THREADS, h->kf_smem, P));
+            CK(launch_l2(h, fast_modes(P) ? (const void *)k_refine_small<true> : (const void *)k_refine_small<false>,
+                         (unsigned)grid, KF_THREADS, h->kf_smem, P));
         }
         CK(cudaGetLastError());
     }
@@ -1803,7 +1814,8 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
     if (prof) CK(cudaEventRecord(h->ev[slot][5], h->stream));
     if (n_tri > 0) {   // K4
         const int grid = h->num_sms * h->k4_blocks_per_sm;
-        CK(launch_l2(h, (const void *)k_isect, (unsigned)grid, K4_THREADS, sizeof(EmDev) * h->n_em, P));
+        CK(launch_l2(h, fast_modes(P) ? (const void *)k_isect<true> : (const void *)k_isect<false>, (unsigned)grid,
+                     K4_THREADS, sizeof(EmDev) * h->n_em, P));
         CK(cudaGetLastError());
     }
     return GRCA_OK;
