@@ -126,6 +126,10 @@ class Scene:
         self.ids = torch.as_tensor(np.concatenate([self.own_static, n_static + self.own_dyn]).astype(np.int32),
                                    device=device)
         self.n_tri = int(self.ids.numel())
+        # every triangle in its global order (one GPU, sensor shards): ids are the identity, so the
+        # library derives them (tri_id_base) instead of gathering an id array per survivor
+        self.identity = self.n_tri == self.n_tri_global
+        self.ids_arg = None if self.identity else self.ids
         self.n_static_local = len(self.own_static)
         self.ns3 = 3 * self.n_static_local
         static = torch.as_tensor(w["tris"][:n_static][self.own_static].reshape(-1, 3), device=device)
@@ -169,9 +173,9 @@ class Scene:
     def bind(self, g, buf, n_triangles=None):
         """Point handle g at one frame buffer (public API: grca_update_scene / grca_update_triangles)."""
         if self.indexed:
-            g.update_scene(soup=self.static_soup, mesh_xyz=buf, mesh_indices=self.idx_dyn, tri_ids=self.ids)
+            g.update_scene(soup=self.static_soup, mesh_xyz=buf, mesh_indices=self.idx_dyn, tri_ids=self.ids_arg)
         else:
-            g.update_triangles(buf, tri_ids=self.ids, n_triangles=n_triangles)
+            g.update_triangles(buf, tri_ids=self.ids_arg, n_triangles=n_triangles)
 
     def dynamic(self, frame: int):
         """Motion f.i: per-frame random pose/scale of every car instance; world
@@ -610,11 +614,16 @@ def main():
         gh.set_emitters(ems)
         ns3 = scene.fs
         st4 = scene.static_soup if scene.indexed else scene.frames[0][:ns3]   # float4 triplets
-        gh.set_static_triangles(st4, tri_ids=scene.ids[: scene.n_static_local])
-        dyn_ids = scene.ids[scene.n_static_local:]
+        if scene.identity:
+            gh.set_static_triangles(st4, tri_id_base=0)
+            dyn_ids, dyn_base = None, scene.n_static_local
+        else:
+            gh.set_static_triangles(st4, tri_ids=scene.ids[: scene.n_static_local])
+            dyn_ids, dyn_base = scene.ids[scene.n_static_local:], 0
 
         def hstep(k):
-            gh.update_triangles(scene.frames[k % N_FRAMES][ns3:], indices=scene.idx_dyn, tri_ids=dyn_ids)
+            gh.update_triangles(scene.frames[k % N_FRAMES][ns3:], indices=scene.idx_dyn, tri_ids=dyn_ids,
+                                tri_id_base=dyn_base)
             gh.cast(dist_out, tri_out)
 
         for k in range(3):
