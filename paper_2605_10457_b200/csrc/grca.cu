@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KP
 // list.  Warp-collective; slot / excl are this warp's shared-memory staging areas.
 // kFast: no debug / multicast modes (no-cull, forced fp64, all-hit counts, NVLS keys), so the per-
 // candidate checks of those flags compile away (the host launches this instantiation when they are off)
-template <bool kFast>
+template <bool kFast, bool kLevel>
 __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, const float *sSin,
                                              const unsigned char *sLut, float4 *slot, int *excl,
                                              unsigned long long *wc, int smax, int lane, bool valid,
@@ -662,8 +662,8 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
         f3 v[3];
         load_tri(P.tri, t, v);
         const EmDev &E = sE[e];
-        const int st = cull_pair(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
-                                 !kFast && P.nocull != 0, R);
+        const int st = cull_pair<kLevel>(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
+                                         !kFast && P.nocull != 0, R);
         if (st == CULL_KEEP) {
             // Eq. sat_cond with (gamma_T, chi_T) = (64, 64); all-CW = the arc does not wrap the seam
             const bool wraps = R.r_len >= E.chi || R.r_lo + R.r_len > E.chi || R.pole_rows;
@@ -797,7 +797,7 @@ __device__ __forceinline__ unsigned atom_add_u32(unsigned *p, unsigned v) {
     return old;
 }
 
-template <bool kFast>
+template <bool kFast, bool kLevel>
 __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4 *sSlot = reinterpret_cast<float4 *>(smem);   // [warp][6][32]
@@ -836,7 +836,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
         if (lane == 0) wn = atom_add_u32(P.n_surv + 2, 1u);   // next round, fetched early (latency hidden)
         const unsigned idx = w * 32u + (unsigned)lane;
         const bool valid = idx < ns;
-        refine_round<kFast>(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
+        refine_round<kFast, kLevel>(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
                      valid ? __ldcs(P.surv + idx) : 0ull);
         w = __shfl_sync(FULL, wn, 0);
     }
@@ -1167,6 +1167,7 @@ struct grca_ctx {
     float noise_sigma = 0.f;           // distance noise (K5), 0 = off
     bool all_ortho = false;
     bool all_level = false;   // every frame's up row of M^-1 is exactly (0, 0, 1)
+    bool all_dev_level = false;   // every EmDev.level (cull_pair's level instantiation)
     unsigned long long noise_seed = 0;   // persisting window over ray table + hits (num_bytes 0 = off)
     size_t k2f_smem = 0;
     int4 *d_large = nullptr;
@@ -1376,7 +1377,8 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2b_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k4s_smem_bytes(kMaxEmitters));
-    for (const void *f : {(const void *)k_refine_small<true>, (const void *)k_refine_small<false>})
+    for (const void *f : {(const void *)k_refine_small<true, true>, (const void *)k_refine_small<true, false>,
+                          (const void *)k_refine_small<false, false>})
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kfused_smem_bytes(kMaxEmitters, kMaxSin, false));
     for (const void *f : {(const void *)k_isect<true>, (const void *)k_isect<false>})
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(EmDev) * kMaxEmitters));
@@ -1603,6 +1605,8 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     h->use_lut = use_lut;
     h->all_ortho = true;
     h->all_level = true;
+    h->all_dev_level = true;
+    for (int n = 0; n < n_emitters; ++n) h->all_dev_level = h->all_dev_level && recs[n].level;
     for (int n = 0; n < n_emitters; ++n) {
         h->all_ortho = h->all_ortho && lites[n].ortho;
         h->all_level = h->all_level && lites[n].Au[0] == 0.f && lites[n].Au[1] == 0.f && lites[n].Au[2] == 1.f;
@@ -1638,7 +1642,7 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4s, k_small, K2_THREADS, h->k4s_smem));
     h->k4s_blocks_per_sm = std::max(1, b4s);
     int bf = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_refine_small<true>, KF_THREADS, h->kf_smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_refine_small<true, false>, KF_THREADS, h->kf_smem));
     h->kf_blocks_per_sm = std::max(1, bf);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_isect<true>, K4_THREADS, sizeof(EmDev) * n_emitters));
     h->k2_blocks_per_sm = std::max(1, b2);
@@ -1800,8 +1804,10 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
             k_small<<<(unsigned)grid, K2_THREADS, h->k4s_smem, h->stream>>>(P);
         } else {
             const long long grid = (long long)h->num_sms * h->kf_blocks_per_sm;
-            CK(launch_l2(h, fast_modes(P) ? (const void *)k_refine_small<true> : (const void *)k_refine_small<false>,
-                         (unsigned)grid, KF_THREADS, h->kf_smem, P));
+            const void *kf = !fast_modes(P) ? (const void *)k_refine_small<false, false>
+                             : h->all_dev_level ? (const void *)k_refine_small<true, true>
+                                                : (const void *)k_refine_small<true, false>;
+            CK(launch_l2(h, kf, (unsigned)grid, KF_THREADS, h->kf_smem, P));
         }
         CK(cudaGetLastError());
     }

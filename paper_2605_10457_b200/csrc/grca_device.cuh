@@ -257,6 +257,8 @@ __device__ __forceinline__ bool on_arc(f3 p, f3 q, f3 m, f3 T) {
 }
 
 // Conservative (channel, ray) rectangle of triangle v seen from emitter E.
+// kLevel: every emitter's frame is level (EmDev.level for all; the host picks the instantiation)
+template <bool kLevel = false>
 __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, const unsigned char *lut, bool nocull,
                          Rect &R) {
     const f3 o = {E.o[0], E.o[1], E.o[2]};
@@ -282,7 +284,7 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
     // sensor coordinates x = A a  (x = (x_f, x_r, x_u))
     f3 x[3];
     float r2[3], inv[3], s[3];
-    if (E.level) {   // level frame: the zero / unit entries of A dropped (same values up to the sign of 0)
+    if (kLevel || E.level) {   // level frame: the zero / unit entries of A dropped (same values up to the sign of 0)
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             x[k].x = E.A[0] * a[k].x + E.A[1] * a[k].y;
@@ -319,7 +321,7 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         h2[k] = x[k].x * x[k].x + x[k].y * x[k].y;
-        near_axis |= h2[k] < (E.level ? kNearAxisLevel2 : kNearAxis2) * r2[k];
+        near_axis |= h2[k] < ((kLevel || E.level) ? kNearAxisLevel2 : kNearAxis2) * r2[k];
     }
     // Fast path (most survivors: far, small triangles).  In sensor coordinates every point of T is
     // within diam of each vertex, so with rlb = max|x_k| - diam > 2 diam every chord subtends <= q =
@@ -355,7 +357,8 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
     for (int k = 0; k < 3; ++k) {
         const int k1 = (k + 1) % 3;
         float w = x[k].x * x[k1].y - x[k].y * x[k1].x;
-        float eps = E.level ? 16.f * kU * (sqrt_approx(h2[k]) * sqrt_approx(h2[k1])) : 9.f * kU * xn[k] * xn[k1];
+        float eps = (kLevel || E.level) ? 16.f * kU * (sqrt_approx(h2[k]) * sqrt_approx(h2[k1]))
+                                        : 9.f * kU * xn[k] * xn[k1];
         pos |= (w > eps);
         neg |= (w < -eps);
     }
