@@ -257,7 +257,7 @@ struct EmLitePack {
 template <int NE, bool kLevel, bool kFast>
 __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, const float *sSin,
                                        const unsigned char *sLut, long long t, unsigned &keep, unsigned &rng,
-                                       unsigned &chan, unsigned &c_area) {
+                                       unsigned &c_area) {
     f3 v[3];
     load_tri(P.tri, t, v);   // A1 (fused K1)
     const float l0 = (v[1].x - v[0].x) * (v[1].x - v[0].x) + (v[1].y - v[0].y) * (v[1].y - v[0].y) +
@@ -294,7 +294,6 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
             rb |= (r >> 1) << e;
         }
     }
-    chan = (unsigned)(NE - __popc(kb) - __popc(rb));
     if (!kFast && P.area_eps2 > 0.f) {   // NEXT-f1 paper mode (approximate): apparent-area cull
         for (unsigned m = kb; m; m &= m - 1u) {
             const int e = __ffs(m) - 1;
@@ -314,7 +313,7 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
 template <int NE, bool kLevel, bool kFast>
 __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL, const float *sSin,
                                          const unsigned char *sLut, int *wsum, unsigned &qbase, int lane, int wib,
-                                         unsigned &c_pairs, unsigned &c_range, unsigned &c_chan, unsigned &c_surv,
+                                         unsigned &c_pairs, unsigned &c_range, unsigned &c_surv,
                                          unsigned &c_area) {
     const long long ntiles = (P.n_tri + K2_TILE - 1) / K2_TILE;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -326,10 +325,8 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
             const long long t = tile * K2_TILE + h * K2_THREADS + threadIdx.x;
             unsigned keep = 0u, rng = 0u;
             if (t < P.n_tri) {
-                unsigned chan = 0u;
-                k2_tri<NE, kLevel, kFast>(P, EL, sSin, sLut, t, keep, rng, chan, c_area);
+                k2_tri<NE, kLevel, kFast>(P, EL, sSin, sLut, t, keep, rng, c_area);
                 c_pairs += NE;
-                c_chan += chan;
             }
             keeps[h] = keep;
             cntk += __popc(keep);
@@ -383,17 +380,18 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid
     if (threadIdx.x < ST_COUNT) acc[threadIdx.x] = 0ull;
     __syncthreads();
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    unsigned c_pairs = 0, c_range = 0, c_chan = 0, c_surv = 0, c_area = 0;
+    unsigned c_pairs = 0, c_range = 0, c_surv = 0, c_area = 0;
     if (!P.nocull && (P.pairs_ok || NE == 1) && !(P.area_eps2 > 0.f))
-        k2_tiles<NE, kLevel, true>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_chan, c_surv, c_area);
+        k2_tiles<NE, kLevel, true>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_surv, c_area);
     else
-        k2_tiles<NE, kLevel, false>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_chan, c_surv, c_area);
+        k2_tiles<NE, kLevel, false>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_surv, c_area);
     unsigned cnt[ST_COUNT];
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0u;
     cnt[ST_PAIRS] = c_pairs;
     cnt[ST_RANGE] = c_range;
-    cnt[ST_CHANNEL] = c_chan;
+    // every pair is kept, range-culled, area-culled or channel-culled: no per-triangle counter
+    cnt[ST_CHANNEL] = c_pairs - c_surv - c_area - c_range;
     cnt[ST_K2SURV] = c_surv;
     cnt[ST_AREA] = c_area;
     block_flush(acc, P.stats, cnt);
