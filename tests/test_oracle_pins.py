@@ -172,6 +172,17 @@ def test_ground_plane_closed_form(oracle_lib):
     np.testing.assert_allclose(res["t64"][inside], t[inside], rtol=1e-12)
     assert np.all(res["t"][:512] == np.float32(h))          # channel 0 = nadir
     assert not _hits(res)[8 * 512:].any()                     # channels 8.. have d_z >= 0
+    # a second emitter (180 deg, 0.75 m higher): its rays occupy g in [O_1, O_2) = [8192, 8192 + 12*300)
+    # and follow the same closed form with its own height (PAPER.md:760-765 global index)
+    em2 = _em(origin=(3.0, -2.0, 0.75), elev=sg.vlp16_elev()[:12], rays_per_channel=300, hfov_deg=180)
+    res2 = oracle.cast([em, em2], tris, want_t64=True)
+    D2 = oracle.ray_table([em2]).astype(np.float64)
+    with np.errstate(divide="ignore"):
+        t2 = np.where(D2[:, 2] < 0, (h + 0.75) / -D2[:, 2], np.inf)
+    assert np.array_equal(res2["t64"][:8192], res["t64"])
+    down = D2[:, 2] < 0
+    assert down.sum() > 1000 and np.array_equal(_hits(res2)[8192:], down)
+    np.testing.assert_allclose(res2["t64"][8192:][down], t2[down], rtol=1e-12)
 
 
 def test_room_box_closed_form(oracle_lib):
@@ -196,10 +207,20 @@ def test_room_box_closed_form(oracle_lib):
     # room_box face order: z-lo, z-hi, y-lo, y-hi, x-lo, x-hi (2 triangles each)
     face_idx = np.select([face_axis == 2, face_axis == 1, face_axis == 0], [0, 2, 4]) + face_hi.astype(int)
     assert np.array_equal(res["id"][clear] // 2, face_idx[clear])
-    # all-hit count = 1 away from edges (each ray leaves a closed box exactly once)
+    # all-hit count: a ray leaves a closed box exactly once, so away from face edges and from the face
+    # diagonals (where two closed triangles share the point) it hits exactly ONE triangle.
     res2 = oracle.cast([em], sg.room_box(lo, hi), want_allhits=True)
-    inner = clear & ((np.sort(np.abs(tp - t[:, None]) / t[:, None], axis=1)[:, 1]) > 1e-6)
-    assert np.all(res2["allhits"][inner] >= 1)
+    rows = np.arange(len(D))
+    P = o64[None, :] + t[:, None] * D                              # exit point (closed form)
+    ax_b = np.array([1, 0, 0])[face_axis]                         # the face's two in-plane axes
+    ax_c = np.array([2, 2, 1])[face_axis]
+    s_b = (P[rows, ax_b] - lo[ax_b]) / (hi - lo)[ax_b]            # normalised in-plane coordinates
+    s_c = (P[rows, ax_c] - lo[ax_c]) / (hi - lo)[ax_c]
+    # room_box splits every face (a, b, c, d) into (a, b, c) + (a, c, d): the diagonal is s_b == s_c
+    inner = (np.minimum.reduce([s_b, 1 - s_b, s_c, 1 - s_c]) > 1e-6) & (np.abs(s_b - s_c) > 1e-6)
+    assert inner.sum() > 0.9 * len(D)
+    assert np.all(res2["allhits"][inner] == 1)
+    assert np.all(res2["allhits"] >= 1)
 
 
 def _point_in_tri_2d(p, a, b, c):
@@ -266,6 +287,17 @@ def test_closest_and_tie_by_hand(oracle_lib):
     assert r["t"][2] == 5.0 and r["id"][2] == 3
     r = oracle.cast([em], np.array([behind], np.float32))
     assert r["id"][2] == -1 and r["id"][0] == 0 and r["t"][0] == 2.0   # ray 0 is -x
+    # t > 0 strictly -- a triangle through the origin meets every crossing ray at t = 0
+    through = np.array([[[0, -1, -1], [0, 1, -1], [0, 0, 1]]], np.float32)   # plane x = 0 contains o
+    r = oracle.cast([em], through)
+    assert np.all(r["id"] == -1)
+    # closed triangle: the ray +x meets (5, 0, 0), which lies exactly on the v1-v2 edge (u = v = 1/2,
+    # u + v = 1) of this triangle -- exact in fp64 for these integer vertices, so it must hit at t = 5
+    edge = np.array([[[5, -1, -1], [5, 1, -1], [5, -1, 1]]], np.float32)
+    ok, t, u, v, _ = oracle.mt([0, 0, 0], [1, 0, 0], *edge[0])
+    assert ok and u == 0.5 and v == 0.5
+    r = oracle.cast([em], edge)
+    assert r["id"][2] == 0 and r["t"][2] == 5.0
 
 
 def test_faces_modes(oracle_lib):
@@ -305,17 +337,28 @@ def test_sampled_rays_match_full(oracle_lib):
 
 
 def test_allhits_translation_of_closed_form(oracle_lib):
-    """Closed form for all-hit counts: a stack of k parallel quads in front of the emitter is hit
-    k times by every ray through all of them."""
-    em = _em(elev=np.array([-0.05, 0.0, 0.05], np.float32), rays_per_channel=64)
+    """Closed form for all-hit counts: quads at x = 5, 4, 3 (|y|, |z| <= 1 each) in front of the emitter.
+    A ray with slopes (y/x, z/x) = (a, b) crosses the quad at x = k iff k max(|a|, |b|) <= 1, so away from
+    the quads' borders and their shared diagonals its all-hit count is EXACTLY #{k : k max(|a|,|b|) < 1}
+    (3 inside the x = 5 cone, 1 or 2 in the rings between); behind the emitter it is 0.  The centre ray
+    (1, 0, 0) lies on all three shared diagonals: both closed triangles of each quad -> exactly 6."""
+    em = _em(elev=np.array([-0.3, -0.22, -0.1, 0.0, 0.05, 0.21, 0.3], np.float32), rays_per_channel=256)
     quads = np.concatenate([sg.quad_x5((-float(k), 0, 0)) for k in range(3)], 0)   # x = 5, 4, 3
     r = oracle.cast([em], quads, want_allhits=True, want_t64=True)
     D = oracle.ray_table([em]).astype(np.float64)
+    fwd = D[:, 0] > 0
     with np.errstate(divide="ignore", invalid="ignore"):
-        inside5 = (D[:, 0] > 0) & (np.abs(5 * D[:, 1] / D[:, 0]) < 1 - 1e-9) & (np.abs(5 * D[:, 2] / D[:, 0]) < 1 - 1e-9)
-    assert inside5.sum() > 0
-    assert np.all(r["allhits"][inside5] >= 3)
+        a, b = D[:, 1] / D[:, 0], D[:, 2] / D[:, 0]
+    m = np.maximum(np.abs(a), np.abs(b))
+    expect = np.where(fwd, sum((k * m < 1).astype(int) for k in (3, 4, 5)), 0)
+    clear = ~fwd | ((np.min([np.abs(k * m - 1) for k in (3, 4, 5)], axis=0) > 1e-9) & (np.abs(a - b) > 1e-9))
+    assert set(np.unique(expect[clear])) == {0, 1, 2, 3}
+    assert np.array_equal(r["allhits"][clear], expect[clear].astype(np.uint32))
+    inside5 = clear & (expect == 3)
     np.testing.assert_allclose(r["t64"][inside5], 3.0 / D[inside5, 0], rtol=1e-12)
+    g = 3 * 256 + 128                                              # channel phi = 0, theta = 0: d = (1, 0, 0)
+    assert np.array_equal(D[g], [1.0, 0.0, 0.0])
+    assert r["allhits"][g] == 6 and r["t"][g] == 3.0 and r["id"][g] == 4   # tie on x = 3 -> smaller id
 
 
 def test_comparator_self_and_perturbed(oracle_lib):
@@ -354,3 +397,197 @@ def test_perturbed_azimuth_table(oracle_lib):
     g2.ray_azimuth = np.array([-(8 // 2) * (math.pi / 8) + i * (math.pi / 8) for i in range(8)], np.float64).astype(np.float32)
     a, b = oracle.ray_table([grid]), oracle.ray_table([g2])
     np.testing.assert_allclose(a, b, atol=2e-7)
+
+
+# ------------------------------------------------- comparator, constructed --
+
+def _tri_with_margin(p, margin):
+    """Right triangle in the plane x = p_x whose barycentric margin min(u, v, 1-u-v) at the point p is
+    `margin` (u = margin along the +y leg, v = 0.5 along the +z leg): v0 = p - (0, 2 margin, 1), legs
+    of length 2.  p lies inside for margin > 0 (fp32 vertex rounding moves u by <= 2e-8)."""
+    v0 = np.array([p[0], p[1] - 2.0 * margin, p[2] - 1.0])
+    return np.array([[v0, v0 + [0, 2, 0], v0 + [0, 0, 2]]]).astype(np.float32)
+
+
+def _fake(ref):
+    return ref["t"].copy(), ref["id"].copy()
+
+
+def test_comparator_excusal_boundary(oracle_lib):
+    """SURVEY 8(c) comparator, excusal branch: a dropped hit is excused iff the oracle's triangle has
+    |margin| <= 1e-6 for that ray.  Constructed cases around the threshold (margins 5e-7 -> excused,
+    2e-6 and 1e-3 -> unexcused) and the exact shared-diagonal ray of quad x = 5 (margin 0 -> excused)."""
+    em = _em(elev=np.array([-0.07, 0.0, 0.09], np.float32), rays_per_channel=64)
+    D = oracle.ray_table([em]).astype(np.float64)
+    g = 2 * 64 + 33                                      # phi = 0.09, theta = dtheta: a generic ray
+    p = 5.0 * D[g] / D[g, 0]
+    for margin, excused in [(5e-7, True), (2e-6, False), (1e-3, False)]:
+        tri = _tri_with_margin(p, margin)
+        ref = oracle.cast([em], tri, want_t64=True)
+        assert ref["id"][g] == 0
+        ok, t, u, v, hit = oracle.ray_tri([em], g, tri[0])
+        assert hit and abs(min(u, v, 1 - u - v) - margin) < 0.05 * margin
+        t_g, i_g = _fake(ref)
+        t_g[g], i_g[g] = np.inf, -1                      # "GPU" drops the hit
+        rep = oracle.compare([em], tri, t_g, i_g, ref)
+        assert rep["disagree"] == 1 and rep["kinds"]["gpu_miss"] == 1
+        assert rep["excused"] == int(excused) and rep["unexcused"] == int(not excused)
+        assert not rep["passed"] or excused
+        # the mirror case: the GPU reports a hit on a triangle the oracle misses (ray just outside)
+        out = _tri_with_margin(p, -margin)
+        ref2 = oracle.cast([em], out, want_t64=True)
+        assert ref2["id"][g] == -1
+        t_g, i_g = _fake(ref2)
+        t_g[g], i_g[g] = np.float32(t), 0
+        rep = oracle.compare([em], out, t_g, i_g, ref2)
+        assert rep["kinds"]["gpu_extra"] == 1 and rep["excused"] == int(excused)
+    # the shared diagonal of quad x = 5: the centre ray (1, 0, 0) hits both closed triangles (u = 0 in T0)
+    em = sg.c1_emitter()
+    tris = sg.quad_x5(em.origin.astype(np.float64))
+    ref = oracle.cast([em], tris, want_t64=True)
+    g = 8 * 512 + 256
+    t_g, i_g = _fake(ref)
+    t_g[g], i_g[g] = np.inf, -1
+    rep = oracle.compare([em], tris, t_g, i_g, ref)
+    assert rep["excused"] == 1 and rep["unexcused"] == 0 and rep["kinds"]["gpu_miss"] == 1
+    assert not rep["passed"]                             # 8191 / 8192 = 99.988 % < 99.999 %
+    # ... while the same excused drop among 103,424 rays passes (1 - 1/103424 >= 99.999 %) and an
+    # unexcused one (a 1e-4 relative distance error) does not
+    elev = np.concatenate([np.linspace(-0.3, -0.006, 50), [0.0], np.linspace(0.006, 0.3, 50)]).astype(np.float32)
+    big = _em(origin=(0, 0, 0), elev=elev, rays_per_channel=1024)
+    tris = sg.quad_x5()
+    ref = oracle.cast([big], tris, want_t64=True)
+    g = 50 * 1024 + 512                                  # phi = 0, theta = 0: d = (1, 0, 0), the diagonal
+    assert np.array_equal(oracle.ray_table([big])[g], [1, 0, 0]) and ref["id"][g] == 0
+    t_g, i_g = _fake(ref)
+    t_g[g], i_g[g] = np.inf, -1
+    rep = oracle.compare([big], tris, t_g, i_g, ref)
+    assert rep["rays"] == 103424 and rep["excused"] == 1 and rep["passed"]
+    t_g, i_g = _fake(ref)
+    t_g[g] = np.float32(ref["t64"][g] * (1 + 1e-4))
+    rep = oracle.compare([big], tris, t_g, i_g, ref)
+    assert rep["disagree"] == 1 and rep["unexcused"] == 1 and not rep["passed"]
+
+
+def test_comparator_near_tie_and_swaps(oracle_lib):
+    """SURVEY 8(c) comparator, near-tie branch.  (a) Two identical triangles (ids 0, 1): the oracle
+    takes id 0; a GPU answer of id 1 at the same t is a near-tie (agrees).  (b) Two parallel quads 2e-4
+    apart (relative): reporting the farther id is NOT a near-tie (its fp64 t is 2e-4 > 1e-5 away) and
+    not excused.  (c) An id whose triangle the ray misses entirely: unexcused.  (d) A distance off by
+    2e-5 relative with the right id: a 'dist' disagreement, never excused."""
+    em = _em(elev=np.array([0.0, 0.05], np.float32), rays_per_channel=64)
+    q = sg.quad_x5()
+    twin = np.concatenate([q[:1], q[:1], q[1:]], 0)     # ids 0 and 1 identical, id 2 the other half
+    ref = oracle.cast([em], twin, want_t64=True)
+    hit0 = np.nonzero(ref["id"] == 0)[0]
+    assert len(hit0) >= 3
+    g = int(hit0[0])
+    t_g, i_g = _fake(ref)
+    i_g[g] = 1
+    rep = oracle.compare([em], twin, t_g, i_g, ref)
+    assert rep["passed"] and rep["near_ties"] == 1 and rep["disagree"] == 0
+    # (b) parallel quads at x = 5 and x = 5.001
+    two = np.concatenate([q, sg.quad_x5((0.001, 0, 0))], 0)  # ids 0, 1 near; 2, 3 far
+    ref = oracle.cast([em], two, want_t64=True)
+    g = int(np.nonzero(ref["id"] == 0)[0][0])
+    t_g, i_g = _fake(ref)
+    i_g[g] = 2
+    rep = oracle.compare([em], two, t_g, i_g, ref)
+    assert rep["near_ties"] == 0 and rep["kinds"]["id"] == 1 and rep["unexcused"] == 1
+    # (c) swap to a triangle behind the emitter
+    scene = np.concatenate([q, sg.seam_triangle()], 0)   # id 2 is at x = -5
+    ref = oracle.cast([em], scene, want_t64=True)
+    g = int(np.nonzero(ref["id"] == 0)[0][0])
+    t_g, i_g = _fake(ref)
+    i_g[g] = 2
+    rep = oracle.compare([em], scene, t_g, i_g, ref)
+    assert rep["near_ties"] == 0 and rep["kinds"]["id"] == 1 and rep["unexcused"] == 1
+    # (d) distance tolerance 1e-5 relative: 2e-5 fails, 5e-6 passes
+    t_g, i_g = _fake(ref)
+    t_g[g] = np.float32(ref["t64"][g] * (1 + 2e-5))
+    rep = oracle.compare([em], scene, t_g, i_g, ref)
+    assert rep["kinds"]["dist"] == 1 and rep["unexcused"] == 1
+    t_g[g] = np.float32(ref["t64"][g] * (1 + 5e-6))
+    assert oracle.compare([em], scene, t_g, i_g, ref)["passed"]
+    # (e) sentinels: a miss must carry (+inf, -1); a finite distance with id -1 is a disagreement
+    t_g, i_g = _fake(ref)
+    miss = int(np.nonzero(ref["id"] == -1)[0][0])
+    t_g[miss] = 3.0
+    rep = oracle.compare([em], scene, t_g, i_g, ref)
+    assert rep["kinds"]["sentinel"] == 1 and rep["unexcused"] == 1
+
+
+# ------------------------------------------------- grazing (north star iii) --
+
+def test_grazing_edge_planes(oracle_lib):
+    """SURVEY 8(c) hand-built (iii): rays within ~1e-7 rad of an edge plane.  A vertical edge in the
+    plane x = 5 at y = y_e is crossed by ray d at y = 5 d_y / d_x (closed form); the triangle lies on
+    the y <= y_e side, so the ray hits iff 5 d_y / d_x <= y_e.  Edges placed 5e-7 m (1e-7 rad at 5 m)
+    on either side of each aimed point: exactly the inside ones hit, at t = 5 / d_x."""
+    em = _em(elev=np.array([-0.2, 0.0, 0.13], np.float32), rays_per_channel=128)
+    D = oracle.ray_table([em]).astype(np.float64)
+    gs = [g for g in range(len(D)) if D[g, 0] > 0.9]
+    for g in gs[::7]:
+        y = 5.0 * D[g, 1] / D[g, 0]
+        z = 5.0 * D[g, 2] / D[g, 0]
+        for off in (5e-7, -5e-7):
+            ye = np.float32(y + off)
+            tri = np.array([[[5, ye, z - 2], [5, ye, z + 2], [5, ye - 3, z]]], np.float32)
+            r = oracle.cast([em], tri, rays=np.array([g]), want_t64=True)
+            inside = y <= np.float64(ye)
+            assert inside == (off > 0)
+            assert (r["id"][0] == 0) == inside, (g, off)
+            if inside:
+                assert abs(r["t64"][0] - 5.0 / D[g, 0]) <= 1e-12 * r["t64"][0]
+
+
+def test_grazing_incidence_and_flush_plane(oracle_lib):
+    """SURVEY 8(c) hand-built (iii): triangles at |cos| < 1e-3 to the ray.  Plane z - 1.5 = 2^-11 (x - 10)
+    (exact fp32 vertices), emitter at (0, 0, 1.5): every horizontal ray (phi = 0: d_z = 0 exactly) meets
+    it at x = 10, so t = 10 / d_x and it hits iff -1 <= 10 d_y / d_x <= 3 (the triangle's cross-section
+    at x = 10); |d.n| = 2^-11 / sqrt(1 + 2^-22) < 1e-3.  Then the paper's absolute plane guard
+    (PAPER.md:2471-2474 skips planes within 1e-4 m of o): a ground plane 2^-15 m below the emitter is
+    still hit by every downward ray, at t = 2^-15 / -d_z (the plain definition has no such guard)."""
+    s = 2.0 ** -11
+    tri = np.array([[[2, -1, 1.5 - 8 * s], [18, -1, 1.5 + 8 * s], [10, 3, 1.5]]], np.float32)
+    assert np.array_equal(tri.astype(np.float64), np.array([[[2, -1, 1.5 - 8 * s], [18, -1, 1.5 + 8 * s], [10, 3, 1.5]]]))
+    em = _em(origin=(0, 0, 1.5), elev=np.array([-0.4, 0.0, 0.4], np.float32), rays_per_channel=720)
+    D = oracle.ray_table([em]).astype(np.float64)
+    r = oracle.cast([em], tri, want_t64=True)
+    row = slice(720, 1440)                                   # the phi = 0 channel
+    assert np.all(D[row, 2] == 0.0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        y = 10.0 * D[row, 1] / D[row, 0]
+    fwd = D[row, 0] > 0
+    inside = fwd & (y >= -1) & (y <= 3)
+    clear = ~fwd | ((np.abs(y + 1) > 1e-9) & (np.abs(y - 3) > 1e-9))
+    assert inside.sum() > 20
+    assert np.array_equal((r["id"][row] == 0)[clear], inside[clear])
+    np.testing.assert_allclose(r["t64"][row][inside & clear], 10.0 / D[row][inside & clear, 0], rtol=1e-12)
+    ncos = s / math.sqrt(1 + s * s)
+    assert ncos < 1e-3
+    # flush plane
+    h = 2.0 ** -15
+    em2 = _em(origin=(0, 0, 1.5), elev=sg.full_sphere_elev(16), rays_per_channel=256)
+    ground = sg.ground_quad(h, half=100.0, offset=(0, 0, 1.5))
+    assert np.all(ground[..., 2] == np.float32(1.5 - h))
+    r = oracle.cast([em2], ground, want_t64=True)
+    D = oracle.ray_table([em2]).astype(np.float64)
+    down = D[:, 2] < -1e-3
+    assert np.all(r["id"][down] >= 0)
+    np.testing.assert_allclose(r["t64"][down], h / -D[down, 2], rtol=1e-9)
+    assert np.all(r["id"][D[:, 2] >= 0] == -1)
+
+
+def test_mutations_named_by_the_review_are_killed(tmp_path):
+    """tools/mutate_oracle.py on the slips that survived the round-1 pins (all-hit count before the
+    accept test, BARY_EPS = 1e9) plus the near-tie branch: each must now fail a pin.  The full list
+    (28 mutations) is run by the tool itself (profiles/r02_oracle_mutations.md)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "mutate_oracle.py"), "--out",
+                        str(tmp_path / "m.md"), "--only", "count before,BARY_EPS = 1e9,no near-tie"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "3/3 killed" in r.stdout
