@@ -963,17 +963,22 @@ __global__ void __launch_bounds__(256, K3_MINB) k_bin(const __grid_constant__ KP
             wbase = __shfl_sync(FULL, wbase, 31);
             if (!mych) continue;
             long long pos = (long long)wbase + incl - mych;
-            if (pos + mych > P.cap_chunks) {   // capacity fallback: intersect here (never dropped)
-                cnt[ST_OVF_CHUNK]++;
-                intersect_rect_serial(P, E, tri, j, 1, lo, len);
-                continue;
-            }
-            cnt[ST_CHUNKS] += mych;
-            for (int c0 = 0; c0 < len; c0 += kColMax) {
+            // every reserved slot below the capacity is written (K4 runs min(n_chunks, cap) slots, so a
+            // skipped one would replay a stale chunk); the columns past the capacity are intersected
+            // here (capacity fallback: slower, never dropped)
+            int c0 = 0;
+            for (; c0 < len && pos < P.cap_chunks; c0 += kColMax) {
                 int l0 = lo + c0;
                 if (l0 >= E.chi) l0 -= E.chi;
                 P.chunks[pos++] = make_int4((int)w, e | (j << 8), (int)(1u | ((unsigned)l0 << 16)),
                                             min(kColMax, len - c0));
+                cnt[ST_CHUNKS]++;
+            }
+            if (c0 < len) {
+                cnt[ST_OVF_CHUNK]++;
+                int l0 = lo + c0;
+                if (l0 >= E.chi) l0 -= E.chi;
+                intersect_rect_serial(P, E, tri, j, 1, l0, len - c0);
             }
         }
     }
@@ -1508,6 +1513,9 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     }
     if ((int)sins.size() > kMaxSin) return fail(h, GRCA_E_INVALID, "sum of (n_channels + 2) over emitters > 4096");
     if (offs[n_emitters] > h->ci.max_rays) return fail(h, GRCA_E_CAPACITY, "sum gamma*chi exceeds max_rays");
+    if (h->nvls_mc && offs[n_emitters] != h->n_rays)   // the bound NVLS buffer was sized for the old rays
+        return fail(h, GRCA_E_STATE, "a fused NVLS merge is bound for a different ray count: "
+                                     "grca_set_nvls(h, NULL, NULL, 0) first, then re-bind a buffer of the new size");
     // A0: the fp32 ray table, built in fp64 on the host (Eq. ray_dir)
     std::vector<float4> tab((size_t)offs[n_emitters]);
     for (int n = 0; n < n_emitters; ++n) {
@@ -1595,11 +1603,15 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
         h->surv_n_em = n_emitters;
         h->surv_cap_tiles = tiles;
     }
-    CK(cudaMemcpy(h->d_raytab, tab.data(), sizeof(float4) * tab.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->d_em, recs.data(), sizeof(EmDev) * recs.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->d_sin, sins.data(), sizeof(float) * sins.size(), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(h->d_lite, lites.data(), sizeof(EmLite) * lites.size(), cudaMemcpyHostToDevice));
-    if (use_lut) CK(cudaMemcpy(h->d_lut, lut.data(), sizeof(unsigned char) * lut.size(), cudaMemcpyHostToDevice));
+    // uploads ordered on the handle's stream (which may be a non-blocking side stream), then waited
+    // for: the next cast never reads a partially written table
+    CK(cudaMemcpyAsync(h->d_raytab, tab.data(), sizeof(float4) * tab.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_em, recs.data(), sizeof(EmDev) * recs.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_sin, sins.data(), sizeof(float) * sins.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaMemcpyAsync(h->d_lite, lites.data(), sizeof(EmLite) * lites.size(), cudaMemcpyHostToDevice, h->stream));
+    if (use_lut)
+        CK(cudaMemcpyAsync(h->d_lut, lut.data(), sizeof(unsigned char) * lut.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
     h->use_lut = use_lut;
     h->all_ortho = true;
     h->all_level = true;
@@ -1629,6 +1641,24 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     h->k2b_smem = k2b_smem_bytes(n_emitters, h->n_sin, use_lut);
     h->k4s_smem = k4s_smem_bytes(n_emitters);
     h->kf_smem = kfused_smem_bytes(n_emitters, h->n_sin, use_lut);
+    {   // dynamic shared memory of these emitters (the LUT variant can exceed what create assumed)
+        int max_optin = 0;
+        cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+        const size_t need = std::max({h->k2_smem, h->k2f_smem, h->k2b_smem, h->k4s_smem, h->kf_smem});
+        if (max_optin > 0 && need > (size_t)max_optin)
+            return fail(h, GRCA_E_INVALID, "emitter tables need " + std::to_string(need) +
+                                               " B of shared memory per block (> the device's opt-in limit)");
+        if (n_emitters <= kFixedEm && use_lut)
+            for (bool lv : {false, true})
+                CK(cudaFuncSetAttribute(k2_fixed_fn(n_emitters, lv), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)h->k2f_smem));
+        CK(cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k2_smem));
+        CK(cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k2b_smem));
+        CK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k4s_smem));
+        for (const void *f : {(const void *)k_refine_small<true, true>, (const void *)k_refine_small<true, false>,
+                              (const void *)k_refine_small<false, false>})
+            CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->kf_smem));
+    }
     int b2 = 0, b2b = 0, b4s = 0, b4 = 0;
     if (n_emitters <= kFixedEm && use_lut) {   // the fixed kernel relies on the LUT (gamma <= 255)
         const void *fn = k2_fixed_fn(n_emitters, false);

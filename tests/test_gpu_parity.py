@@ -205,6 +205,42 @@ def test_binning_and_capacity_paths(small_max, max_large):
         assert alt[2]["overflow"] == 1
 
 
+def test_capacity_fallback_across_casts():
+    """Capacity overflow must never replay stale work: one handle with a 3-entry large list (12 chunk
+    slots) casts scene A, then a different scene B and emitter set, then A again; every result equals
+    a fresh handle's (K3 writes every reserved chunk slot below the capacity and intersects the rest)."""
+    ems_a, tris_a = sg.random_scene(11, n_tris=700, n_emitters=2, gamma=16, chi=300, extent=5.0)
+    ems_b, tris_b = sg.random_scene(12, n_tris=900, n_emitters=1, gamma=24, chi=256, extent=4.0)
+    n_rays = max(sg.n_rays_total(ems_a), sg.n_rays_total(ems_b))
+    g = Grca(device=0, max_triangles=1000, max_rays=n_rays, small_max=1, max_large_items=3)
+    for ems, tris in ((ems_a, tris_a), (ems_b, tris_b), (ems_a, tris_a)):
+        fresh = run(ems, tris)
+        got = run(ems, tris, handle=g)
+        assert got[2]["overflow"] == 1
+        assert np.array_equal(fresh[1], got[1]) and np.array_equal(fresh[0].view(np.uint32), got[0].view(np.uint32))
+    g.close()
+
+
+def test_nvls_binding_blocks_ray_count_change():
+    """A bound NVLS buffer was sized for the current rays: set_emitters with another ray count is a
+    state error until the binding is dropped (no cast runs here: the views are plain device memory)."""
+    ems, tris = sg.random_scene(13, n_tris=100, n_emitters=1, gamma=8, chi=64)
+    g = Grca(device=0, max_triangles=100, max_rays=4096)
+    g.set_emitters(ems)
+    need = g.nvls_status()["bytes_needed"]
+    buf = torch.zeros(need // 8 + 32, dtype=torch.int64, device="cuda")
+    ptr = (buf.data_ptr() + 127) // 128 * 128
+    g.set_nvls(ptr, ptr, 1)
+    g.set_emitters(ems)                                   # same ray count: fine
+    bigger = [sg.Emitter(origin=(0, 0, 0), elev=sg.full_sphere_elev(8), rays_per_channel=128)]
+    with pytest.raises(GrcaError) as ei:
+        g.set_emitters(bigger)
+    assert ei.value.status == 2
+    g.set_nvls(None, None, 0)
+    g.set_emitters(bigger)
+    g.close()
+
+
 @pytest.mark.parametrize("faces", [1, 2])
 def test_face_modes(faces):
     ems, tris = sg.random_scene(21, n_tris=500, n_emitters=2)
@@ -528,10 +564,11 @@ def test_update_scene_parts_and_errors():
     assert L.grca_update_scene(h, v4.data_ptr(), n + 1, None, 0, None, 0, None, 0) == E_CAPACITY      # > max_triangles
 
 
-@pytest.mark.parametrize("n_em", [9, 17])
-def test_many_emitters_generic_paths(n_em):
-    """More emitters than the unrolled K2 handles (9: generic kernel + LUT; 17: no LUT, binary search)."""
-    ems, tris = sg.random_scene(40 + n_em, n_tris=400, n_emitters=n_em, gamma=10, chi=60, extent=7.0)
+@pytest.mark.parametrize("n_em,gamma", [(9, 10), (17, 10), (16, 192)])
+def test_many_emitters_generic_paths(n_em, gamma):
+    """More emitters than the unrolled K2 handles (9: generic kernel + LUT; 17: no LUT, binary search;
+    16 x 192 channels: the largest LUT tables, whose shared memory exceeds what create assumed)."""
+    ems, tris = sg.random_scene(40 + n_em, n_tris=400, n_emitters=n_em, gamma=gamma, chi=60, extent=7.0)
     dist, tri, st, _ = run(ems, tris)
     check(ems, tris, dist, tri)
     assert st["pairs"] == len(tris) * n_em
