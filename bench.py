@@ -7,8 +7,9 @@ One step = one LiDAR frame of BASELINE config C4 (8 LiDARs 128x4096 = 4,194,304 
 small-rectangle intersection -> K3 bin -> K4 intersect -> K5 unpack.  Inputs are resident in HBM
 (grca_update_scene: the static scenery as one float4 soup, the cars as indexed float3 meshes with
 4 posed frames cycled; every step streams 0.78 GB, > L2).  With N>1 (torchrun) the emitters are
-sharded across ranks (sensor sharding, no reduction; --shard triangles|mixed adds an NCCL
-min-merge of the packed hit keys: all-reduce, reduce-scatter or the fused NVLS path).  `e2e`
+sharded across ranks (sensor sharding, no reduction; --shard triangles|mixed adds the library's
+in-stream NCCL min-merge of the packed hit keys: all-reduce, reduce-scatter or the fused NVLS path --
+the handle owns its communicator, grca_cast is collective).  `e2e`
 repeats the measurement through the public API with the frame's car vertices copied from pinned
 host memory and the outputs copied back inside the timed region.  `--impl reference` times the
 brute-force oracle (the reference arm of this tier) on host cores.
@@ -321,16 +322,16 @@ def main():
                     "on this one GPU (sensor shards: ranks never wait on one another); see tools/emulate_ranks.py")
     ap.add_argument("--emulate-rank", type=int, default=0)
     ap.add_argument("--merge", choices=["allreduce", "reduce_scatter", "nvls"], default="allreduce",
-                    help="triangle-shard merge: NCCL all-reduce(MIN) of the packed keys, reduce-scatter(MIN) "
-                         "(each rank keeps its ray slice; half the traffic), or the fused NVLS "
-                         "multimem.red.min in the intersection kernels (NEXT-f3; needs NVLS multicast)")
+                    help="triangle-shard merge inside grca_cast: NCCL all-reduce(MIN) of the packed keys, "
+                         "reduce-scatter(MIN) (each rank keeps its ray slice; half the traffic), or the fused NVLS "
+                         "multimem.red.min into an NCCL symmetric window (NEXT-f3; needs NVLS multicast)")
+    ap.add_argument("--collective", action="store_true", help="N=1: cast through a one-rank NCCL communicator "
+                    "(the library's collective path, merge included) instead of a plain handle")
     ap.add_argument("--soup", action="store_true", help="triangle-soup scene (float4 triplets) instead of the indexed "
                     "car meshes (same triangles; the e2e upload is then every dynamic triangle's vertices)")
     ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters", "mixed"])
     ap.add_argument("--emitter-groups", type=int, default=2, help="--shard mixed: emitter groups (each split "
                     "into world / groups triangle shards merged within the group)")
-    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
-                    help="gloo only to exercise the N>1 logic with several ranks on one GPU")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -385,18 +386,12 @@ def main():
     from paper_2605_10457_b200 import dist as D
     from paper_2605_10457_b200 import grca as G
 
-    dev_index = local_rank if args.backend == "nccl" else local_rank % max(1, torch.cuda.device_count())
+    dev_index = local_rank
     if world > 1:
         torch.cuda.set_device(dev_index)
-        if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev_index}"))
-        else:
-            dist.init_process_group("gloo")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev_index}"))
     device = torch.device(f"cuda:{dev_index}")
     torch.cuda.set_device(device)
-    if args.merge == "nvls" and world > max(1, torch.cuda.device_count()):
-        # the NVLS barrier spins on flags the other ranks write: never several ranks on one GPU
-        raise SystemExit("--merge nvls needs one GPU per rank")
     # --emulate-world W --emulate-rank R: this process does exactly rank R's share of a W-rank run
     # (its shard of the scene, no process group).  Valid for sensor shards, whose ranks never wait on
     # one another; tools/emulate_ranks.py runs every rank and takes the slowest (projected frame).
@@ -412,46 +407,52 @@ def main():
     scene = Scene(args.config, s_rank, s_world, device, args.deformation, shard=shard,
                   max_range=(None if args.max_range == 0 else args.max_range), subdiv=args.subdiv, car_scale=car_scale,
                   mesh="soup" if args.soup else "indexed")
-    ems = scene.emitters
-    n_rays = sg.n_rays_total(ems)
+    # The library casts the partition itself: sensor shards pass EVERY emitter (the handle casts n mod P),
+    # triangle shards pass every emitter and their own triangles, a mixed partition passes its group's
+    # emitters and its triangle shard; grca_cast is collective and merges in-stream (NCCL).
+    ems = scene.emitters                               # the emitters this rank casts
+    ems_lib = scene.w["emitters"] if shard == "emitters" else ems
+    n_rays = sg.n_rays_total(ems_lib)                   # output layout of the handle
     n_rays_job = sg.n_rays_total(scene.w["emitters"])
-    # the timed handle is uninstrumented (what a user runs); the per-kernel breakdown comes from a
-    # second, profiled handle afterwards (CUDA events around every kernel)
     mode_flags = ((G.DEBUG_SPLIT_REFINE if args.split_refine else 0) | (G.L2_PERSIST if args.l2_persist else 0)
                   | (G.DEBUG_NO_PACKED if args.no_packed else 0))
-    g = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays, debug_flags=mode_flags,
-             small_max=args.small_max, nranks=world, rank=rank)
-    g.set_emitters(ems)
+    shard_mode = G.SHARD_EMITTERS if shard == "emitters" else G.SHARD_TRIANGLES
+    merge_mode = {"allreduce": G.MERGE_ALLREDUCE, "reduce_scatter": G.MERGE_REDUCE_SCATTER, "nvls": G.MERGE_NVLS}[args.merge]
+    coll_group, c_ranks, c_rank = None, 1, 0
+    if world > 1:
+        c_ranks, c_rank = world, rank
+        if shard.startswith("mixed"):   # one communicator per emitter group (its T triangle shards)
+            n_groups = int(shard.split(":")[1])
+            gi, ti, T = D.mixed_partition(rank, world, n_groups)
+            subs = [dist.new_group(ranks=[gg * T + t for t in range(T)]) for gg in range(n_groups)]
+            coll_group, c_ranks, c_rank = subs[gi], T, ti
+    elif args.emulate_world > 1:        # this rank's exact share, no collective (library virtual ranks)
+        c_ranks, c_rank = s_world, s_rank
+        mode_flags |= G.DEBUG_VIRTUAL_RANKS
+    collective = world > 1 or args.collective
+
+    def new_handle(flags):
+        uid = None
+        if world > 1:
+            uid = D.nccl_uid(coll_group)
+        elif args.collective:
+            uid = G.nccl_unique_id()
+        h = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays, debug_flags=flags,
+                 small_max=args.small_max, nranks=c_ranks, rank=c_rank, nccl_uid=uid, shard_mode=shard_mode,
+                 merge=merge_mode if (collective or c_ranks > 1) else G.MERGE_ALLREDUCE)
+        h.set_emitters(ems_lib)
+        return h
+
+    # the timed handle is uninstrumented (what a user runs); the per-kernel breakdown comes from a
+    # second, profiled handle afterwards (CUDA events around every kernel)
+    g = new_handle(mode_flags)
+    shard_info = g.get_shard()
+    nvls = collective and args.merge == "nvls" and shard_mode == G.SHARD_TRIANGLES
     dist_out = torch.empty(n_rays, dtype=torch.float32, device=device)
     tri_out = torch.empty(n_rays, dtype=torch.int32, device=device)
 
-    merge = world > 1 and (shard == "triangles" or shard.startswith("mixed"))
-    merge_group = None
-    if world > 1 and shard.startswith("mixed"):   # merge only within this rank's emitter group
-        n_groups = int(shard.split(":")[1])
-        _, _, T = D.mixed_partition(rank, world, n_groups)
-        subs = [dist.new_group(ranks=[gg * T + t for t in range(T)]) for gg in range(n_groups)]
-        merge_group = subs[rank // T]
-    nvls = None
-    if args.merge == "nvls" and (merge or world == 1):
-        # NEXT-f3: hits reduced in-switch by the intersection kernels (multimem.red.min); no all-reduce
-        nvls = D.NvlsBuffer(g.nvls_status()["bytes_needed"], dev_index)
-        g.set_nvls(nvls.uc_ptr, nvls.mc_ptr, world)
-        if world > 1:
-            dist.barrier()
-        merge = False
-
     def cast_once(dout=dist_out, tout=tri_out):
-        if merge and args.merge == "reduce_scatter":   # ray-sharded result: this rank's slice only
-            g.cast_packed()
-            sl, first = D.merge_packed_scatter(g.hits_packed(), group=merge_group)
-            g.unpack_range(sl, first, dout[first: first + sl.numel()], tout[first: first + sl.numel()])
-        elif merge:   # triangle shards: exact merge = all-reduce(MIN) of the packed (t, id) keys
-            g.cast_packed()
-            D.merge_packed(g.hits_packed(), group=merge_group)
-            g.unpack(dout, tout)
-        else:       # single GPU, or sensor shards (disjoint ray slices, no reduction)
-            g.cast(dout, tout)
+        g.cast(dout, tout)   # collective with a communicator: K0..K4, in-stream merge, K5
 
     def step(k):
         scene.bind(g, scene.frames[k % N_FRAMES])
@@ -481,9 +482,7 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     # per-kernel breakdown: the same casts on a profiled handle (not part of the timed region)
-    gp = Grca(device=dev_index, max_triangles=scene.n_tri, max_rays=n_rays, debug_flags=mode_flags | G.PROFILE_KERNELS,
-              small_max=args.small_max, nranks=world, rank=rank)
-    gp.set_emitters(ems)
+    gp = new_handle(mode_flags | G.PROFILE_KERNELS)
     n_last = min(max(args.steps, 8), 64)
     for k in range(n_last + 2):
         scene.bind(gp, scene.frames[k % N_FRAMES])
@@ -530,13 +529,18 @@ def main():
             dev_bufs.append(db)
         outs = [(torch.empty(n_rays, dtype=torch.float32, device=device),
                  torch.empty(n_rays, dtype=torch.int32, device=device)) for _ in range(2)]
-        r_lo, r_n = 0, n_rays                           # rays this rank reads back
-        if merge:   # the merged keys are on every rank of the merge group: each reads 1/T of them
-            m_rank, m_size = (rank % D.mixed_partition(rank, world, int(shard.split(":")[1]))[2],
-                              D.mixed_partition(rank, world, int(shard.split(":")[1]))[2]) \
-                if shard.startswith("mixed") else (rank, world)
-            rch = -(-n_rays // m_size)
-            r_lo, r_n = m_rank * rch, max(0, min(rch, n_rays - m_rank * rch))
+        # rays this rank reads back (grca_get_shard): emitter shards their emitters' slices, a reduce-scatter
+        # its merged slice, an all-reduce group 1/T of the merged rays each, one GPU everything
+        if shard_info["first_ray"] == -1:
+            ranges = [(g.offsets[m], g.offsets[m + 1] - g.offsets[m]) for m in range(len(ems_lib)) if m % c_ranks == c_rank]
+        elif shard_info["n_written"] < n_rays:
+            ranges = [(shard_info["first_ray"], shard_info["n_written"])]
+        elif c_ranks > 1:
+            rch = -(-n_rays // c_ranks)
+            ranges = [(c_rank * rch, max(0, min(rch, n_rays - c_rank * rch)))]
+        else:
+            ranges = [(0, n_rays)]
+        r_n = sum(n for _, n in ranges)
         host_out = [(torch.empty(r_n, dtype=torch.float32).pin_memory(),
                      torch.empty(r_n, dtype=torch.int32).pin_memory()) for _ in range(2)]
         cs, ds = torch.cuda.Stream(device), torch.cuda.Stream(device)
@@ -572,8 +576,11 @@ def main():
                     issue_h2d(k + 1)
                 with torch.cuda.stream(ds):
                     ds.wait_event(ev_cast[b])
-                    host_out[b][0].copy_(outs[b][0][r_lo: r_lo + r_n], non_blocking=True)
-                    host_out[b][1].copy_(outs[b][1][r_lo: r_lo + r_n], non_blocking=True)
+                    pos = 0
+                    for lo, nn in ranges:
+                        host_out[b][0][pos: pos + nn].copy_(outs[b][0][lo: lo + nn], non_blocking=True)
+                        host_out[b][1][pos: pos + nn].copy_(outs[b][1][lo: lo + nn], non_blocking=True)
+                        pos += nn
                     ev_d2h[b].record(ds)
             stream.wait_stream(cs)
             stream.wait_stream(ds)
@@ -595,7 +602,7 @@ def main():
         # the host results are the cast's (checked on the last step), and the gathered frame equals
         # the resident one
         last = (k_e2e - 1) % 2
-        assert torch.equal(host_out[last][1], outs[last][1][r_lo: r_lo + r_n].cpu())
+        assert torch.equal(host_out[last][1], torch.cat([outs[last][1][lo: lo + nn] for lo, nn in ranges]).cpu())
         fr = (k_e2e - 1) % N_FRAMES
         assert torch.equal(dev_bufs[last][ns3: ns3 + n_dyn], scene.frames[fr][ns3:])
         e2e = {"value": n_rays_job * k_e2e / (ems_e2e / 1e3), "unit": "rays/s", "ms_per_step": ems_e2e / k_e2e,
@@ -645,7 +652,7 @@ def main():
 
     # our kernels per cast (cf. the ncu launch list): K0, K2, fused K2b+K4s (split: K2b and K4s),
     # K3, K4, K5; the fused NVLS merge adds its two barrier kernels
-    launches_per_cast = 6 + (1 if args.split_refine else 0) + (2 if nvls is not None else 0)
+    launches_per_cast = 6 + (1 if args.split_refine else 0) + (2 if nvls else 0)
     # ---- per-kernel roofline (per-kernel CUDA events on the launch stream, last <= 64 steps)
     kernel_ms = {n: kms[i] for i, n in enumerate(KERNELS)}
     roof = kernel_rooflines(kernel_ms, stats, n_rays, scene.n_tri, len(ems), clk, device, split=args.split_refine,

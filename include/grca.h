@@ -42,7 +42,7 @@ typedef enum {
     GRCA_E_STATE = 2,    /* call order: cast before set_emitters / update_triangles */
     GRCA_E_CAPACITY = 3, /* counts above the capacities fixed at create */
     GRCA_E_CUDA = 4,     /* a CUDA runtime error (message has cudaGetErrorString) */
-    GRCA_E_NCCL = 5,     /* reserved for the in-library collective path */
+    GRCA_E_NCCL = 5,     /* an NCCL call of the in-library collective failed (message has the NCCL error) */
     GRCA_E_OOM = 6       /* device allocation failed at create */
 } grca_status;
 
@@ -63,16 +63,46 @@ enum {
                                        the fused refine+small kernel (A/B measurement, same results) */
     GRCA_DEBUG_NO_REFINE = 32u,     /* K3 keeps whole rectangle rows (no A7 per-channel refinement) */
     GRCA_DEBUG_NO_PACKED = 128u,    /* K2 without the packed fp32x2 (two-emitter) path (A/B) */
+    GRCA_DEBUG_VIRTUAL_RANKS = 256u, /* nranks > 1 without nccl_uid: the handle casts exactly rank's share of the
+                                        partition (shard_mode / merge as with a communicator) and writes the
+                                        outputs that rank would write, but runs no collective (the caller merges;
+                                        one-GPU tests and per-rank timing of a P-rank run) */
     GRCA_L2_PERSIST = 64u           /* opt-in: reserve persisting L2 for the ray table + hit keys
                                        (raises cudaLimitPersistingL2CacheSize device-wide and sets a
                                        per-launch access-policy window on the gather kernels) */
+};
+
+/* Multi-GPU partition of a collective cast (the paper itself is single-GPU).
+ * The per-ray closest hit is a min over triangles (a lattice), so any triangle partition merges exactly
+ * by an element-wise min of the packed (t, id) keys. */
+enum {
+    GRCA_SHARD_AUTO = 0,      /* EMITTERS when n_emitters >= nranks and nranks | n_emitters, else TRIANGLES */
+    GRCA_SHARD_TRIANGLES = 1, /* each rank passes its own triangle shard (global ids); grca_cast merges */
+    GRCA_SHARD_EMITTERS = 2   /* each rank passes every triangle; emitter n is cast by rank n mod nranks */
+};
+/* How a triangle-sharded cast merges (in-stream, between K4 and K5). */
+enum {
+    GRCA_MERGE_ALLREDUCE = 0,      /* ncclAllReduce(keys, ncclUint64, ncclMin): every rank gets every ray */
+    GRCA_MERGE_REDUCE_SCATTER = 1, /* ncclReduceScatter(ncclMin): rank r gets rays [r c, r c + c), c = ceil(n / P),
+                                      half the traffic; only that slice of the outputs is written */
+    GRCA_MERGE_NVLS = 2            /* fused: the intersection kernels record hits with multimem.red.min.u64 into
+                                      an NCCL symmetric window (ncclMemAlloc + ncclCommWindowRegister + the lsa
+                                      multimem pointer), no separate reduction (NEXT-f3); needs NVLS multicast */
 };
 
 typedef struct {
     int32_t device;          /* CUDA device ordinal */
     void *stream;            /* cudaStream_t all work is enqueued on (e.g. torch's current stream);
                                 NULL -> the legacy default stream */
-    int32_t nranks, rank;    /* informational: the caller shards triangles / emitters and merges */
+    int32_t nranks, rank;    /* collective cast over nranks processes (one GPU each); 1, 0 for one GPU */
+    const void *nccl_uid;    /* 128-byte ncclUniqueId (grca_nccl_unique_id on one rank, broadcast by the caller;
+                                the library copies it).  Non-NULL -> grca_create builds an NCCL communicator
+                                (ncclCommInitRank: every rank must call grca_create) and grca_cast is collective.
+                                Required when nranks > 1; allowed with nranks == 1 (a one-rank communicator) */
+    int32_t shard_mode;      /* GRCA_SHARD_* (used with a communicator) */
+    int32_t merge;           /* GRCA_MERGE_* (triangle shards) */
+    int32_t gather_outputs;  /* emitter shards: 1 -> ncclBroadcast every emitter's keys from its owner so every
+                                rank's outputs hold every ray; 0 -> each rank writes only its emitters' rays */
     int64_t max_triangles;   /* per handle; fixes scratch sizes so grca_cast never allocates */
     int64_t max_rays;        /* upper bound of sum_n gamma_n chi_n */
     int64_t max_large_items; /* capacity of the large-pair list (0 -> default); overflow is
@@ -84,7 +114,7 @@ typedef struct {
     float apparent_area_eps; /* NEXT-f1 paper mode, APPROXIMATE: skip a (triangle, emitter) pair when
                                 (A_T (c-o).n)^2 < eps^2 |c-o|^6 (eps_A = 1e-6 there;
                                 |.| of (c-o).n in two-sided mode).  0 -> off (exact results) */
-    int32_t reserved[6];
+    int32_t reserved[4];
 } grca_create_info;
 
 /* One spinning LiDAR (ray origin); SPEC SensorConfig. */
@@ -130,14 +160,32 @@ typedef struct {
                                 refine+small (K4s in split mode), K3 bin, K4 large, K5 unpack */
 } grca_stats;
 
-/* Create a handle bound to ci->device.  Allocates all device scratch.
- * Errors: GRCA_E_INVALID (null/negative sizes, bad faces), GRCA_E_CUDA, GRCA_E_OOM. */
+/* Create a handle bound to ci->device.  Allocates all device scratch.  With ci->nccl_uid, also the NCCL
+ * communicator of the collective cast (blocks until all ci->nranks ranks have called grca_create).
+ * Errors: GRCA_E_INVALID (null/negative sizes, bad faces / shard / merge mode, rank outside [0, nranks),
+ * nranks > 1 without nccl_uid), GRCA_E_CUDA, GRCA_E_OOM, GRCA_E_NCCL. */
 grca_status grca_create(const grca_create_info *ci, grca_t *out);
+
+/* Write a fresh 128-byte ncclUniqueId to out (host memory) for grca_create_info.nccl_uid: call on one
+ * rank, broadcast the bytes to the others (e.g. over torch.distributed).  Errors: GRCA_E_INVALID (NULL),
+ * GRCA_E_NCCL. */
+grca_status grca_nccl_unique_id(void *out);
+
+/* The partition this rank casts after grca_set_emitters: *shard_mode = GRCA_SHARD_TRIANGLES or
+ * GRCA_SHARD_EMITTERS (0 without a communicator), and the rays of the outputs grca_cast writes:
+ * [*first_ray, *first_ray + *n_written) for triangle shards (all rays, or this rank's reduce-scatter
+ * slice); for emitter shards *first_ray = -1 and *n_written = the rays of this rank's emitters (n mod
+ * nranks == rank; all rays when gather_outputs).  Any pointer may be NULL.  Errors: GRCA_E_STATE
+ * (before grca_set_emitters). */
+grca_status grca_get_shard(grca_t h, int32_t *shard_mode, int64_t *first_ray, int64_t *n_written);
 
 /* Destroy the handle and free its memory (synchronizes its stream).  NULL is a no-op. */
 grca_status grca_destroy(grca_t h);
 
-/* Set the emitters (copies everything; host arrays may be freed after return).
+/* Set the emitters (copies everything; host arrays may be freed after return).  With a communicator every
+ * rank passes the SAME full emitter list (collective under GRCA_MERGE_NVLS, which (re)binds its symmetric
+ * window here); under emitter sharding the handle casts only its own emitters (n mod nranks == rank) but
+ * keeps the global ray layout.
  * Builds the fp32 ray table in fp64 on the host (O1 above; PAPER.md:2322-2325 ray setup)
  * and uploads it with the per-emitter records and sin(phi_j) tables (synchronous).
  * Errors: GRCA_E_INVALID for n_emitters not in [1, 255], gamma/chi out of range, an
@@ -188,14 +236,17 @@ grca_status grca_set_static_triangles(grca_t h, const float *d_vertices, int64_t
 grca_status grca_clear_static(grca_t h);
 
 /* Cast one frame: K0 init -> K2 cull (+ inline small work) -> K3 bin -> K4 intersect ->
- * K5 unpack, all enqueued on the handle's stream (no allocation, no host sync unless
+ * [merge] -> K5 unpack, all enqueued on the handle's stream (no allocation, no host sync unless
  * h_stats != NULL).  d_out_dist: device float[n_rays] (+inf on a miss); d_out_tri: device
- * int32[n_rays] (-1 on a miss).  Either output may be NULL to skip K5.
- * Errors: GRCA_E_STATE (no emitters), GRCA_E_CUDA. */
+ * int32[n_rays] (-1 on a miss), n_rays = all emitters' rays (global layout).  Either output may be NULL
+ * to skip K5.  With a communicator the call is COLLECTIVE (every rank, same sequence): triangle shards
+ * merge in-stream (GRCA_MERGE_*) before K5; emitter shards cast their own emitters and optionally
+ * broadcast them (gather_outputs).  grca_get_shard says which rays of the outputs are written.
+ * Errors: GRCA_E_STATE (no emitters), GRCA_E_CUDA, GRCA_E_NCCL. */
 grca_status grca_cast(grca_t h, float *d_out_dist, int32_t *d_out_tri, grca_stats *h_stats);
 
-/* Split form for multi-rank merges: grca_cast_packed runs K0..K4 into the handle's packed
- * hit buffer (uint64 per ray: fp32 distance bits << 32 | triangle id; miss =
+/* Split form: grca_cast_packed runs K0..K4 (and, with a communicator, the merge / gather) into the
+ * handle's packed hit buffer (uint64 per ray: fp32 distance bits << 32 | triangle id; miss =
  * 0x7F800000FFFFFFFF; ordered like (t, id), positive as int64 so a signed or unsigned
  * min-allreduce merges shards exactly).  grca_hits_packed returns its device pointer.
  * grca_unpack runs K5 from that buffer (after the caller's merge). */

@@ -11,9 +11,26 @@ SRC = [os.path.join(PKG, "csrc", "grca.cu")]
 DEPS = SRC + [os.path.join(PKG, "csrc", "grca_device.cuh"), os.path.join(ROOT, "include", "grca.h")]
 LIB = os.path.join(PKG, "libgrca.so")
 
+def nccl_root() -> str:
+    """NCCL headers + library: the nvidia-nccl wheel torch itself loads (one libnccl.so.2 per process)."""
+    import importlib
+
+    try:
+        paths = list(importlib.import_module("nvidia.nccl").__path__)
+    except ImportError:
+        paths = []
+    for base in paths:
+        if os.path.exists(os.path.join(base, "include", "nccl_device.h")):
+            return base
+    raise RuntimeError("NCCL >= 2.28 headers (nvidia-nccl wheel with include/nccl_device.h) not found")
+
+
+NCCL = nccl_root()
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-ftz=true",
     "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared", "-I", os.path.join(ROOT, "include"),
+    "-I", os.path.join(NCCL, "include"), "-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2",
+    "-Xlinker", "-rpath," + os.path.join(NCCL, "lib"),
 ]
 
 

@@ -12,6 +12,8 @@
 // Cites: PAPER.md:2304-2466 (paper's GPU pipeline, prior art), SURVEY.md 8(a)/(b).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <nccl.h>
+#include <nccl_device.h>
 #include <cmath>
 #include <stdint.h>
 #include <string.h>
@@ -153,6 +155,12 @@ __global__ void k_nvls_barrier(unsigned *flag_uc, unsigned *flag_mc, unsigned ta
         __nanosleep(64);
     }
     __threadfence_system();
+}
+
+// NEXT-f3 through NCCL (GRCA_MERGE_NVLS): the multicast address of this rank's symmetric window, i.e.
+// where a multimem.red lands in every rank's copy (NCCL device API; one thread, once per binding).
+__global__ void k_sym_multimem_ptr(ncclWindow_t win, ncclDevComm dc, unsigned long long *out) {
+    out[0] = reinterpret_cast<unsigned long long>(ncclGetLsaMultimemPointer(win, 0, dc));
 }
 
 // ------------------------------------------------------- K2 cull (phase A) --
@@ -1189,6 +1197,21 @@ struct grca_ctx {
     bool st_set = false, st_dirty = false;
     unsigned long long *d_static_keys = nullptr;
     unsigned *d_static_allhits = nullptr;
+    // collective cast (grca_create_info.nccl_uid / shard_mode / merge / gather_outputs)
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    int shard = 0;                        // resolved by grca_set_emitters: 0 (no communicator) or GRCA_SHARD_*
+    int n_em_global = 0;                  // emitters of the layout (h->n_em = the ones this handle casts)
+    std::vector<int> own;                 // global indices of the emitters this handle casts
+    long long n_rays_own = 0;
+    unsigned long long *d_slice = nullptr;   // reduce-scatter receive buffer (ceil(max_rays / nranks) keys)
+    unsigned long long *d_scratch = nullptr; // 8 words: stream barrier operand, multimem pointer readback
+    // GRCA_MERGE_NVLS: this rank's NCCL symmetric window (keys + barrier flag) and its multimem view
+    void *sym_buf = nullptr;
+    size_t sym_bytes = 0;
+    ncclWindow_t sym_win = nullptr;
+    ncclDevComm sym_dc{};
+    bool sym_dc_ok = false;
     // profiling ring
     cudaEvent_t ev[kRing][kEv];
     bool ev_ok = false;
@@ -1197,6 +1220,16 @@ struct grca_ctx {
 };
 
 static std::string g_create_err;
+
+#define NK(call)                                                                        \
+    do {                                                                                \
+        ncclResult_t r_ = (call);                                                       \
+        if (r_ != ncclSuccess) {                                                        \
+            h->err = std::string(#call) + ": " + ncclGetErrorString(r_) + " (" +       \
+                     ncclGetLastError(h->comm) + ")";                                   \
+            return GRCA_E_NCCL;                                                         \
+        }                                                                               \
+    } while (0)
 
 #define CK(call)                                                                        \
     do {                                                                                \
@@ -1225,7 +1258,25 @@ grca_status fail(grca_t h, grca_status s, const std::string &m) {
     return s;
 }
 
+void sym_release(grca_t h) {   // GRCA_MERGE_NVLS window (collective with the other ranks' releases)
+    if (h->sym_win) ncclCommWindowDeregister(h->comm, h->sym_win);
+    if (h->sym_buf) ncclMemFree(h->sym_buf);
+    if (h->nvls_uc == h->sym_buf) { h->nvls_uc = h->nvls_mc = nullptr; h->nvls_n = 0; }
+    h->sym_win = nullptr;
+    h->sym_buf = nullptr;
+    h->sym_bytes = 0;
+}
+
 void free_all(grca_t h) {
+    if (h->comm) {
+        cudaStreamSynchronize(h->stream);
+        sym_release(h);
+        if (h->sym_dc_ok) ncclDevCommDestroy(h->comm, &h->sym_dc);
+        ncclCommDestroy(h->comm);
+        h->comm = nullptr;
+    }
+    cudaFree(h->d_slice);
+    cudaFree(h->d_scratch);
     cudaFree(h->d_raytab);   // (d_hits lives in the same allocation)
     cudaFree(h->d_static_keys);
     cudaFree(h->d_static_allhits);
@@ -1245,6 +1296,48 @@ void free_all(grca_t h) {
         for (int r = 0; r < kRing; ++r)
             for (int k = 0; k < kEv; ++k) cudaEventDestroy(h->ev[r][k]);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+}
+
+size_t nvls_flag_offset(long long n_rays) { return (size_t)((n_rays + 15) / 16) * 16; }   // in u64 words
+size_t sym_bytes_for(long long n_rays) { return ((nvls_flag_offset(n_rays) * 8 + 128 + 4095) / 4096) * 4096; }
+
+// GRCA_MERGE_NVLS: allocate this rank's keys + barrier flag as an NCCL symmetric window and bind it
+// as the fused merge's (unicast, multicast) pair.  Collective over the communicator (every rank calls
+// it from grca_set_emitters).  NCCL supplies the multicast object (NVLS through its own cuMem / POSIX
+// handle exchange -- no fabric handles, no IMEX channel); any failure is reported, never silent.
+grca_status sym_bind(grca_t h) {
+    CK(cudaStreamSynchronize(h->stream));
+    sym_release(h);
+    const size_t bytes = sym_bytes_for(h->n_rays);
+    NK(ncclMemAlloc(&h->sym_buf, bytes));
+    h->sym_bytes = bytes;
+    NK(ncclCommWindowRegister(h->comm, h->sym_buf, bytes, &h->sym_win, NCCL_WIN_COLL_SYMMETRIC));
+    if (!h->sym_dc_ok) {
+        ncclDevCommRequirements req = {};
+        req.lsaMultimem = true;
+        NK(ncclDevCommCreate(h->comm, &req, &h->sym_dc));
+        h->sym_dc_ok = true;
+    }
+    unsigned long long mc = 0;
+    k_sym_multimem_ptr<<<1, 1, 0, h->stream>>>(h->sym_win, h->sym_dc, h->d_scratch);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&mc, h->d_scratch, sizeof(mc), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (!mc) {
+        h->err = "NCCL gave no lsa multimem pointer (NVLS multicast unavailable on this communicator)";
+        return GRCA_E_NCCL;
+    }
+    h->nvls_uc = reinterpret_cast<unsigned long long *>(h->sym_buf);
+    h->nvls_mc = reinterpret_cast<unsigned long long *>(mc);
+    h->nvls_n = h->nranks;
+    h->nvls_epoch = 0;
+    CK(cudaMemsetAsync(h->nvls_uc + nvls_flag_offset(h->n_rays), 0, 128, h->stream));
+    CK(cudaMemsetAsync(h->d_ctrl + 7, 0, sizeof(unsigned), h->stream));
+    // every rank's flag is zero before any rank's first barrier adds to it: a one-word all-reduce as a
+    // stream barrier, then wait for it
+    NK(ncclAllReduce(h->d_scratch, h->d_scratch, 1, ncclUint64, ncclMax, h->comm, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return GRCA_OK;
 }
 
 KParams params(grca_t h) {
@@ -1324,9 +1417,19 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
         g_create_err = "invalid create info (max_rays in [1, 2^25], faces in {0,1,2}, sizes >= 0)";
         return GRCA_E_INVALID;
     }
+    const int nranks = ci->nranks < 1 ? 1 : ci->nranks;
+    if (ci->rank < 0 || ci->rank >= nranks || ci->shard_mode < 0 || ci->shard_mode > 2 || ci->merge < 0 ||
+        ci->merge > 2 || (nranks > 1 && !ci->nccl_uid && !(ci->debug_flags & GRCA_DEBUG_VIRTUAL_RANKS)) ||
+        (ci->merge == GRCA_MERGE_NVLS && !ci->nccl_uid)) {
+        g_create_err = "invalid collective setup (rank in [0, nranks), shard_mode in {0,1,2}, merge in {0,1,2}; "
+                       "nranks > 1 and GRCA_MERGE_NVLS need nccl_uid)";
+        return GRCA_E_INVALID;
+    }
     grca_t h = new grca_ctx();
     h->ci = *ci;
     h->device = ci->device;
+    h->nranks = nranks;
+    h->rank = ci->rank;
     DeviceGuard dg(h->device);
     cudaError_t e = cudaSetDevice(h->device);
     if (e != cudaSuccess) {
@@ -1347,7 +1450,8 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     };
     // ray table and hit keys in ONE allocation so a single persisting L2 access-policy window
     // covers both (the gathers of K4s/K4 hit them randomly; the triangle stream must not evict them)
-    alloc((void **)&h->d_raytab, (sizeof(float4) + sizeof(unsigned long long)) * ci->max_rays);
+    // (the keys are padded by nranks entries: a reduce-scatter merges ceil(n / P) * P keys)
+    alloc((void **)&h->d_raytab, sizeof(float4) * ci->max_rays + sizeof(unsigned long long) * (ci->max_rays + nranks));
     if (ok) h->d_hits = reinterpret_cast<unsigned long long *>(h->d_raytab + ci->max_rays);
     if (ci->debug_flags & GRCA_DEBUG_COUNT_ALL_HITS) alloc((void **)&h->d_allhits, sizeof(unsigned) * ci->max_rays);
     alloc((void **)&h->d_static_keys, sizeof(unsigned long long) * ci->max_rays);
@@ -1361,6 +1465,8 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     alloc((void **)&h->d_large_setup, sizeof(float4) * 5 * h->cap_large);
     alloc((void **)&h->d_ctrl, sizeof(unsigned) * 8);
     alloc((void **)&h->d_stats, sizeof(unsigned long long) * 32);
+    alloc((void **)&h->d_scratch, sizeof(unsigned long long) * 8);
+    if (ci->nccl_uid) alloc((void **)&h->d_slice, sizeof(unsigned long long) * ((ci->max_rays + nranks - 1) / nranks));
     if (!ok) {
         g_create_err = "device allocation failed";
         cudaGetLastError();
@@ -1411,7 +1517,31 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
         delete h;
         return GRCA_E_CUDA;
     }
+    if (ci->nccl_uid) {   // the collective cast's communicator (blocks until every rank has joined)
+        ncclUniqueId id;
+        memcpy(&id, ci->nccl_uid, sizeof(id));
+        const ncclResult_t r = ncclCommInitRank(&h->comm, nranks, id, ci->rank);
+        if (r != ncclSuccess) {
+            g_create_err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r) + " (" + ncclGetLastError(nullptr) + ")";
+            h->comm = nullptr;
+            free_all(h);
+            delete h;
+            return GRCA_E_NCCL;
+        }
+    }
     *out = h;
+    return GRCA_OK;
+}
+
+grca_status grca_nccl_unique_id(void *out) {
+    if (!out) return GRCA_E_INVALID;
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) {
+        g_create_err = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r);
+        return GRCA_E_NCCL;
+    }
+    memcpy(out, &id, sizeof(id));
     return GRCA_OK;
 }
 
@@ -1516,6 +1646,36 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     if (h->nvls_mc && offs[n_emitters] != h->n_rays)   // the bound NVLS buffer was sized for the old rays
         return fail(h, GRCA_E_STATE, "a fused NVLS merge is bound for a different ray count: "
                                      "grca_set_nvls(h, NULL, NULL, 0) first, then re-bind a buffer of the new size");
+    // partition of a collective cast: emitter shards cast emitters n mod P == rank over all
+    // triangles (disjoint output slices); triangle shards cast every emitter over the rank's triangles
+    int shard = 0;
+    if (h->comm || (h->ci.debug_flags & GRCA_DEBUG_VIRTUAL_RANKS)) {
+        shard = h->ci.shard_mode;
+        if (shard == GRCA_SHARD_AUTO)
+            shard = (n_emitters >= h->nranks && n_emitters % h->nranks == 0) ? GRCA_SHARD_EMITTERS : GRCA_SHARD_TRIANGLES;
+        if (shard == GRCA_SHARD_EMITTERS && h->ci.merge == GRCA_MERGE_NVLS)
+            return fail(h, GRCA_E_INVALID, "GRCA_MERGE_NVLS merges triangle shards: use GRCA_SHARD_TRIANGLES");
+    }
+    std::vector<int> own;
+    for (int n = 0; n < n_emitters; ++n)
+        if (shard != GRCA_SHARD_EMITTERS || n % h->nranks == h->rank) own.push_back(n);
+    const int n_own = (int)own.size();
+    {   // the emitters this handle casts: records and sin tables compacted (local index k), ray bases global
+        std::vector<EmDev> orecs;
+        std::vector<float> osins;
+        for (int n : own) {
+            EmDev D = recs[n];
+            const int sb = D.sin_base;
+            D.sin_base = (int)osins.size();
+            osins.insert(osins.end(), sins.begin() + sb, sins.begin() + sb + D.gamma + 2);
+            orecs.push_back(D);
+        }
+        recs.swap(orecs);
+        sins.swap(osins);
+        if (sins.empty()) sins.assign(2, INFINITY);
+    }
+    long long rays_own = 0;
+    for (int n : own) rays_own += offs[n + 1] - offs[n];
     // A0: the fp32 ray table, built in fp64 on the host (Eq. ray_dir)
     std::vector<float4> tab((size_t)offs[n_emitters]);
     for (int n = 0; n < n_emitters; ++n) {
@@ -1544,13 +1704,13 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
         }
     }
     // K2 phase-A records (EmLite) and the O(1) channel LUTs
-    std::vector<EmLite> lites(n_emitters);
+    std::vector<EmLite> lites(n_own);
     int max_gamma = 0;
-    for (int n = 0; n < n_emitters; ++n) max_gamma = std::max(max_gamma, (int)em[n].n_channels);
-    const bool use_lut = n_emitters <= kLutMaxEm && max_gamma <= 255;
-    std::vector<unsigned char> lut(use_lut ? (size_t)n_emitters * kLutBins : 0);
-    for (int n = 0; n < n_emitters; ++n) {
-        const grca_emitter &E = em[n];
+    for (int n : own) max_gamma = std::max(max_gamma, (int)em[n].n_channels);
+    const bool use_lut = n_own <= kLutMaxEm && max_gamma <= 255;
+    std::vector<unsigned char> lut(use_lut ? (size_t)n_own * kLutBins : 0);
+    for (int n = 0; n < n_own; ++n) {   // (n: local index of emitter own[n])
+        const grca_emitter &E = em[own[n]];
         const EmDev &D = recs[n];
         EmLite &L = lites[n];
         memset(&L, 0, sizeof(L));
@@ -1589,18 +1749,19 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     CK(cudaStreamSynchronize(h->stream));
     // survivor buffer of K2: K2_THREADS * n_em entries per tile of max_triangles
     const long long tiles = (std::max<long long>(1, h->ci.max_triangles) + K2_THREADS - 1) / K2_THREADS;
-    if (!h->d_surv || h->surv_n_em < n_emitters) {
+    if (!h->d_surv || h->surv_n_em < std::max(1, n_own)) {
         cudaFree(h->d_surv);
         cudaFree(h->d_desc);
         h->d_surv = nullptr;
         h->d_desc = nullptr;
-        if (cudaMalloc((void **)&h->d_surv, sizeof(unsigned long long) * tiles * K2_THREADS * n_emitters) != cudaSuccess ||
-            cudaMalloc((void **)&h->d_desc, sizeof(unsigned long long) * tiles * K2_THREADS * n_emitters) != cudaSuccess) {
+        const long long ne = std::max(1, n_own);
+        if (cudaMalloc((void **)&h->d_surv, sizeof(unsigned long long) * tiles * K2_THREADS * ne) != cudaSuccess ||
+            cudaMalloc((void **)&h->d_desc, sizeof(unsigned long long) * tiles * K2_THREADS * ne) != cudaSuccess) {
             cudaGetLastError();
             h->surv_n_em = 0;
             return fail(h, GRCA_E_OOM, "survivor buffer allocation failed");
         }
-        h->surv_n_em = n_emitters;
+        h->surv_n_em = (int)ne;
         h->surv_cap_tiles = tiles;
     }
     // uploads ordered on the handle's stream (which may be a non-blocking side stream), then waited
@@ -1616,31 +1777,35 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     h->all_ortho = true;
     h->all_level = true;
     h->all_dev_level = true;
-    for (int n = 0; n < n_emitters; ++n) h->all_dev_level = h->all_dev_level && recs[n].level;
-    for (int n = 0; n < n_emitters; ++n) {
+    for (int n = 0; n < n_own; ++n) h->all_dev_level = h->all_dev_level && recs[n].level;
+    for (int n = 0; n < n_own; ++n) {
         h->all_ortho = h->all_ortho && lites[n].ortho;
         h->all_level = h->all_level && lites[n].Au[0] == 0.f && lites[n].Au[1] == 0.f && lites[n].Au[2] == 1.f;
     }
-    h->n_em = n_emitters;
+    h->n_em = n_own;
+    h->n_em_global = n_emitters;
+    h->own = own;
+    h->shard = shard;
+    h->n_rays_own = rays_own;
     h->st_dirty = h->st_set;   // cached static keys depend on the emitters
     h->n_sin = (int)sins.size();
     h->n_rays = offs[n_emitters];
     h->offsets = offs;
     // dynamic smem for these emitters; occupancy of the persistent kernels
-    h->k2_smem = k2_smem_bytes(n_emitters, h->n_sin, use_lut);
+    h->k2_smem = k2_smem_bytes(n_own, h->n_sin, use_lut);
     memset(&h->lite_pack, 0, sizeof(h->lite_pack));
-    for (int n = 0; n < n_emitters && n < kFixedEm; ++n) h->lite_pack.e[n] = lites[n];
-    for (int n = 0; n + 1 < n_emitters && n + 1 < kFixedEm; n += 2) {
+    for (int n = 0; n < n_own && n < kFixedEm; ++n) h->lite_pack.e[n] = lites[n];
+    for (int n = 0; n + 1 < n_own && n + 1 < kFixedEm; n += 2) {
         EmPair &pr = h->lite_pack.p[n / 2];
         for (int c = 0; c < 3; ++c) {
             pr.no[c] = make_float2(-lites[n].o[c], -lites[n + 1].o[c]);
             pr.u[c] = make_float2(lites[n].Au[c], lites[n + 1].Au[c]);
         }
     }
-    h->k2f_smem = sizeof(float) * ((h->n_sin + 3) & ~3) + (use_lut ? (size_t)n_emitters * kLutBins : 0);
-    h->k2b_smem = k2b_smem_bytes(n_emitters, h->n_sin, use_lut);
-    h->k4s_smem = k4s_smem_bytes(n_emitters);
-    h->kf_smem = kfused_smem_bytes(n_emitters, h->n_sin, use_lut);
+    h->k2f_smem = sizeof(float) * ((h->n_sin + 3) & ~3) + (use_lut ? (size_t)n_own * kLutBins : 0);
+    h->k2b_smem = k2b_smem_bytes(n_own, h->n_sin, use_lut);
+    h->k4s_smem = k4s_smem_bytes(n_own);
+    h->kf_smem = kfused_smem_bytes(n_own, h->n_sin, use_lut);
     {   // dynamic shared memory of these emitters (the LUT variant can exceed what create assumed)
         int max_optin = 0;
         cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
@@ -1648,9 +1813,9 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
         if (max_optin > 0 && need > (size_t)max_optin)
             return fail(h, GRCA_E_INVALID, "emitter tables need " + std::to_string(need) +
                                                " B of shared memory per block (> the device's opt-in limit)");
-        if (n_emitters <= kFixedEm && use_lut)
+        if (n_own >= 1 && n_own <= kFixedEm && use_lut)
             for (bool lv : {false, true})
-                CK(cudaFuncSetAttribute(k2_fixed_fn(n_emitters, lv), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                CK(cudaFuncSetAttribute(k2_fixed_fn(n_own, lv), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)h->k2f_smem));
         CK(cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k2_smem));
         CK(cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k2b_smem));
@@ -1660,8 +1825,8 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
             CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->kf_smem));
     }
     int b2 = 0, b2b = 0, b4s = 0, b4 = 0;
-    if (n_emitters <= kFixedEm && use_lut) {   // the fixed kernel relies on the LUT (gamma <= 255)
-        const void *fn = k2_fixed_fn(n_emitters, false);
+    if (n_own >= 1 && n_own <= kFixedEm && use_lut) {   // the fixed kernel relies on the LUT (gamma <= 255)
+        const void *fn = k2_fixed_fn(n_own, false);
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, fn, K2_THREADS, h->k2f_smem));
     } else {
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_cull, K2_THREADS, h->k2_smem));
@@ -1672,10 +1837,12 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     int bf = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_refine_small<true, false>, KF_THREADS, h->kf_smem));
     h->kf_blocks_per_sm = std::max(1, bf);
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_isect<true>, K4_THREADS, sizeof(EmDev) * n_emitters));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_isect<true>, K4_THREADS, sizeof(EmDev) * std::max(1, n_own)));
     h->k2_blocks_per_sm = std::max(1, b2);
     h->k2b_blocks_per_sm = std::max(1, b2b);
     h->k4_blocks_per_sm = std::max(1, b4);
+    if (h->comm && h->ci.merge == GRCA_MERGE_NVLS && (!h->sym_buf || h->sym_bytes != sym_bytes_for(h->n_rays)))
+        return sym_bind(h);   // collective: every rank re-binds its symmetric window for the new ray count
     return GRCA_OK;
 }
 
@@ -1805,6 +1972,11 @@ static cudaError_t launch_l2(grca_t h, const void *fn, unsigned grid, unsigned b
 // the kFast instantiations of the fused kernel and K4: no debug / multicast modes in effect
 static bool fast_modes(const KParams &P) { return !P.nocull && !P.force64 && !P.allhits && !P.mc_hits; }
 
+static bool rs_merge(grca_t h) {   // (also in GRCA_DEBUG_VIRTUAL_RANKS: the slice this rank would own)
+    return h->shard == GRCA_SHARD_TRIANGLES && h->ci.merge == GRCA_MERGE_REDUCE_SCATTER;
+}
+static long long rs_chunk(grca_t h) { return (h->n_rays + h->nranks - 1) / h->nranks; }
+
 static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof, int slot) {
     const bool split = (h->ci.debug_flags & GRCA_DEBUG_SPLIT_REFINE) != 0;
     if (n_tri > 0) {   // K2
@@ -1855,7 +2027,6 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
     return GRCA_OK;
 }
 
-static size_t nvls_flag_offset(long long n_rays) { return (size_t)((n_rays + 15) / 16) * 16; }   // in u64 words
 
 static cudaError_t nvls_barrier(grca_t h) {
     ++h->nvls_epoch;
@@ -1867,7 +2038,7 @@ static cudaError_t nvls_barrier(grca_t h) {
 }
 
 static grca_status launch_packed(grca_t h) {
-    if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
+    if (h->n_em_global < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
     if (!h->have_tri && !h->st_set) return fail(h, GRCA_E_STATE, "grca_update_triangles has not been called");
     if (h->nvls_mc && h->st_set)
         return fail(h, GRCA_E_STATE, "the fused NVLS merge cannot be combined with cached static triangles");
@@ -1892,22 +2063,52 @@ static grca_status launch_packed(grca_t h) {
         h->st_dirty = false;
     }
     if (prof) CK(cudaEventRecord(h->ev[slot][0], h->stream));
-    {   // K0
+    {   // K0 (a reduce-scatter merges ceil(n / P) * P keys: the padding starts as MISS too)
         const int grid = h->num_sms * 8;   // full occupancy: stores in flight for HBM bandwidth
-        k_init<<<grid, 256, 0, h->stream>>>(P.hits, P.allhits, h->n_rays, h->d_ctrl, h->d_stats,
+        const long long n_init = rs_merge(h) ? rs_chunk(h) * h->nranks : h->n_rays;
+        k_init<<<grid, 256, 0, h->stream>>>(P.hits, P.allhits, h->st_set ? h->n_rays : n_init, h->d_ctrl, h->d_stats,
                                             h->st_set ? h->d_static_keys : nullptr,
                                             (h->st_set && P.allhits) ? h->d_static_allhits : nullptr);
         CK(cudaGetLastError());
+        if (h->st_set && n_init > h->n_rays)
+            k_init<<<1, 256, 0, h->stream>>>(P.hits + h->n_rays, nullptr, n_init - h->n_rays, h->d_ctrl, h->d_stats,
+                                             nullptr, nullptr);
     }
     // NVLS: no rank may reduce into a peer's copy before the peer has initialised it
     if (h->nvls_mc) CK(nvls_barrier(h));
     if (prof) CK(cudaEventRecord(h->ev[slot][1], h->stream));
-    if (!h->have_tri) P.n_tri = 0;
+    if (!h->have_tri || h->n_em == 0) P.n_tri = 0;
     grca_status st = launch_core(h, P, P.n_tri, prof, slot);
     if (st != GRCA_OK) return st;
     // NVLS: every rank's reductions have landed in every copy before anyone unpacks
     if (h->nvls_mc) CK(nvls_barrier(h));
     if (prof) CK(cudaEventRecord(h->ev[slot][6], h->stream));
+    // the collective step, in-stream between K4 and K5
+    if (h->comm && h->shard == GRCA_SHARD_TRIANGLES && !h->nvls_mc) {
+        if (rs_merge(h))   // rank r receives the min over ranks of keys [r c, r c + c)
+            NK(ncclReduceScatter(P.hits, h->d_slice, (size_t)rs_chunk(h), ncclUint64, ncclMin, h->comm, h->stream));
+        else               // packed keys are ordered like (t, id): an unsigned min merges shards exactly
+            NK(ncclAllReduce(P.hits, P.hits, (size_t)h->n_rays, ncclUint64, ncclMin, h->comm, h->stream));
+    }
+    if (h->comm && h->shard == GRCA_SHARD_EMITTERS && h->ci.gather_outputs) {
+        NK(ncclGroupStart());   // every emitter's keys from its owner (rank m mod P) to every rank
+        for (int m = 0; m < h->n_em_global; ++m) {
+            const long long o = h->offsets[m], c = h->offsets[m + 1] - o;
+            NK(ncclBroadcast(P.hits + o, P.hits + o, (size_t)c, ncclUint64, m % h->nranks, h->comm, h->stream));
+        }
+        NK(ncclGroupEnd());
+    }
+    return GRCA_OK;
+}
+
+// K5 over global rays [first, first + n): keys[0..n) -> dist[0..n) / tri[0..n)
+static grca_status k5(grca_t h, const unsigned long long *keys, float *dist, int32_t *tri, long long n, long long first) {
+    if ((dist || tri) && n > 0) {
+        const long long blocks = std::min<long long>((n + 255) / 256, (long long)h->num_sms * 8);
+        k_unpack<<<(unsigned)std::max<long long>(1, blocks), 256, 0, h->stream>>>(
+            keys, dist, tri, n, first, h->noise_sigma, h->noise_seed, (unsigned long long)h->n_casts);
+        CK(cudaGetLastError());
+    }
     return GRCA_OK;
 }
 
@@ -1915,14 +2116,26 @@ static grca_status launch_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri
                                  const unsigned long long *keys = nullptr, long long first = 0, long long n = -1) {
     DeviceGuard dg(h->device);
     const int slot = (int)(h->n_casts % kRing);
-    if (!keys) keys = (h->nvls_uc ? h->nvls_uc : h->d_hits) + first;
-    if (n < 0) n = h->n_rays;
-    if ((d_out_dist || d_out_tri) && n > 0) {
-        const long long blocks = std::min<long long>((n + 255) / 256, (long long)h->num_sms * 8);
-        k_unpack<<<(unsigned)std::max<long long>(1, blocks), 256, 0, h->stream>>>(
-            keys, d_out_dist, d_out_tri, n, first, h->noise_sigma, h->noise_seed, (unsigned long long)h->n_casts);
-        CK(cudaGetLastError());
+    const unsigned long long *own_keys = h->nvls_uc ? h->nvls_uc : h->d_hits;
+    grca_status st = GRCA_OK;
+    if (keys) {   // grca_unpack_range: caller's keys, slice-local outputs
+        st = k5(h, keys, d_out_dist, d_out_tri, n, first);
+    } else if (n >= 0) {   // grca_unpack_range on the handle's own keys
+        st = k5(h, own_keys + first, d_out_dist, d_out_tri, n, first);
+    } else if (rs_merge(h)) {   // this rank's merged slice (virtual ranks: its unmerged keys of the slice)
+        const long long c = rs_chunk(h), f = (long long)h->rank * c, m = std::max(0ll, std::min(c, h->n_rays - f));
+        st = k5(h, h->comm ? h->d_slice : own_keys + f, d_out_dist ? d_out_dist + f : nullptr,
+                d_out_tri ? d_out_tri + f : nullptr, m, f);
+    } else if (h->shard == GRCA_SHARD_EMITTERS && !h->ci.gather_outputs) {   // own emitters only
+        for (int m : h->own) {
+            const long long o = h->offsets[m], c = h->offsets[m + 1] - o;
+            st = k5(h, own_keys + o, d_out_dist ? d_out_dist + o : nullptr, d_out_tri ? d_out_tri + o : nullptr, c, o);
+            if (st != GRCA_OK) break;
+        }
+    } else {
+        st = k5(h, own_keys, d_out_dist, d_out_tri, h->n_rays, 0);
     }
+    if (st != GRCA_OK) return st;
     if (h->ev_ok) CK(cudaEventRecord(h->ev[slot][7], h->stream));
     return GRCA_OK;
 }
@@ -1942,7 +2155,7 @@ static grca_status fill_stats(grca_t h, grca_stats *s) {
     s->large_pairs = (int64_t)st[ST_LARGE];
     s->chunks = (int64_t)st[ST_CHUNKS];
     s->rtic_tested = (int64_t)(st[ST_ITEMS_SMALL] + st[ST_ITEMS_LARGE]);
-    s->rtic_brute = (int64_t)(h->n_rays * ((h->have_tri ? h->n_tri : 0) + (h->st_set ? h->st_n : 0)));
+    s->rtic_brute = (int64_t)(h->n_rays_own * ((h->have_tri ? h->n_tri : 0) + (h->st_set ? h->st_n : 0)));
     s->fp64_fallbacks = (int64_t)st[ST_FP64];
     s->hits_recorded = (int64_t)st[ST_HITS];
     s->overflow_inline = (int64_t)(st[ST_OVF_LARGE] + st[ST_OVF_CHUNK]);
@@ -1973,7 +2186,7 @@ grca_status grca_cast_packed(grca_t h) {
 
 grca_status grca_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri) {
     if (!h) return GRCA_E_INVALID;
-    if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
+    if (h->n_em_global < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
     grca_status s = launch_unpack(h, d_out_dist, d_out_tri);
     ++h->n_casts;
     return s;
@@ -1982,7 +2195,7 @@ grca_status grca_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri) {
 grca_status grca_unpack_range(grca_t h, const uint64_t *d_keys, int64_t first_ray, int64_t n, float *d_out_dist,
                               int32_t *d_out_tri) {
     if (!h) return GRCA_E_INVALID;
-    if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
+    if (h->n_em_global < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
     if (first_ray < 0 || n < 0 || first_ray + n > h->n_rays)
         return fail(h, GRCA_E_INVALID, "ray range outside [0, n_rays)");
     grca_status s = launch_unpack(h, d_out_dist, d_out_tri, reinterpret_cast<const unsigned long long *>(d_keys),
@@ -2011,6 +2224,7 @@ grca_status grca_hits_packed(grca_t h, uint64_t **d_hits, int64_t *n_rays) {
 
 grca_status grca_set_nvls(grca_t h, void *d_uc, void *d_mc, int32_t n_ranks) {
     if (!h) return GRCA_E_INVALID;
+    if (h->sym_buf) return fail(h, GRCA_E_STATE, "the handle's GRCA_MERGE_NVLS window is bound (owned by the library)");
     if (!d_uc && !d_mc) {   // back to the handle's own buffer and local RED.MIN
         h->nvls_uc = h->nvls_mc = nullptr;
         h->nvls_n = 0;
@@ -2018,7 +2232,7 @@ grca_status grca_set_nvls(grca_t h, void *d_uc, void *d_mc, int32_t n_ranks) {
     }
     if (!d_uc || !d_mc || n_ranks < 1) return fail(h, GRCA_E_INVALID, "need both views and n_ranks >= 1");
     if ((((uintptr_t)d_uc) | ((uintptr_t)d_mc)) & 127) return fail(h, GRCA_E_INVALID, "views must be 128-byte aligned");
-    if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters first (the buffer holds one key per ray)");
+    if (h->n_em_global < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters first (the buffer holds one key per ray)");
     if (h->ci.debug_flags & GRCA_DEBUG_COUNT_ALL_HITS)
         return fail(h, GRCA_E_STATE, "all-hit counting is per rank: not available with the fused NVLS merge");
     DeviceGuard dg(h->device);
@@ -2106,16 +2320,34 @@ grca_status grca_debug_fast_atan2(const float *h_y, const float *h_x, float *h_o
 
 grca_status grca_get_layout(grca_t h, int64_t *n_rays_total, int64_t *ray_offsets) {
     if (!h) return GRCA_E_INVALID;
-    if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
+    if (h->n_em_global < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
     if (n_rays_total) *n_rays_total = h->n_rays;
     if (ray_offsets)
-        for (int n = 0; n <= h->n_em; ++n) ray_offsets[n] = h->offsets[n];
+        for (int n = 0; n <= h->n_em_global; ++n) ray_offsets[n] = h->offsets[n];
+    return GRCA_OK;
+}
+
+grca_status grca_get_shard(grca_t h, int32_t *shard_mode, int64_t *first_ray, int64_t *n_written) {
+    if (!h) return GRCA_E_INVALID;
+    if (h->n_em_global < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
+    long long first = 0, n = h->n_rays;
+    if (rs_merge(h)) {
+        const long long c = rs_chunk(h);
+        first = (long long)h->rank * c;
+        n = std::max(0ll, std::min(c, h->n_rays - first));
+    } else if (h->shard == GRCA_SHARD_EMITTERS && !h->ci.gather_outputs) {
+        first = -1;
+        n = h->n_rays_own;
+    }
+    if (shard_mode) *shard_mode = h->shard;
+    if (first_ray) *first_ray = first;
+    if (n_written) *n_written = n;
     return GRCA_OK;
 }
 
 grca_status grca_debug_ray_table(grca_t h, float *h_xyz) {
     if (!h || !h_xyz) return GRCA_E_INVALID;
-    if (h->n_em < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
+    if (h->n_em_global < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
     DeviceGuard dg(h->device);
     std::vector<float4> tab((size_t)h->n_rays);
     CK(cudaStreamSynchronize(h->stream));

@@ -21,13 +21,16 @@ DEBUG_COUNT_ALL_HITS, DEBUG_NO_CULL, PROFILE_KERNELS, DEBUG_FORCE_FP64, DEBUG_SP
     1, 2, 4, 8, 16, 32)
 L2_PERSIST = 64
 DEBUG_NO_PACKED = 128
+DEBUG_VIRTUAL_RANKS = 256
+SHARD_AUTO, SHARD_TRIANGLES, SHARD_EMITTERS = 0, 1, 2
+MERGE_ALLREDUCE, MERGE_REDUCE_SCATTER, MERGE_NVLS = 0, 1, 2
 
 EXPORTS = [
     "grca_create", "grca_destroy", "grca_set_emitters", "grca_update_triangles", "grca_cast",
     "grca_cast_packed", "grca_hits_packed", "grca_set_static_triangles", "grca_clear_static", "grca_unpack", "grca_get_stats", "grca_kernel_times", "grca_set_distance_noise",
     "grca_debug_all_hits", "grca_debug_large_list", "grca_debug_fast_atan2", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
     "grca_set_nvls", "grca_nvls_status", "grca_update_triangles_f3", "grca_update_scene",
-    "grca_unpack_range",
+    "grca_unpack_range", "grca_nccl_unique_id", "grca_get_shard",
 ]
 
 
@@ -40,9 +43,10 @@ class GrcaError(RuntimeError):
 class CreateInfo(C.Structure):
     _fields_ = [
         ("device", C.c_int32), ("stream", C.c_void_p), ("nranks", C.c_int32), ("rank", C.c_int32),
+        ("nccl_uid", C.c_void_p), ("shard_mode", C.c_int32), ("merge", C.c_int32), ("gather_outputs", C.c_int32),
         ("max_triangles", C.c_int64), ("max_rays", C.c_int64), ("max_large_items", C.c_int64),
         ("faces", C.c_int32), ("debug_flags", C.c_uint32), ("small_max", C.c_int32),
-        ("apparent_area_eps", C.c_float), ("reserved", C.c_int32 * 6),
+        ("apparent_area_eps", C.c_float), ("reserved", C.c_int32 * 4),
     ]
 
 
@@ -105,6 +109,8 @@ def load(path: str = LIB_PATH):
         "grca_set_nvls": ([vp, vp, vp, i32], C.c_int),
         "grca_nvls_status": ([vp, C.POINTER(i64), C.POINTER(i32)], C.c_int),
         "grca_last_error": ([vp], C.c_char_p),
+        "grca_nccl_unique_id": ([vp], C.c_int),
+        "grca_get_shard": ([vp, C.POINTER(i32), C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "grca_version": ([], C.c_char_p),
     }
     for name, (args, res) in sig.items():
@@ -117,6 +123,15 @@ def load(path: str = LIB_PATH):
 
 def version() -> str:
     return load().grca_version().decode()
+
+
+def nccl_unique_id() -> bytes:
+    """grca_nccl_unique_id: 128 bytes for Grca(nccl_uid=...) (create on one rank, broadcast to the rest)."""
+    buf = C.create_string_buffer(128)
+    st = load().grca_nccl_unique_id(buf)
+    if st != GRCA_OK:
+        raise GrcaError(st, load().grca_last_error(None).decode())
+    return buf.raw
 
 
 def debug_fast_atan2(y, x):
@@ -174,7 +189,8 @@ class Grca:
 
     def __init__(self, device: int = 0, stream=None, max_triangles: int = 1 << 20, max_rays: int = 1 << 20,
                  max_large_items: int = 0, faces: int = 0, debug_flags: int = 0, small_max: int = 0,
-                 nranks: int = 1, rank: int = 0, apparent_area_eps: float = 0.0):
+                 nranks: int = 1, rank: int = 0, apparent_area_eps: float = 0.0, nccl_uid: Optional[bytes] = None,
+                 shard_mode: int = SHARD_AUTO, merge: int = MERGE_ALLREDUCE, gather_outputs: bool = False):
         import torch
 
         L = load()
@@ -190,6 +206,12 @@ class Grca:
         ci.max_triangles, ci.max_rays, ci.max_large_items = int(max_triangles), int(max_rays), int(max_large_items)
         ci.faces, ci.debug_flags, ci.small_max = int(faces), int(debug_flags), int(small_max)
         ci.apparent_area_eps = float(apparent_area_eps)
+        uid = None
+        if nccl_uid is not None:
+            assert len(nccl_uid) == 128
+            uid = C.create_string_buffer(bytes(nccl_uid), 128)
+            ci.nccl_uid = C.cast(uid, C.c_void_p)
+        ci.shard_mode, ci.merge, ci.gather_outputs = int(shard_mode), int(merge), int(bool(gather_outputs))
         h = C.c_void_p()
         st = L.grca_create(C.byref(ci), C.byref(h))
         if st != GRCA_OK:
@@ -275,10 +297,17 @@ class Grca:
         self.n_triangles = ns + nm
         return self
 
-    # -- grca_set_nvls / grca_nvls_status (NEXT-f3 fused NVLS merge; plumbing in dist.NvlsBuffer)
+    # -- grca_set_nvls / grca_nvls_status (NEXT-f3 fused NVLS merge on caller-bound buffers; the library binds
+    #    its own NCCL symmetric window under merge=MERGE_NVLS)
     def set_nvls(self, uc_ptr, mc_ptr, n_ranks: int):
         self._check(self._L.grca_set_nvls(self._h, C.c_void_p(uc_ptr or None), C.c_void_p(mc_ptr or None),
                                           int(n_ranks)))
+
+    def get_shard(self) -> dict:
+        """grca_get_shard: the partition this rank casts and the output rays a cast writes."""
+        mode, first, n = C.c_int32(), C.c_int64(), C.c_int64()
+        self._check(self._L.grca_get_shard(self._h, C.byref(mode), C.byref(first), C.byref(n)))
+        return {"shard_mode": mode.value, "first_ray": first.value, "n_written": n.value}
 
     def nvls_status(self) -> dict:
         need, to = C.c_int64(), C.c_int32()

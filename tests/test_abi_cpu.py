@@ -117,3 +117,24 @@ def test_fast_atan2_error_bound(lib):
     err = np.abs(got - ref)
     err = np.minimum(err, 2 * np.pi - err)   # +-pi are the same azimuth
     assert err.max() <= 2.0e-6, err.max()
+
+
+def test_collective_setup_host_side(lib):
+    """grca_nccl_unique_id needs no GPU (128 fresh bytes per call); invalid collective setups are rejected
+    before any device work: nranks > 1 without an id, a rank outside [0, nranks), bad shard / merge."""
+    import ctypes as C
+
+    from paper_2605_10457_b200 import grca
+
+    a, b = grca.nccl_unique_id(), grca.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
+    uid = C.create_string_buffer(a, 128)
+    for kw in ({"nranks": 2}, {"nranks": 2, "rank": 2, "nccl_uid": uid}, {"nranks": 1, "rank": -1},
+               {"nccl_uid": uid, "shard_mode": 3}, {"nccl_uid": uid, "merge": 5}, {"merge": grca.MERGE_NVLS}):
+        ci = grca.CreateInfo()
+        ci.max_triangles, ci.max_rays, ci.nranks = 10, 10, 1
+        for k, v in kw.items():
+            setattr(ci, k, C.cast(v, C.c_void_p) if k == "nccl_uid" else v)
+        h = C.c_void_p()
+        assert lib.grca_create(C.byref(ci), C.byref(h)) == grca.GRCA_E_INVALID, kw
+        assert b"collective" in lib.grca_last_error(None)

@@ -1,6 +1,10 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): triangle sharding + min-merge and sensor
-sharding + gather reproduce the single-rank result exactly.  The per-shard hit buffers come from
-the oracle (CPU), packed as (fp32 t bits << 32 | id) exactly like the library's K4 output."""
+"""Multi-rank host logic on CPU (gloo, world sizes 2-4): the partitions of paper_2605_10457_b200.dist
+and the library's collective steps reproduce the single-rank result exactly.  The per-shard hit
+buffers come from the oracle (CPU), packed as (fp32 t bits << 32 | id) exactly like the library's K4
+output; the library's in-stream NCCL steps (grca.cu launch_packed: ncclAllReduce / ncclReduceScatter
+with ncclMin on uint64, one ncclBroadcast per emitter from rank n mod P) are modelled with the same
+gloo collectives on int64 views (the keys are positive as int64, so a signed min is the unsigned
+min).  The NCCL calls themselves run on the GPU (tests/test_gpu_parity.py, one-rank communicator)."""
 import os
 import socket
 
@@ -13,6 +17,35 @@ import torch.multiprocessing as mp
 import oracle
 import scenegen as sg
 from paper_2605_10457_b200 import dist as D
+
+
+# ---- models of the library's collective steps (same operation, gloo instead of NCCL) --------------
+def merge_packed(hits, group=None):
+    """GRCA_MERGE_ALLREDUCE: in-place all-reduce(MIN) of the packed keys."""
+    dist.all_reduce(hits, op=dist.ReduceOp.MIN, group=group)
+    return hits
+
+
+def merge_packed_scatter(hits, group=None):
+    """GRCA_MERGE_REDUCE_SCATTER: rank r keeps the min over ranks of rays [r c, r c + c), c = ceil(n / P);
+    the keys are padded with MISS to c P (grca.cu K0 initialises the padding)."""
+    P, r = dist.get_world_size(group), dist.get_rank(group)
+    n = hits.numel()
+    c = -(-n // P)
+    src = torch.cat([hits, torch.full((c * P - n,), D.MISS_KEY, dtype=hits.dtype)])
+    dist.all_reduce(src, op=dist.ReduceOp.MIN, group=group)
+    first = r * c
+    return src[first: first + max(0, min(c, n - first))].clone(), first
+
+
+def gather_emitters(keys, offsets, world):
+    """gather_outputs under emitter sharding: every emitter's keys broadcast from its owner n mod P."""
+    for n in range(len(offsets) - 1):
+        a, b = int(offsets[n]), int(offsets[n + 1])
+        seg = keys[a:b].clone()
+        dist.broadcast(seg, src=n % world)
+        keys[a:b] = seg
+    return keys
 
 
 def _packed(res):
@@ -39,15 +72,23 @@ def _worker(rank, world, port, q):
         own = D.shard_triangles(len(tris), rank, world, block=512)
         res = oracle.cast(ems, tris[own], ids=own.astype(np.int32), threads=2)
         hits = torch.as_tensor(_packed(res))
-        D.merge_packed(hits)
-        # sensor sharding: each rank casts its emitters with all triangles, then gathers
+        merge_packed(hits)
+        # sensor sharding: each rank casts its emitters (n mod P) with all triangles into the global layout
+        # (other emitters' rays stay MISS), then every emitter's keys are broadcast from its owner
         mine = D.shard_emitters(len(ems), rank, world)
         offs = np.cumsum([0] + [e.n_rays for e in ems])
-        sub = oracle.cast([ems[n] for n in mine], tris, threads=2)
-        d_full, t_full = D.gather_emitter_slices(torch.as_tensor(sub["t"]), torch.as_tensor(sub["id"]),
-                                                 [D.shard_emitters(len(ems), r, world) for r in range(world)], offs)
+        keys = torch.full((int(offs[-1]),), D.MISS_KEY, dtype=torch.int64)
+        for n in mine:
+            keys[offs[n]: offs[n + 1]] = torch.as_tensor(_packed(oracle.cast([ems[n]], tris, threads=2)))
+        gather_emitters(keys, offs, world)
+        k = keys.numpy()
+        d_full = (k >> 32).astype(np.uint32).view(np.float32)
+        t_full = (k & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+        uid = D.nccl_uid()
         if rank == 0:
-            q.put((hits.numpy(), d_full.numpy(), t_full.numpy()))
+            q.put((hits.numpy(), d_full, t_full, uid))
+        else:
+            q.put(uid)
     finally:
         dist.destroy_process_group()
 
@@ -59,7 +100,10 @@ def test_two_rank_triangle_and_sensor_sharding():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    merged, d_full, t_full = q.get(timeout=300)
+    got = [q.get(timeout=300) for _ in range(2)]
+    merged, d_full, t_full, uid0 = [x for x in got if isinstance(x, tuple)][0]
+    uid1 = [x for x in got if not isinstance(x, tuple)][0]
+    assert len(uid0) == 128 and uid0 == uid1      # the communicator id reached both ranks intact
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -87,7 +131,7 @@ def _worker_mixed(rank, world, port, q):
         own = D.shard_triangles(len(tris), t, T, block=512)
         res = oracle.cast([ems[n] for n in mine_em], tris[own], ids=own.astype(np.int32), threads=2)
         hits = torch.as_tensor(_packed(res))
-        D.merge_packed(hits, group=subs[g])   # merge only within this emitter group
+        merge_packed(hits, group=subs[g])   # merge only within this emitter group
         q.put((rank, mine_em, hits.numpy()))
     finally:
         dist.destroy_process_group()
@@ -123,7 +167,7 @@ def _worker_scatter(rank, world, port, q):
         own = D.shard_triangles(len(tris), rank, world, block=256)
         res = oracle.cast(ems, tris[own], ids=own.astype(np.int32), threads=2)
         hits = torch.as_tensor(_packed(res))
-        sl, first = D.merge_packed_scatter(hits)
+        sl, first = merge_packed_scatter(hits)
         q.put((rank, first, sl.numpy()))
     finally:
         dist.destroy_process_group()

@@ -786,36 +786,106 @@ def test_unpack_range_slices():
         gr.close()
 
 
-def test_nvls_fused_merge_single_device():
-    """NEXT-f3: with a 1-device multicast (NVLS) object, every hit goes through
-    multimem.red.min.u64 and both device-side barriers run: bit-identical to the local path,
-    over several casts (barrier epochs advance); then back to the local buffer."""
-    from paper_2605_10457_b200 import dist as D
+def _uid():
+    from paper_2605_10457_b200.grca import nccl_unique_id
 
+    return nccl_unique_id()
+
+
+@pytest.mark.parametrize("shard,merge,gather", [(1, 0, 0), (1, 1, 0), (2, 0, 1), (2, 0, 0), (0, 0, 0)])
+def test_collective_one_rank_nccl(shard, merge, gather):
+    """the library-owned collective (grca_create with an NCCL unique id ->
+    ncclCommInitRank; grca_cast merges in-stream: ncclAllReduce / ncclReduceScatter(ncclMin, uint64)
+    for triangle shards, one ncclBroadcast per emitter for gathered emitter shards) on a one-rank
+    communicator gives the non-collective result bit for bit, over several casts."""
+    ems, tris = sg.random_scene(91, n_tris=2000, n_emitters=3, gamma=12, chi=200, extent=9.0)
+    base = run(ems, tris)
+    g = Grca(device=0, max_triangles=len(tris), max_rays=sg.n_rays_total(ems), nranks=1, rank=0, nccl_uid=_uid(),
+             shard_mode=shard, merge=merge, gather_outputs=bool(gather))
+    for _ in range(3):
+        got = run(ems, tris, handle=g)
+        assert np.array_equal(base[1], got[1]) and np.array_equal(base[0].view(np.uint32), got[0].view(np.uint32))
+    sh = g.get_shard()
+    assert sh["shard_mode"] == (shard or G.SHARD_TRIANGLES)   # AUTO with 1 rank: triangle shards
+    assert sh["n_written"] == sg.n_rays_total(ems) and sh["first_ray"] in (0, -1)
+    g.close()
+
+
+def test_nvls_merge_nccl_window_one_rank():
+    """NEXT-f3 through NCCL (GRCA_MERGE_NVLS): keys + barrier flag in an ncclMemAlloc'd symmetric window
+    (ncclCommWindowRegister), hits recorded with multimem.red.min.u64 at the window's lsa multimem
+    address, device barriers on the window's flag.  Bit-identical to the local path where NCCL provides
+    multimem; where it does not (NVLS needs an NVSwitch multicast group), set_emitters reports
+    GRCA_E_NCCL with NCCL's reason -- never a silent fallback."""
     ems, tris = sg.random_scene(61, n_tris=3000, n_emitters=2, gamma=16, chi=256, extent=10.0)
-    a_d, a_t, _, g = run(ems, tris)
-    need = g.nvls_status()["bytes_needed"]
-    assert need >= 8 * sg.n_rays_total(ems) + 128
+    a_d, a_t, _, _ = run(ems, tris)
+    g = Grca(device=0, max_triangles=len(tris), max_rays=sg.n_rays_total(ems), nranks=1, rank=0, nccl_uid=_uid(),
+             shard_mode=G.SHARD_TRIANGLES, merge=G.MERGE_NVLS)
     try:
-        buf = D.NvlsBuffer(need, device_index=0)
-    except RuntimeError as e:  # pragma: no cover - depends on the box
-        pytest.skip(f"no NVLS multicast here: {e}")
-    try:
-        with pytest.raises(GrcaError):
-            g.set_nvls(buf.uc_ptr, None, 1)
-        g.set_nvls(buf.uc_ptr, buf.mc_ptr, 1)
-        for _ in range(3):
-            d, t = g.cast()
-            torch.cuda.synchronize()
-            assert np.array_equal(t.cpu().numpy(), a_t)
-            assert np.array_equal(d.cpu().numpy().view(np.uint32), a_d.view(np.uint32))
-        assert not g.nvls_status()["timed_out"]
-        g.set_nvls(None, None, 0)
-        d, t = g.cast()
-        torch.cuda.synchronize()
-        assert np.array_equal(t.cpu().numpy(), a_t)
-    finally:
-        buf.close()
+        g.set_emitters(ems)
+    except GrcaError as e:
+        assert e.status == G.GRCA_E_NCCL, e
+        g.close()
+        pytest.skip(f"no NVLS multimem on a one-rank NCCL communicator here: {e}")
+    for _ in range(3):
+        d, t, _, _ = run(ems, tris, handle=g)
+        assert np.array_equal(t, a_t) and np.array_equal(d.view(np.uint32), a_d.view(np.uint32))
+    assert not g.nvls_status()["timed_out"]
+    g.close()
+
+
+def test_virtual_ranks_partitions():
+    """GRCA_DEBUG_VIRTUAL_RANKS: each handle does exactly rank r's share of a P-rank cast on one GPU.
+    Emitter shards (P = 3, 4 emitters: rank r casts n mod 3 == r) write exactly their emitters' rays,
+    equal to the one-GPU result, and leave the rest of the outputs untouched; triangle shards (P = 2)
+    min-merge to the one-GPU keys, and under the reduce-scatter merge each rank unpacks only its slice
+    [r c, r c + c), c = ceil(n / P)."""
+    ems, tris = sg.random_scene(92, n_tris=2500, n_emitters=4, gamma=10, chi=150, extent=9.0)
+    n = sg.n_rays_total(ems)
+    base_d, base_t, _, gb = run(ems, tris)
+    gb.cast_packed()
+    base_keys = gb.hits_packed().clone().cpu().numpy()
+    offs = np.cumsum([0] + [e.n_rays for e in ems])
+    v4 = tris_to_float4(tris)
+    for r in range(3):
+        g = Grca(device=0, max_triangles=len(tris), max_rays=n, nranks=3, rank=r, shard_mode=G.SHARD_EMITTERS,
+                 debug_flags=G.DEBUG_VIRTUAL_RANKS)
+        g.set_emitters(ems)
+        g.update_triangles(v4)
+        d = torch.full((n,), 7.0, device="cuda")
+        t = torch.full((n,), -7, dtype=torch.int32, device="cuda")
+        _, _, st = g.cast(d, t, stats=True)
+        d, t = d.cpu().numpy(), t.cpu().numpy()
+        mine = np.zeros(n, bool)
+        for m in range(4):
+            if m % 3 == r:
+                mine[offs[m]: offs[m + 1]] = True
+        assert np.array_equal(t[mine], base_t[mine]) and np.array_equal(d[mine].view(np.uint32), base_d[mine].view(np.uint32))
+        assert np.all(t[~mine] == -7) and np.all(d[~mine] == 7.0)
+        sh = g.get_shard()
+        assert sh == {"shard_mode": G.SHARD_EMITTERS, "first_ray": -1, "n_written": int(mine.sum())}
+        assert st["pairs"] == len(tris) * sum(1 for m in range(4) if m % 3 == r)
+        g.close()
+    merged = None
+    c = -(-n // 2)
+    for r in range(2):
+        own = np.nonzero(((np.arange(len(tris)) // 256) % 2) == r)[0]
+        g = Grca(device=0, max_triangles=len(tris), max_rays=n, nranks=2, rank=r, shard_mode=G.SHARD_TRIANGLES,
+                 merge=G.MERGE_REDUCE_SCATTER, debug_flags=G.DEBUG_VIRTUAL_RANKS)
+        g.set_emitters(ems)
+        g.update_triangles(tris_to_float4(tris[own]), tri_ids=torch.as_tensor(own.astype(np.int32), device="cuda"))
+        d = torch.full((n,), 7.0, device="cuda")
+        t = torch.full((n,), -7, dtype=torch.int32, device="cuda")
+        g.cast(d, t)
+        keys = g.hits_packed().clone().cpu().numpy()
+        merged = keys if merged is None else np.minimum(merged, keys)
+        f, m = r * c, min(c, n - r * c)
+        assert g.get_shard() == {"shard_mode": G.SHARD_TRIANGLES, "first_ray": f, "n_written": m}
+        t = t.cpu().numpy()
+        kt = (keys[f: f + m] & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+        assert np.array_equal(t[f: f + m], kt) and np.all(t[:f] == -7) and np.all(t[f + m:] == -7)
+        g.close()
+    assert np.array_equal(merged, base_keys)
 
 
 def test_float3_vertices_identical():
