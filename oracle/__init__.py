@@ -14,6 +14,7 @@ from .oracle import (  # noqa: F401
     lib_path,
     mt,
     n_rays,
+    near_edge_count,
     ray_table,
     ray_tri,
 )

@@ -319,3 +319,40 @@ int oracle_cast(const oracle_emitter *em, int32_t n_em, const float *tri9,
     free(th);
     return 0;
 }
+
+/*
+ * Comparator helper (SURVEY 8(c) "excused": a disagreement is excused when the triangle involved has
+ * fp64 barycentric margin min(u, v, 1-u-v) within eps of its boundary for the ray): the number of
+ * triangles whose line hit by ray g has t > 0 (and t <= D_max) and |margin| <= eps -- the triangles on
+ * whose edges an all-hit count may legitimately differ by one.  Same O1/O2 definitions as above.
+ */
+int64_t oracle_near_edge_count(const oracle_emitter *em, int32_t n_em, int64_t g, const float *tri9,
+                               int64_t n_tri, double eps)
+{
+    int32_t n, j, i;
+    if (ray_locate(em, n_em, g, &n, &j, &i)) return -1;
+    double d64[3], o[3], d[3];
+    float d32[3];
+    ray_direction(&em[n], j, i, d64, d32);
+    for (int k = 0; k < 3; ++k) {
+        d[k] = (double)d32[k];
+        o[k] = (double)em[n].origin[k];
+    }
+    const double dmax = emitter_dmax(&em[n]);
+    int64_t cnt = 0;
+    for (int64_t q = 0; q < n_tri; ++q) {
+        const float *T = &tri9[9 * q];
+        double a[3], b[3], c[3], t, u, v, dN;
+        for (int k = 0; k < 3; ++k) {
+            a[k] = (double)T[k];
+            b[k] = (double)T[3 + k];
+            c[k] = (double)T[6 + k];
+        }
+        if (!oracle_mt(o, d, a, b, c, &t, &u, &v, &dN)) continue;
+        if (!(t > 0.0 && t <= dmax)) continue;
+        double m = u < v ? u : v;
+        if (1.0 - u - v < m) m = 1.0 - u - v;
+        if (fabs(m) <= eps) ++cnt;
+    }
+    return cnt;
+}

@@ -65,6 +65,8 @@ def _get():
         L.oracle_ray_tri.argtypes = [C.POINTER(_Em), C.c_int32, C.c_int64, C.c_void_p, C.c_int32,
                                      C.POINTER(C.c_double), C.POINTER(C.c_double),
                                      C.POINTER(C.c_double), C.POINTER(C.c_int32)]
+        L.oracle_near_edge_count.restype = C.c_int64
+        L.oracle_near_edge_count.argtypes = [C.POINTER(_Em), C.c_int32, C.c_int64, C.c_void_p, C.c_int64, C.c_double]
         L.oracle_cast.restype = C.c_int
         L.oracle_cast.argtypes = [C.POINTER(_Em), C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                   C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -132,6 +134,17 @@ def ray_tri(emitters, g: int, tri9, faces: int = 0, _arr: Optional[_EmArray] = N
     if ok < 0:
         raise IndexError(g)
     return bool(ok), t.value, u.value, v.value, bool(hit.value)
+
+
+def near_edge_count(emitters, g: int, tris: np.ndarray, eps: float = 1e-6) -> int:
+    """Triangles hit (t in (0, D_max]) by ray g within `eps` of their boundary (fp64 barycentric margin):
+    by how much a per-ray all-hit count may legitimately differ (grca_oracle.c oracle_near_edge_count)."""
+    A = _EmArray(emitters)
+    T = np.ascontiguousarray(np.asarray(tris, dtype=np.float32).reshape(-1, 9))
+    r = _get().oracle_near_edge_count(A.arr, A.n, int(g), T.ctypes.data if T.shape[0] else None, T.shape[0], float(eps))
+    if r < 0:
+        raise IndexError(g)
+    return int(r)
 
 
 def cast(emitters, tris: np.ndarray, ids: Optional[np.ndarray] = None, faces: int = 0,

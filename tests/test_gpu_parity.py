@@ -139,23 +139,22 @@ def test_random_scenes(seed):
     assert st["rtic_tested"] <= st["rtic_brute"]
 
 
-def _near_edge_count(ems, tris, g):
-    """Triangles whose fp64 barycentric margin for ray g is within 1e-6 of their boundary."""
-    n = 0
-    for T in np.asarray(tris, np.float32).reshape(-1, 9):
-        ok, t, u, v, hit = oracle.ray_tri(ems, int(g), T)
-        if ok and t > 0 and abs(min(u, v, 1 - u - v)) <= 1e-6:
-            n += 1
-    return n
-
-
-def _check_all_hits(ems, tris, counts, ref):
-    diff = np.nonzero(counts != ref["allhits"])[0]
+def _check_all_hits(ems, tris, counts, ref, rays=None):
+    """All-hits invariant (north star: culling never drops a brute-force hit).  Per-ray counts of every
+    accepted hit equal the oracle's, except on rays where a triangle lies within 1e-6 barycentric of its
+    boundary (the excusal of the parity contract): there the counts may differ by at most the number of
+    such triangles (oracle.near_edge_count).  Returns the number of excused rays, bounded by 1e-4 of the
+    rays checked (the certified test disagrees with exact arithmetic only at ~1e-16 relative)."""
+    got = counts if rays is None else counts[rays]
+    exp = ref["allhits"]
+    diff = np.nonzero(got != exp)[0]
+    assert len(diff) <= max(2, int(1e-4 * len(exp))), (len(diff), len(exp))
     bad = []
-    for r in diff[:200]:
-        if abs(int(counts[r]) - int(ref["allhits"][r])) > _near_edge_count(ems, tris, r):
-            bad.append((int(r), int(counts[r]), int(ref["allhits"][r])))
-    assert not bad and len(diff) <= 200, (len(diff), bad[:10])
+    for r in diff:
+        g = int(ref["rays"][r])
+        if abs(int(got[r]) - int(exp[r])) > oracle.near_edge_count(ems, g, tris):
+            bad.append((g, int(got[r]), int(exp[r])))
+    assert not bad, bad[:10]
     return len(diff)
 
 
@@ -173,7 +172,8 @@ def test_all_hits_invariant():
     tris = sg.c1_scene()
     dist, tri, st, g = run(ems, tris, flags=G.DEBUG_COUNT_ALL_HITS)
     ref = oracle.cast(ems, tris, want_allhits=True)
-    _check_all_hits(ems, tris, g.debug_all_hits().cpu().numpy(), ref)
+    excused = _check_all_hits(ems, tris, g.debug_all_hits().cpu().numpy(), ref)
+    print(f"C1 all-hits: {len(ref['allhits'])} rays, {int(ref['allhits'].sum())} hits, {excused} excused rays")
 
 
 def test_no_cull_bit_identical_and_fp64_mode():
@@ -362,34 +362,53 @@ def test_c3_like_ranged_sampled(rng_m):
     assert st["range_culled"] > 0
 
 
+def _scale_parity(w, n_per_emitter, seed, label):
+    """Full-size frame in the launch configuration bench.py times (grca_update_scene: static float4 soup
+    + indexed float3 cars, an uninstrumented handle) == the triangle-soup cast bit for bit; then, on
+    n_per_emitter sampled rays per emitter, closest-hit parity (north-star comparator) and the all-hits
+    invariant against ONE oracle pass over all triangles."""
+    ems, tris = w["emitters"], w["tris"]
+    n_rays = sg.n_rays_total(ems)
+    g = Grca(device=0, max_triangles=len(tris), max_rays=n_rays)
+    g.set_emitters(ems)
+    di, ti = run_indexed_frame(w, g)
+    g.close()
+    dist, tri, st, ga = run(ems, tris, flags=G.DEBUG_COUNT_ALL_HITS)
+    assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
+    counts = ga.debug_all_hits().cpu().numpy()
+    rays = _sampled(ems, n_per_emitter, seed)
+    ref = oracle.cast(ems, tris, rays=rays, want_t64=True, want_allhits=True)
+    rep, _ = check(ems, tris, di, ti, rays=rays, ref=ref)
+    excused = _check_all_hits(ems, tris, counts, ref, rays=rays)
+    print(f"{label}: {rep['rays']} rays, agree {rep['agree_frac']:.6f}, excused {rep['excused']}, near-ties "
+          f"{rep['near_ties']}, Hit% 1 mm {rep['hit_pct_1mm']:.4f}, oracle hits {rep['oracle_hits']}, "
+          f"all-hit counts {int(ref['allhits'].sum())} (excused rays {excused})")
+    assert rep["oracle_hits"] > n_per_emitter * len(ems) // 4
+    ga.close()
+    return st, rep
+
+
+def test_c2_full_size_all_hits():
+    """C2 at full size (2 x 128x4096 rays, ~1M triangles): parity + all-hits on 2,048 rays per emitter."""
+    st, rep = _scale_parity(sg.workload("C2", frame=1), 2048, 21, "C2 frame 1")
+    assert st["pairs"] == st["pairs"] and rep["agree_frac"] >= 0.99999
+
+
 @pytest.mark.slow
 def test_c4_full_size_sampled():
-    """C4 at full size (8 x 128x4096 rays, ~21.8M triangles), in the launch configuration
-    bench.py times, checked on sampled rays against the oracle (all triangles per ray)."""
+    """C4 at full size (8 x 128x4096 rays, ~21.8M triangles), frame 0: 1,024 sampled rays per emitter
+    (8,192 rays x all triangles in the oracle), parity + all-hits invariant."""
     w = sg.workload("C4", frame=0)
-    dist, tri, st, g = run(w["emitters"], w["tris"])
-    rays = _sampled(w["emitters"], 24, 9)
-    rep, _ = check(w["emitters"], w["tris"], dist, tri, rays=rays)
+    st, _ = _scale_parity(w, 1024, 9, "C4 frame 0")
     assert st["pairs"] == len(w["tris"]) * 8
-    assert rep["oracle_hits"] > 20
-    # bench.py's default representation of the same frame (grca_update_scene: static float4 soup +
-    # indexed float3 cars) gives the bit-identical result
-    di, ti = run_indexed_frame(w, g)
-    assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
 
 
 @pytest.mark.slow
 def test_c4_full_size_large_rectangle_frame():
-    """C4 frame 2 (the bench cycles frames 0-3; frames with huge scaled cars send many large
-    rectangles through K3/K4), full size, in the scene layout bench.py times: sampled
-    parity against the oracle, plus soup == indexed bit for bit."""
-    w = sg.workload("C4", frame=2)
-    dist, tri, st, g = run(w["emitters"], w["tris"])
+    """C4 frame 2 (huge scaled cars send many large rectangles through K3/K4 and A7), full size:
+    1,024 sampled rays per emitter, parity + all-hits invariant."""
+    st, _ = _scale_parity(sg.workload("C4", frame=2), 1024, 19, "C4 frame 2")
     assert st["large_pairs"] > 1000 and st["chunks"] > 10000
-    di, ti = run_indexed_frame(w, g)
-    assert np.array_equal(ti, tri) and np.array_equal(di.view(np.uint32), dist.view(np.uint32))
-    rep, _ = check(w["emitters"], w["tris"], di, ti, rays=_sampled(w["emitters"], 24, 19))
-    assert rep["oracle_hits"] > 20
 
 
 def test_c2_hybrid_indexed_dynamic():
@@ -806,7 +825,8 @@ def test_collective_one_rank_nccl(shard, merge, gather):
         got = run(ems, tris, handle=g)
         assert np.array_equal(base[1], got[1]) and np.array_equal(base[0].view(np.uint32), got[0].view(np.uint32))
     sh = g.get_shard()
-    assert sh["shard_mode"] == (shard or G.SHARD_TRIANGLES)   # AUTO with 1 rank: triangle shards
+    # AUTO: emitter shards when n_emitters >= nranks and nranks | n_emitters (always, with one rank)
+    assert sh["shard_mode"] == (shard or G.SHARD_EMITTERS)
     assert sh["n_written"] == sg.n_rays_total(ems) and sh["first_ray"] in (0, -1)
     g.close()
 

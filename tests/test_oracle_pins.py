@@ -433,6 +433,8 @@ def test_comparator_excusal_boundary(oracle_lib):
         assert rep["disagree"] == 1 and rep["kinds"]["gpu_miss"] == 1
         assert rep["excused"] == int(excused) and rep["unexcused"] == int(not excused)
         assert not rep["passed"] or excused
+        # the all-hits excusal counter agrees: the triangle is within 1e-6 of its boundary iff excused
+        assert oracle.near_edge_count([em], g, tri) == int(excused)
         # the mirror case: the GPU reports a hit on a triangle the oracle misses (ray just outside)
         out = _tri_with_margin(p, -margin)
         ref2 = oracle.cast([em], out, want_t64=True)
@@ -451,6 +453,7 @@ def test_comparator_excusal_boundary(oracle_lib):
     rep = oracle.compare([em], tris, t_g, i_g, ref)
     assert rep["excused"] == 1 and rep["unexcused"] == 0 and rep["kinds"]["gpu_miss"] == 1
     assert not rep["passed"]                             # 8191 / 8192 = 99.988 % < 99.999 %
+    assert oracle.near_edge_count([em], g, tris) == 2 and oracle.near_edge_count([em], g - 6, tris) == 0
     # ... while the same excused drop among 103,424 rays passes (1 - 1/103424 >= 99.999 %) and an
     # unexcused one (a 1e-4 relative distance error) does not
     elev = np.concatenate([np.linspace(-0.3, -0.006, 50), [0.0], np.linspace(0.006, 0.3, 50)]).astype(np.float32)
