@@ -139,7 +139,7 @@ def test_random_scenes(seed):
     assert st["rtic_tested"] <= st["rtic_brute"]
 
 
-def _check_all_hits(ems, tris, counts, ref, rays=None):
+def _check_all_hits(ems, tris, counts, ref, rays=None, bound=1e-4):
     """All-hits invariant (north star: culling never drops a brute-force hit).  Per-ray counts of every
     accepted hit equal the oracle's, except on rays where a triangle lies within 1e-6 barycentric of its
     boundary (the excusal of the parity contract): there the counts may differ by at most the number of
@@ -148,7 +148,7 @@ def _check_all_hits(ems, tris, counts, ref, rays=None):
     got = counts if rays is None else counts[rays]
     exp = ref["allhits"]
     diff = np.nonzero(got != exp)[0]
-    assert len(diff) <= max(2, int(1e-4 * len(exp))), (len(diff), len(exp))
+    assert len(diff) <= max(2, int(bound * len(exp))), (len(diff), len(exp))
     bad = []
     for r in diff:
         g = int(ref["rays"][r])
@@ -172,7 +172,9 @@ def test_all_hits_invariant():
     tris = sg.c1_scene()
     dist, tri, st, g = run(ems, tris, flags=G.DEBUG_COUNT_ALL_HITS)
     ref = oracle.cast(ems, tris, want_allhits=True)
-    excused = _check_all_hits(ems, tris, g.debug_all_hits().cpu().numpy(), ref)
+    # C1's ground grid has lines x = 0 and y = 0 right under the emitter: the 14 rays at azimuths 0, 90,
+    # 180, 270 deg of channels 1-5 run exactly along shared ground edges (bound 2e-3 instead of 1e-4)
+    excused = _check_all_hits(ems, tris, g.debug_all_hits().cpu().numpy(), ref, bound=2e-3)
     print(f"C1 all-hits: {len(ref['allhits'])} rays, {int(ref['allhits'].sum())} hits, {excused} excused rays")
 
 
