@@ -38,9 +38,10 @@ def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
         d = json.load(open(p))
-        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "measured", "sm_max_mhz": float(d.get("sm_max_mhz", 1965))}
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src_hbm": "measured (MEASURED_PEAKS.json hbm_gbs, copy b/w)",
+                "sm_max_mhz": float(d.get("sm_max_mhz", 1965))}
     except Exception:
-        return {"hbm_gbs": 6650.0, "src": "fallback", "sm_max_mhz": 1965.0}
+        return {"hbm_gbs": 6650.0, "src_hbm": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0}
 
 
 # ----------------------------------------------------------------- clocks --
@@ -146,7 +147,7 @@ class Scene:
         if self.indexed:
             car_v, car_f = cm
             nv_car, nf_car = len(car_v), len(car_f)
-            self.car_v = torch.as_tensor(car_v, dtype=torch.float32, device=device)   # (V, 3)
+            self.car_v_np = np.asarray(car_v, dtype=np.float32)   # (V, 3) local
             inst, f = self.own_dyn // nf_car, self.own_dyn % nf_car
             rel = (inst.astype(np.int64) * nv_car)[:, None] + car_f[f].astype(np.int64)
             self.idx_dyn = torch.as_tensor(rel.astype(np.int32).reshape(-1), device=device)
@@ -156,8 +157,7 @@ class Scene:
             # 12 B per shared float3 vertex
             self.tri_bytes = self.n_static_local * 48 + len(self.own_dyn) * 12 + self.n_dyn_vert * 12
         else:
-            self.car = torch.as_tensor(w["car_local"], dtype=torch.float32, device=device)   # (m, 3, 3)
-            self.own_dyn_t = torch.as_tensor(self.own_dyn, device=device)
+            self.car_np = np.asarray(w["car_local"], dtype=np.float32)   # (m, 3, 3) local
             self.tri_bytes = self.n_tri * 48
         # frame buffers: soup = [static | dynamic] float4 rows; indexed = the car vertices only
         self.fs = 0 if self.indexed else self.ns3   # static rows at the head of a frame buffer
@@ -180,24 +180,20 @@ class Scene:
 
     def dynamic(self, frame: int):
         """Motion f.i: per-frame random pose/scale of every car instance; world
-        v = R (s * v_local) + p.  Computed with torch on the device.  Indexed: the posed car
-        vertices (n_cars * V, 3); soup: the own dynamic triangles' vertices (3 * n_own_dyn, 3)."""
+        v = R (s * v_local) + p, posed with scenegen.apply_pose (host fp64, rounded once), so every frame
+        equals scenegen.workload(config, frame) bit for bit and the oracle can check it.  Indexed: the
+        posed car vertices (n_cars * V, 3); soup: the own dynamic triangles' vertices (3 * n_own_dyn, 3)."""
         import torch
 
         poses = sg.pose_instances(self.n_cars, self.bbox, int(self.config[1:]), frame, scale_lo=self.scale[0],
                                   scale_hi=self.scale[1])
-        R = torch.as_tensor(np.stack([p.rotation for p in poses]), dtype=torch.float32, device=self.device)
-        s = torch.as_tensor(np.stack([p.scale for p in poses]), dtype=torch.float32, device=self.device)
-        p = torch.as_tensor(np.stack([p.position for p in poses]), dtype=torch.float32, device=self.device)
         if self.indexed:
-            v = (self.car_v[None] * s[:, None, :]) @ R.transpose(1, 2) + p[:, None, :]
-            return v.reshape(-1, 3)
-        v = (self.car[None] * s[:, None, None, :]) @ R.transpose(1, 2)[:, None] + p[:, None, None, :]
-        v = v.reshape(-1, 3, 3)
+            v = np.concatenate([sg.apply_pose(self.car_v_np, p) for p in poses], 0)
+            return torch.as_tensor(v, device=self.device)
+        v = np.concatenate([sg.apply_pose(self.car_np, p) for p in poses], 0)
         if self.deformation == "SWD":
-            v = v.cpu().numpy()
-            v = torch.as_tensor(sg.swd(v, self.bbox, int(self.config[1:]), frame), device=self.device)
-        return v[self.own_dyn_t].reshape(-1, 3)
+            v = sg.swd(v, self.bbox, int(self.config[1:]), frame)
+        return torch.as_tensor(np.ascontiguousarray(v[self.own_dyn].reshape(-1, 3)), device=self.device)
 
 
 # ------------------------------------------------------------- reference --
@@ -221,82 +217,100 @@ def time_oracle(emitters, tris, target_s: float = 12.0, max_rays: int = 4096):
     n2 = int(min(max_rays, max(n, rate * target_s)))
     rays = oracle_sample(emitters, tris, n2, 2)
     t0 = time.perf_counter()
-    oracle.cast(emitters, tris, rays=rays, threads=threads)
+    ref = oracle.cast(emitters, tris, rays=rays, threads=threads, want_t64=True)
     dt = time.perf_counter() - t0
     return {"value": n2 / dt, "unit": "rays/s", "cores": threads, "kind": "oracle",
             "sample": f"{n2} seeded rays x all {len(tris)} triangles (fp64 brute force, Eq. 1), {dt:.1f} s",
-            "tests_per_s": n2 * len(tris) / dt, "frame_ms_extrapolated": 1e3 * dt * sg.n_rays_total(emitters) / n2}
+            "tests_per_s": n2 * len(tris) / dt, "frame_ms_extrapolated": 1e3 * dt * sg.n_rays_total(emitters) / n2,
+            "frame_ms_kind": "extrapolated: measured sample time x rays per frame / sampled rays"}, ref
 
 
 KERNELS = ["K0_init", "K2_cull", "K2b_refine", "K4s_small", "K3_bin", "K4_large", "K5_unpack"]
 # (fused default: "K4s_small" is the fused K2b+K4s kernel k_refine_small and "K2b_refine" is ~0)
 NCU_NAME = {"K2_cull": "k_cull_fixed", "K2b_refine": "k_refine(", "K4s_small": "k_refine_small", "K4_large": "k_isect",
             "K0_init": "k_init", "K3_bin": "k_bin", "K5_unpack": "k_unpack"}
-# algorithmic work per unit: fp32 ALU operations or HBM bytes
-ALU_PER_PAIR_K2 = 50        # elevation pre-test of one (triangle, emitter) pair
-ALU_PER_SURV_K2B = 400      # exact bounds (elevation, pole, azimuth arc, ray range) of one survivor
-ALU_PER_ITEM = 25           # certified edge-function test of one (triangle, ray) candidate
-ALU_PER_SETUP = 150         # per-pair certified setup (3 edge normals + bounds, fp64 plane)
+# Algorithmic work per unit, SURVEY.md 8(d) "Algorithmic work" (midpoints of its ranges):
+#   per (triangle, emitter) pair: quick reject ~40-60 instructions -> 50
+#   per K2 survivor: exact bounds ~250-400 instructions -> 325 (the fused kernel's per-survivor work)
+#   per candidate (RTIC performed): ~20 fp32 flops + compares -> 25 lane-instructions, and one u64 RED.MIN
+#   per improving hit; per ray 8 B init (K0) + 8 B read + 8 B written (K5); per triangle its vertex bytes
+ALU_PER_PAIR = 50
+ALU_PER_SURVIVOR = 325
+ALU_PER_CANDIDATE = 25
+BYTES_K0_PER_RAY = 8
+BYTES_K5_PER_RAY = 16
 
 
-def ncu_traffic():
-    """DRAM bytes per launch from the latest committed `ncu --set full` capture (profiles/)."""
-    import glob
-
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
-    if not files:
-        return {}, None
-    d = json.load(open(files[-1]))
-    out = {}
-    for k, v in d.get("per_kernel", {}).items():
-        for ours, nm in NCU_NAME.items():
-            if nm in k:
-                out[ours] = v
-    return out, os.path.basename(files[-1])
-
-
-def kernel_rooflines(kernel_ms, st, n_rays, n_tri, n_em, clk, device, split=False, tri_bytes=None):
-    import torch
-
+def measured_peaks():
+    """Denominators measured live on this GPU (tools/peaks.cu: FFMA lane-instruction rate, u64 RED.MIN rate
+    into an L2-resident 33.5 MB buffer) plus MEASURED_PEAKS.json's HBM copy bandwidth; the committed
+    profiles/r02_peaks.json if the live run fails."""
     pk = peaks()
-    n_sm = torch.cuda.get_device_properties(device).multi_processor_count
-    mhz = clk.get("sm_mhz") or pk["sm_max_mhz"]
-    alu_peak = n_sm * 128 * mhz * 1e6 / 1e12          # fp32 lane-ops/s (4 SMSP x 32 lanes per SM)
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import peaks as P   # noqa: E402
+
+        m = P.measure()
+        m["src"] = "measured live (tools/peaks.cu)"
+    except Exception as e:  # noqa: BLE001
+        m = json.load(open(os.path.join(ROOT, "profiles", "r02_peaks.json")))
+        m["src"] = f"profiles/r02_peaks.json (live measurement failed: {e})"
+    pk.update(m)
+    return pk
+
+
+def kernel_rooflines(kernel_ms, st, n_rays, pk, tri_bytes, split=False):
+    """Per-kernel achieved / peak with SURVEY 8(d)'s per-unit counts (see the constants above)."""
     traffic, src = ncu_traffic()
     small_items = st["rtic_small"]
     large_items = st["rtic_tested"] - small_items
+    alu_peak = pk["ffma_lane_instr_per_s"] / 1e12
     work = {
-        "K0_init": ("hbm", 8 * n_rays),
-        "K2_cull": ("alu", ALU_PER_PAIR_K2 * st["pairs"]),
-        "K2b_refine": ("alu", ALU_PER_SURV_K2B * st["prefilter_survivors"] if split else 0),
-        # fused default: the refine+small kernel also does K2b's per-survivor bounds
-        "K4s_small": ("alu", ALU_PER_ITEM * small_items + ALU_PER_SETUP * st["small_pairs"] +
-                      (0 if split else ALU_PER_SURV_K2B * st["prefilter_survivors"])),
-        "K3_bin": ("hbm", 32 * max(1, st["large_pairs"])),
-        "K4_large": ("alu", ALU_PER_ITEM * large_items + ALU_PER_SETUP * st["chunks"]),
-        "K5_unpack": ("hbm", 16 * n_rays),
+        "K0_init": ("hbm", BYTES_K0_PER_RAY * n_rays, f"{BYTES_K0_PER_RAY} B x rays"),
+        "K2_cull": ("alu", ALU_PER_PAIR * st["pairs"], f"{ALU_PER_PAIR} x pairs"),
+        "K2b_refine": ("alu", ALU_PER_SURVIVOR * st["prefilter_survivors"] if split else 0,
+                       f"{ALU_PER_SURVIVOR} x K2 survivors (split mode only)"),
+        "K4s_small": ("alu", ALU_PER_CANDIDATE * small_items + (0 if split else ALU_PER_SURVIVOR * st["prefilter_survivors"]),
+                      f"{ALU_PER_SURVIVOR} x K2 survivors + {ALU_PER_CANDIDATE} x small-rectangle candidates"),
+        "K3_bin": ("hbm", 32 * max(1, st["large_pairs"]), "32 B x large pairs (not an 8(d) unit; context)"),
+        "K4_large": ("alu", ALU_PER_CANDIDATE * large_items, f"{ALU_PER_CANDIDATE} x large-rectangle candidates"),
+        "K5_unpack": ("hbm", BYTES_K5_PER_RAY * n_rays, f"{BYTES_K5_PER_RAY} B x rays"),
     }
+    reds = {"K4s_small": st["hits_recorded"] - st["hits_large"], "K4_large": st["hits_large"]}
     out = {}
-    for k, (bound, amount) in work.items():
+    for k, (bound, amount, unit_src) in work.items():
         t = max(kernel_ms[k], 1e-9) / 1e3
         if bound == "hbm":
             ach, peak, unit = amount / t / 1e9, pk["hbm_gbs"], "GB/s"
+            psrc = pk["src_hbm"]
         else:
-            ach, peak, unit = amount / t / 1e12, alu_peak, "Tops/s"
+            ach, peak, unit = amount / t / 1e12, alu_peak, "T lane-instr/s"
+            psrc = "FFMA lane-instruction rate, " + pk["src"]
         tr = traffic.get(k, {})
         out[k] = {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-                  "traffic": tr.get("dram_bytes"), "algorithmic_per_launch": amount,
+                  "traffic": tr.get("dram_bytes"), "algorithmic_per_launch": amount, "algorithmic_units": unit_src,
                   # context from the same ncu capture: fraction of cycles an instruction issued
                   # (a latency-bound kernel sits well below 1 even when its ALU fraction is low)
                   "ncu_issue_slots_busy": (tr["issue_slots_busy_pct"] / 100.0) if "issue_slots_busy_pct" in tr else None,
-                  "peak_src": (pk["src"] + " (MEASURED_PEAKS.json hbm_gbs)") if bound == "hbm" else
-                  f"derived: {n_sm} SMs x 128 fp32 lanes x {mhz:.0f} MHz (median SM clock under load)",
-                  "traffic_src": src}
-    # K2 also streams the triangle soup once: report its HBM fraction beside the ALU one
+                  "peak_src": psrc, "traffic_src": src}
+        if k in reds:   # closest-hit key updates: u64 RED.MIN per accepted hit
+            out[k]["red_min_per_s"] = reds[k] / t
+            out[k]["red_min_frac"] = reds[k] / t / pk["red_min_u64_random_per_s"]
+    # K2 also streams the triangles once: its HBM fraction beside the ALU one
     t2 = max(kernel_ms["K2_cull"], 1e-9) / 1e3
-    out["K2_cull"]["hbm_achieved_gbs"] = (tri_bytes if tri_bytes is not None else 48 * n_tri) / t2 / 1e9
+    out["K2_cull"]["hbm_achieved_gbs"] = tri_bytes / t2 / 1e9
     out["K2_cull"]["hbm_frac"] = out["K2_cull"]["hbm_achieved_gbs"] / pk["hbm_gbs"]
     return out
+
+
+def frame_roofline(roof, ms_step, n_rays, tri_bytes, pk):
+    """Whole-frame bound: t_HBM = (triangle bytes + 24 B per ray) / HBM peak, t_ALU = all kernels'
+    algorithmic lane-instructions / FFMA lane-instruction peak; frac = max(t_HBM, t_ALU) / t_measured."""
+    t_hbm = (tri_bytes + 24 * n_rays) / (pk["hbm_gbs"] * 1e9) * 1e3
+    alu = sum(v["algorithmic_per_launch"] for v in roof.values() if v["bound"] == "alu")
+    t_alu = alu / pk["ffma_lane_instr_per_s"] * 1e3
+    return {"t_hbm_floor_ms": t_hbm, "t_alu_floor_ms": t_alu, "t_measured_ms": ms_step,
+            "frac": max(t_hbm, t_alu) / ms_step, "alu_lane_instr": alu, "hbm_bytes": tri_bytes + 24 * n_rays}
 
 
 # ------------------------------------------------------------------ main --
@@ -346,7 +360,7 @@ def main():
         import oracle
 
         threads = os.cpu_count() or 1
-        cal = time_oracle(w["emitters"], w["tris"], target_s=2.0, max_rays=256)
+        cal, _ = time_oracle(w["emitters"], w["tris"], target_s=2.0, max_rays=256)
         per_step = max(1, int(cal["value"] * 120.0 / max(1, args.steps + args.warmup)))
         vals = []
         for k in range(args.warmup + args.steps):
@@ -361,7 +375,10 @@ def main():
                   "sample": f"{per_step} seeded rays per step x all {len(w['tris'])} triangles (fp64 brute force)"}]
         line = {
             "impl": "reference", "metric": "rays/s", "value": v, "unit": "rays/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n_rays / v, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * n_rays / v,
+            "ms_per_step_kind": (f"extrapolated: each step times {per_step} sampled rays of the frame; ms_per_step = "
+                                 f"{n_rays} rays per frame / the median sampled rate"),
+            "sampled_rays_per_step": per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "rays_per_frame": n_rays, "triangles": int(len(w["tris"])),
                        "deformation": args.deformation},
@@ -459,6 +476,7 @@ def main():
         cast_once()
 
     stream = torch.cuda.current_stream(device)
+    pk = measured_peaks()   # roofline denominators, measured on this GPU before the timed region
     for k in range(args.warmup):
         step(k)
     torch.cuda.synchronize()
@@ -473,14 +491,32 @@ def main():
     clocks.start()
     time.sleep(0.15)
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    # per-frame events on the launch stream (frame pacing) inside the timed region
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
     for k in range(args.steps):
         step(k)
-    e1.record(stream)
+        evs[k + 1].record(stream)
     barrier()
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
+    ms = evs[0].elapsed_time(evs[-1])
+    frame_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    if args.steps < 50:   # the pacing statistics use >= 50 frames (the paper's 50-frame sections)
+        extra = [torch.cuda.Event(enable_timing=True) for _ in range(50 - args.steps + 1)]
+        extra[0].record(stream)
+        for k in range(len(extra) - 1):
+            step(args.steps + k)
+            extra[k + 1].record(stream)
+        torch.cuda.synchronize()
+        frame_ms += [extra[k].elapsed_time(extra[k + 1]) for k in range(len(extra) - 1)]
+    fm = np.asarray(frame_ms)
+    mu = float(fm.mean())
+    pacing = {"frames": int(fm.size), "median_ms": float(np.median(fm)), "mean_ms": mu,
+              "p95_ms": float(np.percentile(fm, 95)), "min_ms": float(fm.min()), "max_ms": float(fm.max()),
+              "within_20pct_of_mean": float(np.mean(np.abs(fm - mu) <= 0.2 * mu)),
+              "below_mean": float(np.mean(fm < mu)),
+              "note": "per-frame CUDA events on the launch stream; +-20 % and < mu as in PAPER.md Table frame_pacing "
+                      "(P:1588-1614); frames beyond --steps (if < 50) are timed after the headline region"}
     # per-kernel breakdown: the same casts on a profiled handle (not part of the timed region)
     gp = new_handle(mode_flags | G.PROFILE_KERNELS)
     n_last = min(max(args.steps, 8), 64)
@@ -655,16 +691,29 @@ def main():
     launches_per_cast = 6 + (1 if args.split_refine else 0) + (2 if nvls else 0)
     # ---- per-kernel roofline (per-kernel CUDA events on the launch stream, last <= 64 steps)
     kernel_ms = {n: kms[i] for i, n in enumerate(KERNELS)}
-    roof = kernel_rooflines(kernel_ms, stats, n_rays, scene.n_tri, len(ems), clk, device, split=args.split_refine,
-                            tri_bytes=scene.tri_bytes)
+    roof = kernel_rooflines(kernel_ms, stats, n_rays, pk, scene.tri_bytes, split=args.split_refine)
+    froof = frame_roofline(roof, ms_step, n_rays, scene.tri_bytes, pk)
     dom = max(roof, key=lambda n: kernel_ms[n])
     roofline = dict(roof[dom])
     roofline["kernel"] = dom
 
-    cpu = None
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        # the GPU result of frame 0 (the frame the oracle sample below is drawn from: scene frames equal
+        # scenegen.workload(config, frame) bit for bit), cast by the timed handle
+        scene.bind(g, scene.frames[0])
+        cast_once()
+        torch.cuda.synchronize()
+        gd, gt = dist_out.cpu().numpy(), tri_out.cpu().numpy()
         tris_np = scene.w["tris"]
-        cpu = time_oracle(ems, tris_np)
+        cpu, ref = time_oracle(ems_lib, tris_np, target_s=15.0)
+        rep = oracle.compare(ems_lib, tris_np, gd[ref["rays"]], gt[ref["rays"]], ref)
+        parity = {k: rep[k] for k in ("rays", "agree_frac", "disagree", "excused", "unexcused", "near_ties",
+                                      "oracle_hits", "hit_pct_1mm", "passed")}
+        parity["what"] = ("frame 0 of the timed handle vs the cpu_baseline's oracle rays (same sample), north-star "
+                          "comparator (oracle/compare.py)")
 
     if rank == 0:
         culled = 1.0 - stats["rtic_tested"] / max(1, stats["rtic_brute"])
@@ -695,13 +744,18 @@ def main():
             "rtic_per_s": stats["rtic_tested"] / (ms_step / 1e3),
             "rtic_effective_per_s": n_rays_job * scene.n_tri_global / (ms_step / 1e3),
             "stats_scope": "rank 0" if world > 1 else "job",
-            "kernel_ms": kernel_ms, "kernel_roofline": {k: {kk: v[kk] for kk in ("bound", "achieved", "unit", "frac")}
-                                                          for k, v in roof.items()},
+            "kernel_ms": kernel_ms,
+            "kernel_roofline": {k: {kk: v[kk] for kk in ("bound", "achieved", "unit", "frac", "hbm_achieved_gbs",
+                                                         "hbm_frac", "red_min_per_s", "red_min_frac") if kk in v}
+                                for k, v in roof.items()},
+            "frame_roofline": froof, "frame_pacing": pacing,
+            "peaks": {k: pk[k] for k in ("hbm_gbs", "src_hbm", "ffma_lane_instr_per_s", "ffma2_lane_instr_per_s",
+                                         "red_min_u64_random_per_s", "red_min_u64_coalesced_per_s", "src") if k in pk},
             "stats": {k: stats[k] for k in ("prefilter_survivors", "rtic_small",
                 "pairs", "range_culled", "channel_culled", "azimuth_culled", "survivors", "small_pairs", "large_pairs",
-                "chunks", "fp64_fallbacks", "hits_recorded", "overflow")},
+                "chunks", "fp64_fallbacks", "hits_recorded", "hits_large", "overflow")},
             "roofline": roofline, "gpu_launches": launches_per_cast * args.steps, "clocks": clk,
-            "e2e": e2e, "cpu_baseline": cpu, "hybrid_static_cache": hybrid,
+            "e2e": e2e, "cpu_baseline": cpu, "parity": parity, "hybrid_static_cache": hybrid,
             "emulated": ({"rank": s_rank, "world": s_world, "shard": shard, "rank_rays": n_rays,
                           "note": "this rank's share of a W-rank run on one GPU (no merge timed)"}
                          if args.emulate_world > 1 else None),

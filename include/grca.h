@@ -154,6 +154,8 @@ typedef struct {
                                 SAT = no seam wrap and gamma_span <= 64 and chi_span <= 64 ... */
     int64_t bat_pairs;       /* ... BAT = the rest (counts only; the build bins by item count) */
     int64_t area_culled;     /* pairs skipped by the apparent-area cull (paper mode) */
+    int64_t hits_large;      /* part of hits_recorded (= RED.MIN key updates issued) made by K4 / the serial
+                                fallback; the rest by the fused small-rectangle kernel */
     int32_t overflow;        /* 1 if any capacity fallback happened */
     float ms_total;          /* device time of the last cast if GRCA_PROFILE_KERNELS */
     float ms_k[8];           /* per kernel: K0 init, K2 cull, K2b refine (split mode only), K2b+K4s

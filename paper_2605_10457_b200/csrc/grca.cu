@@ -57,7 +57,7 @@ constexpr int kLutMaxEm = 16;   // channel LUTs staged in smem for up to 16 emit
 enum Stat {
     ST_PAIRS = 0, ST_RANGE, ST_CHANNEL, ST_AZIMUTH, ST_SURV, ST_SMALL, ST_LARGE, ST_ITEMS_SMALL,
     ST_ITEMS_LARGE, ST_FP64, ST_HITS, ST_CHUNKS, ST_OVF_LARGE, ST_OVF_CHUNK, ST_SETUP64, ST_DEGEN,
-    ST_K2SURV, ST_SAT, ST_BAT, ST_AREA, ST_COUNT
+    ST_K2SURV, ST_SAT, ST_BAT, ST_AREA, ST_HITS_L, ST_COUNT
 };
 static_assert(ST_COUNT <= 32, "per-warp stat rows hold 32 counters");
 
@@ -883,7 +883,7 @@ __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev
     }
     atomicAdd(P.stats + ST_ITEMS_LARGE, (unsigned long long)items);
     atomicAdd(P.stats + ST_FP64, (unsigned long long)fp64);
-    atomicAdd(P.stats + ST_HITS, (unsigned long long)hits);
+    atomicAdd(P.stats + ST_HITS_L, (unsigned long long)hits);
 }
 
 __global__ void __launch_bounds__(256, K3_MINB) k_bin(const __grid_constant__ KParams P) {
@@ -1066,7 +1066,7 @@ __global__ void __launch_bounds__(K4_THREADS, K4_MINB) k_isect(const __grid_cons
                 r = test_exact_r(v, em_o(E), d, E.dmax, P.faces, th);
             }
             if (r == 1) {
-                cnt[ST_HITS]++;
+                cnt[ST_HITS_L]++;
                 record_hit(P.hits, kFast ? nullptr : P.mc_hits, kFast ? nullptr : P.allhits, g, th, id);
             }
         }
@@ -2157,7 +2157,8 @@ static grca_status fill_stats(grca_t h, grca_stats *s) {
     s->rtic_tested = (int64_t)(st[ST_ITEMS_SMALL] + st[ST_ITEMS_LARGE]);
     s->rtic_brute = (int64_t)(h->n_rays_own * ((h->have_tri ? h->n_tri : 0) + (h->st_set ? h->st_n : 0)));
     s->fp64_fallbacks = (int64_t)st[ST_FP64];
-    s->hits_recorded = (int64_t)st[ST_HITS];
+    s->hits_recorded = (int64_t)(st[ST_HITS] + st[ST_HITS_L]);
+    s->hits_large = (int64_t)st[ST_HITS_L];
     s->overflow_inline = (int64_t)(st[ST_OVF_LARGE] + st[ST_OVF_CHUNK]);
     s->prefilter_survivors = (int64_t)st[ST_K2SURV];
     s->rtic_small = (int64_t)st[ST_ITEMS_SMALL];

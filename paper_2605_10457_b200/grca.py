@@ -63,7 +63,7 @@ class Stats(C.Structure):
     _fields_ = [(n, C.c_int64) for n in (
         "pairs", "range_culled", "channel_culled", "azimuth_culled", "survivors", "small_pairs", "large_pairs",
         "chunks", "rtic_tested", "rtic_brute", "fp64_fallbacks", "hits_recorded", "overflow_inline",
-        "prefilter_survivors", "rtic_small", "sat_pairs", "bat_pairs", "area_culled")] + [
+        "prefilter_survivors", "rtic_small", "sat_pairs", "bat_pairs", "area_culled", "hits_large")] + [
         ("overflow", C.c_int32), ("ms_total", C.c_float), ("ms_k", C.c_float * 8)]
 
     def as_dict(self) -> dict:

@@ -19,7 +19,10 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
        "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
-       "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]
+       "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+       # L2 atomics / reductions (the closest-hit RED.MIN keys): sectors and requests
+       "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum", "lts__t_requests_op_red.sum",
+       "lts__t_sectors_op_red.sum.per_second", "smsp__inst_executed_op_global_red.sum"]
 
 
 def launches(path, out, cmd="bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-hybrid"):
