@@ -241,6 +241,22 @@ BYTES_K0_PER_RAY = 8
 BYTES_K5_PER_RAY = 16
 
 
+def ncu_traffic():
+    """DRAM bytes per launch from the latest committed `ncu --set full` capture (profiles/)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
+        return {}, None
+    d = json.load(open(files[-1]))
+    out = {}
+    for k, v in d.get("per_kernel", {}).items():
+        for ours, nm in NCU_NAME.items():
+            if nm in k:
+                out[ours] = v
+    return out, os.path.basename(files[-1])
+
+
 def measured_peaks():
     """Denominators measured live on this GPU (tools/peaks.cu: FFMA lane-instruction rate, u64 RED.MIN rate
     into an L2-resident 33.5 MB buffer) plus MEASURED_PEAKS.json's HBM copy bandwidth; the committed
@@ -339,6 +355,7 @@ def main():
                     help="triangle-shard merge inside grca_cast: NCCL all-reduce(MIN) of the packed keys, "
                          "reduce-scatter(MIN) (each rank keeps its ray slice; half the traffic), or the fused NVLS "
                          "multimem.red.min into an NCCL symmetric window (NEXT-f3; needs NVLS multicast)")
+    ap.add_argument("--graph", action="store_true", help="GRCA_USE_CUDA_GRAPH: each cast runs as one CUDA graph")
     ap.add_argument("--collective", action="store_true", help="N=1: cast through a one-rank NCCL communicator "
                     "(the library's collective path, merge included) instead of a plain handle")
     ap.add_argument("--soup", action="store_true", help="triangle-soup scene (float4 triplets) instead of the indexed "
@@ -409,6 +426,9 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev_index}"))
     device = torch.device(f"cuda:{dev_index}")
     torch.cuda.set_device(device)
+    # one non-default stream for everything (scene set-up, casts, events): a stream the library can capture
+    # into a CUDA graph (--graph), unlike the legacy default stream
+    torch.cuda.set_stream(torch.cuda.Stream(device))
     # --emulate-world W --emulate-rank R: this process does exactly rank R's share of a W-rank run
     # (its shard of the scene, no process group).  Valid for sensor shards, whose ranks never wait on
     # one another; tools/emulate_ranks.py runs every rank and takes the slowest (projected frame).
@@ -432,7 +452,7 @@ def main():
     n_rays = sg.n_rays_total(ems_lib)                   # output layout of the handle
     n_rays_job = sg.n_rays_total(scene.w["emitters"])
     mode_flags = ((G.DEBUG_SPLIT_REFINE if args.split_refine else 0) | (G.L2_PERSIST if args.l2_persist else 0)
-                  | (G.DEBUG_NO_PACKED if args.no_packed else 0))
+                  | (G.DEBUG_NO_PACKED if args.no_packed else 0) | (G.USE_CUDA_GRAPH if args.graph else 0))
     shard_mode = G.SHARD_EMITTERS if shard == "emitters" else G.SHARD_TRIANGLES
     merge_mode = {"allreduce": G.MERGE_ALLREDUCE, "reduce_scatter": G.MERGE_REDUCE_SCATTER, "nvls": G.MERGE_NVLS}[args.merge]
     coll_group, c_ranks, c_rank = None, 1, 0

@@ -63,6 +63,10 @@ enum {
                                        the fused refine+small kernel (A/B measurement, same results) */
     GRCA_DEBUG_NO_REFINE = 32u,     /* K3 keeps whole rectangle rows (no A7 per-channel refinement) */
     GRCA_DEBUG_NO_PACKED = 128u,    /* K2 without the packed fp32x2 (two-emitter) path (A/B) */
+    GRCA_USE_CUDA_GRAPH = 512u,      /* grca_cast runs its launch sequence as one CUDA graph (captured per cast,
+                                        cudaGraphExecUpdate'd in place; needs a non-NULL stream; ignored with
+                                        GRCA_PROFILE_KERNELS or inside a caller's stream capture, where the
+                                        cast's launches are recorded into the caller's graph instead) */
     GRCA_DEBUG_VIRTUAL_RANKS = 256u, /* nranks > 1 without nccl_uid: the handle casts exactly rank's share of the
                                         partition (shard_mode / merge as with a communicator) and writes the
                                         outputs that rank would write, but runs no collective (the caller merges;

@@ -1212,6 +1212,10 @@ struct grca_ctx {
     ncclWindow_t sym_win = nullptr;
     ncclDevComm sym_dc{};
     bool sym_dc_ok = false;
+    // GRCA_USE_CUDA_GRAPH: the cast's launch sequence as one executable graph, re-captured per cast and
+    // updated in place (cudaGraphExecUpdate: new pointers / sizes, same topology -> no re-instantiation)
+    cudaGraphExec_t gexec = nullptr;
+    long long graph_updates = 0, graph_instantiations = 0;
     // profiling ring
     cudaEvent_t ev[kRing][kEv];
     bool ev_ok = false;
@@ -1275,6 +1279,8 @@ void free_all(grca_t h) {
         ncclCommDestroy(h->comm);
         h->comm = nullptr;
     }
+    if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
     cudaFree(h->d_slice);
     cudaFree(h->d_scratch);
     cudaFree(h->d_raytab);   // (d_hits lives in the same allocation)
@@ -2205,11 +2211,59 @@ grca_status grca_unpack_range(grca_t h, const uint64_t *d_keys, int64_t first_ra
     return s;
 }
 
+// GRCA_USE_CUDA_GRAPH: capture K0..K5 (+ the in-stream collective) of this cast into a graph and launch it
+// as one unit.  The sequence is re-captured every cast (its parameters -- triangle pointers, counts, the
+// outputs, the cast index of the noise model -- may change) and applied to the existing executable with
+// cudaGraphExecUpdate, so only a change of topology (e.g. the hybrid static re-cast) re-instantiates.
+static grca_status cast_graph(grca_t h, float *d_out_dist, int32_t *d_out_tri) {
+    DeviceGuard dg(h->device);
+    cudaGraph_t gr = nullptr;
+    CK(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+    grca_status s = launch_packed(h);
+    if (s == GRCA_OK) s = launch_unpack(h, d_out_dist, d_out_tri);
+    const cudaError_t e = cudaStreamEndCapture(h->stream, &gr);
+    if (s != GRCA_OK || e != cudaSuccess) {
+        if (gr) cudaGraphDestroy(gr);
+        if (s != GRCA_OK) return s;
+        CK(e);
+    }
+    if (h->gexec) {
+        cudaGraphExecUpdateResultInfo info;
+        if (cudaGraphExecUpdate(h->gexec, gr, &info) != cudaSuccess) {
+            cudaGetLastError();
+            cudaGraphExecDestroy(h->gexec);
+            h->gexec = nullptr;
+        } else {
+            ++h->graph_updates;
+        }
+    }
+    if (!h->gexec) {
+        const cudaError_t ei = cudaGraphInstantiate(&h->gexec, gr, 0);
+        if (ei != cudaSuccess) {
+            cudaGraphDestroy(gr);
+            CK(ei);
+        }
+        ++h->graph_instantiations;
+    }
+    cudaGraphDestroy(gr);
+    CK(cudaGraphLaunch(h->gexec, h->stream));
+    return GRCA_OK;
+}
+
 grca_status grca_cast(grca_t h, float *d_out_dist, int32_t *d_out_tri, grca_stats *h_stats) {
     if (!h) return GRCA_E_INVALID;
-    grca_status s = launch_packed(h);
-    if (s != GRCA_OK) return s;
-    s = launch_unpack(h, d_out_dist, d_out_tri);
+    bool graph = (h->ci.debug_flags & GRCA_USE_CUDA_GRAPH) && !h->ev_ok && h->stream != nullptr;
+    if (graph) {   // inside a caller's own capture the launches are simply recorded into it
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(h->stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) graph = false;
+    }
+    grca_status s;
+    if (graph) {
+        s = cast_graph(h, d_out_dist, d_out_tri);
+    } else {
+        s = launch_packed(h);
+        if (s == GRCA_OK) s = launch_unpack(h, d_out_dist, d_out_tri);
+    }
     ++h->n_casts;
     if (s != GRCA_OK) return s;
     if (h_stats) return fill_stats(h, h_stats);

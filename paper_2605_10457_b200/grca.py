@@ -22,6 +22,7 @@ DEBUG_COUNT_ALL_HITS, DEBUG_NO_CULL, PROFILE_KERNELS, DEBUG_FORCE_FP64, DEBUG_SP
 L2_PERSIST = 64
 DEBUG_NO_PACKED = 128
 DEBUG_VIRTUAL_RANKS = 256
+USE_CUDA_GRAPH = 512
 SHARD_AUTO, SHARD_TRIANGLES, SHARD_EMITTERS = 0, 1, 2
 MERGE_ALLREDUCE, MERGE_REDUCE_SCATTER, MERGE_NVLS = 0, 1, 2
 

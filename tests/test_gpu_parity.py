@@ -926,3 +926,59 @@ def test_float3_vertices_identical():
     d, t = g.cast()
     torch.cuda.synchronize()
     assert np.array_equal(t.cpu().numpy(), a_t) and np.array_equal(d.cpu().numpy().view(np.uint32), a_d.view(np.uint32))
+
+
+def test_cuda_graph_cast_mode():
+    """GRCA_USE_CUDA_GRAPH: every cast runs as one CUDA graph (re-captured, cudaGraphExecUpdate'd in place);
+    over scene changes, an emitter change and the hybrid static path the results are bit-identical to the
+    plain launches."""
+    s = torch.cuda.Stream()
+    ems, tris = sg.random_scene(93, n_tris=1800, n_emitters=2, gamma=12, chi=160, extent=8.0)
+    ems2, tris2 = sg.random_scene(94, n_tris=1500, n_emitters=3, gamma=10, chi=128, extent=8.0)
+    n = max(sg.n_rays_total(ems), sg.n_rays_total(ems2))
+    g = Grca(device=0, stream=s, max_triangles=2000, max_rays=n, debug_flags=G.USE_CUDA_GRAPH)
+    with torch.cuda.stream(s):
+        for e, t in ((ems, tris), (ems, tris2), (ems2, tris2), (ems2, tris)):
+            ref = run(e, t)
+            got = run(e, t, handle=g)
+            assert np.array_equal(ref[1], got[1]) and np.array_equal(ref[0].view(np.uint32), got[0].view(np.uint32))
+        # hybrid: static triangles cached on the first cast, dynamic ones every cast
+        g.set_emitters(ems)
+        st4 = tris_to_float4(tris)
+        g.set_static_triangles(st4, tri_id_base=0)
+        g.update_triangles(tris_to_float4(tris2), tri_id_base=len(tris))
+        for _ in range(2):
+            d, t = g.cast()
+            s.synchronize()
+        both = np.concatenate([tris, tris2], 0)
+        ref = run(ems, both)
+        assert np.array_equal(ref[1], t.cpu().numpy())
+    g.close()
+
+
+def test_cast_is_capturable_by_the_caller():
+    """grca_cast allocates nothing and syncs nothing, so a caller can capture it into its own
+    CUDA graph (torch.cuda.graph on the handle's stream) and replay it after rewriting the borrowed
+    vertex buffer in place: each replay equals a plain cast of the new vertices."""
+    ems, tris = sg.random_scene(95, n_tris=1200, n_emitters=2, gamma=12, chi=128, extent=8.0)
+    _, tris_b = sg.random_scene(96, n_tris=1200, n_emitters=2, gamma=12, chi=128, extent=8.0)
+    s = torch.cuda.Stream()
+    g = Grca(device=0, stream=s, max_triangles=len(tris), max_rays=sg.n_rays_total(ems))
+    g.set_emitters(ems)
+    v4 = tris_to_float4(tris)
+    d = torch.empty(sg.n_rays_total(ems), device="cuda")
+    t = torch.empty(sg.n_rays_total(ems), dtype=torch.int32, device="cuda")
+    g.update_triangles(v4)
+    with torch.cuda.stream(s):
+        g.cast(d, t)   # warm-up outside the capture
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        g.cast(d, t)
+    for src in (tris_b, tris):
+        v4.copy_(tris_to_float4(src))
+        graph.replay()
+        torch.cuda.synchronize()
+        ref = run(ems, src)
+        assert np.array_equal(ref[1], t.cpu().numpy()) and np.array_equal(ref[0].view(np.uint32), d.cpu().numpy().view(np.uint32))
+    g.close()
