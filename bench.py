@@ -157,7 +157,7 @@ class Scene:
             # 12 B per shared float3 vertex
             self.tri_bytes = self.n_static_local * 48 + len(self.own_dyn) * 12 + self.n_dyn_vert * 12
         else:
-            self.car_np = np.asarray(w["car_local"], dtype=np.float32)   # (m, 3, 3) local
+            self.car_np = np.asarray(w.get("car_local", np.zeros((0, 3, 3))), dtype=np.float32)   # (m, 3, 3) local
             self.tri_bytes = self.n_tri * 48
         # frame buffers: soup = [static | dynamic] float4 rows; indexed = the car vertices only
         self.fs = 0 if self.indexed else self.ns3   # static rows at the head of a frame buffer
