@@ -41,6 +41,12 @@ def nvcc() -> str:
     return "nvcc"
 
 
+def build_variant(out: str, defines: list) -> str:
+    """A/B build (tools/ab.py): the same sources with extra -D macros, to `out`."""
+    subprocess.check_call([nvcc()] + NVCC_FLAGS + [f"-D{d}" for d in defines] + SRC + ["-o", out])
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     stale = force or not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS)
     if stale:

@@ -41,6 +41,9 @@ constexpr int K4_THREADS = 256;
 #ifndef KF_MINB
 #define KF_MINB 2
 #endif
+#ifndef KF_FETCH
+#define KF_FETCH 1   // 32-survivor rounds per dynamic fetch of the fused kernel
+#endif
 #ifndef K3_MINB
 #define K3_MINB 2   // 128 registers (without a bound the compiler took 145: K3 0.028 -> 0.041 ms)
 #endif
@@ -833,18 +836,22 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
     // both paths run the same certified test).  C4: ~56 rounds/warp -> small_max; C2: ~1 -> 64.
     const unsigned rpw = nr / (gridDim.x * (KF_THREADS / 32));
     const int smax = min(P.small_max, (int)max(64u, min(rpw, 1024u) * 16u));
-    // dynamic round fetching (one global atomic per warp per round): no tail imbalance
+    // dynamic round fetching (one global atomic per warp per KF_FETCH rounds): no tail imbalance
     unsigned w = 0;
     if (lane == 0) w = atom_add_u32(P.n_surv + 2, 1u);
-    w = __shfl_sync(FULL, w, 0);
+    w = __shfl_sync(FULL, w, 0) * KF_FETCH;
     for (; w < nr;) {
         unsigned wn = 0;
-        if (lane == 0) wn = atom_add_u32(P.n_surv + 2, 1u);   // next round, fetched early (latency hidden)
-        const unsigned idx = w * 32u + (unsigned)lane;
-        const bool valid = idx < ns;
-        refine_round<kFast, kLevel>(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
-                     valid ? __ldcs(P.surv + idx) : 0ull);
-        w = __shfl_sync(FULL, wn, 0);
+        if (lane == 0) wn = atom_add_u32(P.n_surv + 2, 1u);   // next group, fetched early (latency hidden)
+#pragma unroll 1
+        for (int f = 0; f < KF_FETCH; ++f) {
+            const unsigned idx = (w + f) * 32u + (unsigned)lane;
+            const bool valid = idx < ns;
+            if (!__any_sync(FULL, valid)) break;
+            refine_round<kFast, kLevel>(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
+                                        valid ? __ldcs(P.surv + idx) : 0ull);
+        }
+        w = __shfl_sync(FULL, wn, 0) * KF_FETCH;
     }
     __syncthreads();
     if (threadIdx.x < ST_COUNT) {   // block total of each counter, one global atomic each

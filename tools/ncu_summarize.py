@@ -21,8 +21,9 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
        "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
        "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
        # L2 atomics / reductions (the closest-hit RED.MIN keys): sectors and requests
-       "lts__t_sectors_op_red.sum", "lts__t_sectors_op_atom.sum", "lts__t_requests_op_red.sum",
-       "lts__t_sectors_op_red.sum.per_second", "smsp__inst_executed_op_global_red.sum"]
+       "lts__t_sectors_srcunit_tex_op_red.sum", "lts__t_requests_srcunit_tex_op_red.sum",
+       "lts__t_sectors_srcunit_tex_op_red.sum.pct_of_peak_sustained_elapsed",
+       "lts__t_sectors_srcunit_tex_op_atom.sum", "smsp__inst_executed_op_global_red.sum"]
 
 
 def launches(path, out, cmd="bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-hybrid"):
@@ -38,7 +39,8 @@ def launches(path, out, cmd="bench.py --steps 5 --warmup 3 --no-cpu-baseline --n
     for d in data:
         name = d["Kernel Name"].split("(")[0]
         agg.setdefault(name, []).append(float(d["Metric Value"]))
-    ours = {k: v for k, v in agg.items() if re.match(r"(void )?(grca::)?k_", k)}
+    # the library's kernels (namespace grca); bench.py's measured-peak microbenchmarks (tools/peaks.cu) excluded
+    ours = {k: v for k, v in agg.items() if re.match(r"(void )?grca::k_", k)}
     med = {k: sorted(v)[len(v) // 2] for k, v in ours.items()}
     step_ns = sum(med.values())
     lines = [f"# ncu launch list ({path.split('/')[-1]})", "",
