@@ -42,7 +42,11 @@ constexpr int K4_THREADS = 256;
 #define KF_MINB 2
 #endif
 #ifndef KF_FETCH
-#define KF_FETCH 1   // 32-survivor rounds per dynamic fetch of the fused kernel
+#define KF_FETCH 2   // 32-survivor rounds per dynamic fetch of the fused kernel (measured: 1 -> 1.048, 2 -> 1.033,
+                     // 4 -> 1.121 ms at C4: half the fetch atomics vs a coarser tail)
+#endif
+#ifndef KF_PREFETCH
+#define KF_PREFETCH 0   // fused item loop: issue the next step's ray load before this step's test
 #endif
 #ifndef K3_MINB
 #define K3_MINB 2   // 128 registers (without a bound the compiler took 145: K3 0.028 -> 0.041 ms)
@@ -740,19 +744,17 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
     // one candidate per lane per iteration: resolve the owner (binary search of the inclusive
     // scan), the ray index, then the certified test (scalar state only: nothing to local memory)
     unsigned hw = 0u, fw = 0u;
-    for (int b = 0; b < total; b += 32) {
-        const int qi = b + lane;
-        int ow = 0;
+    // owner lane of item qi (binary search of the inclusive scan) and its global ray index g
+    auto resolve = [&](int qi, int &ow, int &g) {
+        ow = 0;
 #pragma unroll
         for (int s = 16; s > 0; s >>= 1) {
             const int vv = __shfl_sync(FULL, incl, ow + s - 1);
             if (vv <= qi) ow += s;
         }
-        bool hit = false, fb = false;
+        g = 0;
         if (qi < total) {
             const float4 r5 = slot[5 * 32 + ow];
-            const float4 r4 = slot[4 * 32 + ow];
-            const EmDev &EO = sE[__float_as_int(r4.w)];
             const int local = qi - excl[ow];
             const unsigned lc = __float_as_uint(r5.z);
             const int len = (int)(lc & 0xffffu), chi = (int)(lc >> 16);
@@ -760,8 +762,38 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             int col = local - row * len;
             if (col < 0) { --row; col += len; }
             if (col >= len) { ++row; col -= len; }
-            const int g = __float_as_int(r5.x) + row * chi + col - (col >= __float_as_int(r5.y) ? chi : 0);
+            g = __float_as_int(r5.x) + row * chi + col - (col >= __float_as_int(r5.y) ? chi : 0);
+        }
+    };
+#if KF_PREFETCH
+    // software-pipelined: the next step's owner, ray index and ray load are issued before this step's test
+    int ow_n = 0, g_n = 0;
+    float4 d_n = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (total > 0) {
+        resolve(lane, ow_n, g_n);
+        if (lane < total) d_n = __ldg(P.raytab + g_n);
+    }
+#endif
+    for (int b = 0; b < total; b += 32) {
+        const int qi = b + lane;
+#if KF_PREFETCH
+        const int ow = ow_n, g = g_n;
+        const float4 d = d_n;
+        if (b + 32 < total) {
+            resolve(qi + 32, ow_n, g_n);
+            if (qi + 32 < total) d_n = __ldg(P.raytab + g_n);
+        }
+#else
+        int ow, g;
+        resolve(qi, ow, g);
+#endif
+        bool hit = false, fb = false;
+        if (qi < total) {
+            const float4 r4 = slot[4 * 32 + ow];
+            const EmDev &EO = sE[__float_as_int(r4.w)];
+#if !KF_PREFETCH
             const float4 d = __ldg(P.raytab + g);
+#endif
             const float4 r0 = slot[0 * 32 + ow], r1 = slot[1 * 32 + ow], r2 = slot[2 * 32 + ow],
                          r3 = slot[3 * 32 + ow];
             Setup Q;
