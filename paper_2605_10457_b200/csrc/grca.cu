@@ -92,6 +92,7 @@ struct KParams {
     const EmLite *lite;
     const unsigned char *lut;    // NULL -> binary search
     unsigned long long *surv;    // dense K2 survivor list: tri << 8 | emitter
+    long long cap_surv;          // its capacity (entries)
     unsigned *n_surv;
     unsigned long long *desc;    // split path: per survivor, small-rectangle descriptor (0 = none)
     unsigned long long *mc_hits; // NEXT-f3: multicast view of the ranks' hit buffers (NULL = local RED.MIN)
@@ -366,7 +367,12 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
         }
         if (threadIdx.x == 0) qbase = total ? atomicAdd(P.n_surv, (unsigned)total) : 0u;   // one atomic per tile
         __syncthreads();
+#ifdef GRCA_CHECK
+        chk_idx((long long)qbase + wbase + incl - 1, P.cap_surv, CHK_SURV_WRITE);   // this thread's last entry
+        unsigned long long *dst = P.surv + chk_idx((long long)qbase + wbase + incl - cntk, P.cap_surv, CHK_SURV_WRITE);
+#else
         unsigned long long *dst = P.surv + qbase + wbase + incl - cntk;
+#endif
 #pragma unroll
         for (int h = 0; h < K2_TILE / K2_THREADS; ++h) {
             const long long t = tile * K2_TILE + h * K2_THREADS + threadIdx.x;
@@ -615,7 +621,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KP
                     int i = __float_as_int(sl[SF_RLO * 32]) + col;
                     if (i >= EO.chi) i -= EO.chi;
                     const int g = EO.ray_base + j * EO.chi + i;
-                    const float4 d = __ldg(P.raytab + g);
+                    const float4 d = __ldg(P.raytab + chk_idx(g, P.n_rays, CHK_RAY));
                     Setup Q;
                     Q.n0 = {sl[(SF_N0 + 0) * 32], sl[(SF_N0 + 1) * 32], sl[(SF_N0 + 2) * 32]};
                     Q.n1 = {sl[(SF_N1 + 0) * 32], sl[(SF_N1 + 1) * 32], sl[(SF_N1 + 2) * 32]};
@@ -771,7 +777,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
     float4 d_n = make_float4(0.f, 0.f, 0.f, 0.f);
     if (total > 0) {
         resolve(lane, ow_n, g_n);
-        if (lane < total) d_n = __ldg(P.raytab + g_n);
+        if (lane < total) d_n = __ldg(P.raytab + chk_idx(g_n, P.n_rays, CHK_RAY));
     }
 #endif
     for (int b = 0; b < total; b += 32) {
@@ -781,7 +787,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
         const float4 d = d_n;
         if (b + 32 < total) {
             resolve(qi + 32, ow_n, g_n);
-            if (qi + 32 < total) d_n = __ldg(P.raytab + g_n);
+            if (qi + 32 < total) d_n = __ldg(P.raytab + chk_idx(g_n, P.n_rays, CHK_RAY));
         }
 #else
         int ow, g;
@@ -792,7 +798,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             const float4 r4 = slot[4 * 32 + ow];
             const EmDev &EO = sE[__float_as_int(r4.w)];
 #if !KF_PREFETCH
-            const float4 d = __ldg(P.raytab + g);
+            const float4 d = __ldg(P.raytab + chk_idx(g, P.n_rays, CHK_RAY));
 #endif
             const float4 r0 = slot[0 * 32 + ow], r1 = slot[1 * 32 + ow], r2 = slot[2 * 32 + ow],
                          r3 = slot[3 * 32 + ow];
@@ -810,7 +816,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             if (r == 2) {   // rare: reload the ray (keeping d live into the fp64 code spills it)
                 f3 wv[3];
                 load_tri(P.tri, (long long)__float_as_int(r4.z), wv);
-                const float4 d2 = __ldcg(P.raytab + g);
+                const float4 d2 = __ldcg(P.raytab + chk_idx(g, P.n_rays, CHK_RAY));
                 r = test_exact_r<true>(wv, em_o(EO), d2, EO.dmax, P.faces, th);
             }
             if (r == 1) {
@@ -912,7 +918,7 @@ __device__ __noinline__ void intersect_rect_serial(const KParams &P, const EmDev
                 int i = lo + c;
                 if (i >= E.chi) i -= E.chi;
                 const int g = E.ray_base + (row0 + r) * E.chi + i;
-                const float4 d = __ldg(P.raytab + g);
+                const float4 d = __ldg(P.raytab + chk_idx(g, P.n_rays, CHK_RAY));
                 float th;
                 ++items;
                 int res = P.force64 ? 2 : test_fast(d, S, E.dmax_lo, E.dmax_hi, th);
@@ -1088,13 +1094,13 @@ __global__ void __launch_bounds__(K4_THREADS, K4_MINB) k_isect(const __grid_cons
         };
         // software-pipelined: the next item's ray is in flight while this one is tested
         int gn = lane < items ? ray_of(lane) : 0;
-        float4 dn = lane < items ? __ldg(P.raytab + gn) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 dn = lane < items ? __ldg(P.raytab + chk_idx(gn, P.n_rays, CHK_RAY)) : make_float4(0.f, 0.f, 0.f, 0.f);
         for (int q = lane; q < items; q += 32) {
             const int g = gn;
             const float4 d = dn;
             if (q + 32 < items) {
                 gn = ray_of(q + 32);
-                dn = __ldg(P.raytab + gn);
+                dn = __ldg(P.raytab + chk_idx(gn, P.n_rays, CHK_RAY));
             }
             float th = 0.f;
             int r = (!kFast && P.force64) ? 2 : test_fast(d, S, E.dmax_lo, E.dmax_hi, th);
@@ -1417,6 +1423,7 @@ KParams params(grca_t h) {
     P.lite = h->d_lite;
     P.lut = h->use_lut ? h->d_lut : nullptr;
     P.surv = h->d_surv;
+    P.cap_surv = h->surv_cap_tiles * K2_THREADS * h->surv_n_em;
     P.desc = h->d_desc;
     return P;
 }
@@ -1450,7 +1457,11 @@ static size_t kfused_smem_bytes(int n_em, int n_sin, bool lut) {
 
 extern "C" {
 
-const char *grca_version(void) { return "grca-b200 0.1 (sm_100a)"; }
+#ifdef GRCA_CHECK
+const char *grca_version(void) { return "grca-b200 0.2 (sm_100a, bounds-checked build)"; }
+#else
+const char *grca_version(void) { return "grca-b200 0.2 (sm_100a)"; }
+#endif
 
 const char *grca_last_error(grca_t h) { return h ? h->err.c_str() : g_create_err.c_str(); }
 
@@ -1920,6 +1931,8 @@ grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_v
     h->tri.idx = d_indices;
     h->tri.ids = d_tri_ids;
     h->tri.id_base = tri_id_base;
+    h->tri.n_v = n_vertices;
+    h->tri.n_t = n_triangles;
     h->n_tri = n_triangles;
     h->have_tri = true;
     return GRCA_OK;
@@ -1937,6 +1950,8 @@ grca_status grca_update_triangles_f3(grca_t h, const float *d_xyz, int64_t n_ver
     h->tri.idx = d_indices;
     h->tri.ids = d_tri_ids;
     h->tri.id_base = tri_id_base;
+    h->tri.n_v = n_vertices;
+    h->tri.n_t = n_triangles;
     h->n_tri = n_triangles;
     h->have_tri = true;
     return GRCA_OK;
@@ -1963,6 +1978,8 @@ grca_status grca_update_scene(grca_t h, const float *d_soup, int64_t n_soup_tria
     h->tri.idx = d_mesh_indices;
     h->tri.ids = d_tri_ids;
     h->tri.id_base = tri_id_base;
+    h->tri.n_v = n_mesh_vertices;
+    h->tri.n_t = n_soup_triangles + n_mesh_triangles;
     h->n_tri = n_soup_triangles + n_mesh_triangles;
     h->have_tri = true;
     return GRCA_OK;
@@ -1980,6 +1997,8 @@ grca_status grca_set_static_triangles(grca_t h, const float *d_vertices, int64_t
     h->st_tri.idx = d_indices;
     h->st_tri.ids = d_tri_ids;
     h->st_tri.id_base = tri_id_base;
+    h->st_tri.n_v = n_vertices;
+    h->st_tri.n_t = n_triangles;
     h->st_n = n_triangles;
     h->st_set = true;
     h->st_dirty = true;
@@ -2084,6 +2103,12 @@ static cudaError_t nvls_barrier(grca_t h) {
 
 static grca_status launch_packed(grca_t h) {
     if (h->n_em_global < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
+#ifdef GRCA_CHECK
+    {
+        const long long nr = h->n_rays;
+        CK(cudaMemcpyToSymbolAsync(g_check_n_rays, &nr, sizeof(nr), 0, cudaMemcpyHostToDevice, h->stream));
+    }
+#endif
     if (!h->have_tri && !h->st_set) return fail(h, GRCA_E_STATE, "grca_update_triangles has not been called");
     if (h->nvls_mc && h->st_set)
         return fail(h, GRCA_E_STATE, "the fused NVLS merge cannot be combined with cached static triangles");
@@ -2305,6 +2330,18 @@ grca_status grca_cast(grca_t h, float *d_out_dist, int32_t *d_out_tri, grca_stat
     }
     ++h->n_casts;
     if (s != GRCA_OK) return s;
+#ifdef GRCA_CHECK
+    {   // bounds-checked build: every cast is checked before it returns
+        unsigned mask = 0;
+        CK(cudaStreamSynchronize(h->stream));
+        CK(cudaMemcpyFromSymbol(&mask, g_check_err, sizeof(mask)));
+        if (mask) {
+            const unsigned zero = 0;
+            cudaMemcpyToSymbol(g_check_err, &zero, sizeof(zero));
+            return fail(h, GRCA_E_CUDA, "bounds check failed, site mask " + std::to_string(mask));
+        }
+    }
+#endif
     if (h_stats) return fill_stats(h, h_stats);
     return GRCA_OK;
 }

@@ -20,6 +20,24 @@
 
 namespace grca {
 
+// Bounds-checked build (-DGRCA_CHECK; tools/check_build.py): every global index of the hot path is checked
+// against its buffer's extent; a violation sets bit `site` of g_check_err and the access is redirected to
+// index 0 (no fault), and grca_cast reports the mask.  The product build compiles the checks away.
+#ifdef GRCA_CHECK
+__device__ unsigned g_check_err;
+__device__ __forceinline__ long long chk_idx(long long i, long long n, int site) {
+    if (i < 0 || i >= n) {
+        atomicOr(&g_check_err, 1u << site);
+        return 0;
+    }
+    return i;
+}
+#else
+__device__ __forceinline__ long long chk_idx(long long i, long long, int) { return i; }
+#endif
+enum { CHK_SURV_WRITE = 0, CHK_RAY = 1, CHK_VERTEX = 2, CHK_SURV_READ = 3, CHK_LARGE = 4, CHK_CHUNK = 5,
+       CHK_TRI = 6 };
+
 constexpr float kU = 5.9604644775390625e-8f;   // 2^-24, unit roundoff of fp32
 constexpr float kPadS = 4e-6f;                 // sin(elevation) padding (>> 3u ray rounding)
 constexpr float kPadTheta = 5e-5f;             // azimuth padding in radians
@@ -143,11 +161,16 @@ struct TriSrc {
     const uint32_t *idx;   // NULL -> non-indexed triplets
     const int32_t *ids;    // NULL -> id_base + local (global triangle index, parts A and B alike)
     int32_t id_base;
+    long long n_v;         // vertices of part B (bounds-checked build only)
+    long long n_t;         // triangles of parts A + B (bounds-checked build only)
 };
 __device__ __forceinline__ f3 ldcs3(const float *p) { return {__ldcs(p), __ldcs(p + 1), __ldcs(p + 2)}; }
 // Streaming (evict-first) loads: the ~1 GB triangle stream must not evict the L2-resident ray
 // table (67 MB at C4) and hit buffer (33.5 MB) that the intersection kernels gather from.
 __device__ __forceinline__ void load_tri(const TriSrc &T, long long t, f3 v[3]) {
+#ifdef GRCA_CHECK
+    t = chk_idx(t, T.n_t, CHK_TRI);
+#endif
     if (t < T.n_a) {   // part A: float4 triplets, no indirection (static scenery)
         v[0] = mk(__ldcs(T.va + 3 * t));
         v[1] = mk(__ldcs(T.va + 3 * t + 1));
@@ -156,7 +179,13 @@ __device__ __forceinline__ void load_tri(const TriSrc &T, long long t, f3 v[3]) 
     }
     t -= T.n_a;
     if (T.idx) {
+#ifdef GRCA_CHECK
+        const uint32_t i0 = (uint32_t)chk_idx(__ldcs(T.idx + 3 * t), T.n_v, CHK_VERTEX),
+                       i1 = (uint32_t)chk_idx(__ldcs(T.idx + 3 * t + 1), T.n_v, CHK_VERTEX),
+                       i2 = (uint32_t)chk_idx(__ldcs(T.idx + 3 * t + 2), T.n_v, CHK_VERTEX);
+#else
         const uint32_t i0 = __ldcs(T.idx + 3 * t), i1 = __ldcs(T.idx + 3 * t + 1), i2 = __ldcs(T.idx + 3 * t + 2);
+#endif
         if (T.v3) {
             v[0] = ldcs3(T.v3 + 3ll * i0);
             v[1] = ldcs3(T.v3 + 3ll * i1);
@@ -918,9 +947,15 @@ __device__ __forceinline__ int test_exact_r(const f3 v[3], f3 o, float4 d4, doub
 // mc != NULL (NEXT-f3 fused NVLS merge): the key goes to the multicast address of the ranks' hit
 // buffers, and the NVSwitch applies the min to every rank's copy (multimem.red: no separate
 // all-reduce).  Otherwise a local RED.MIN.
+#ifdef GRCA_CHECK
+__device__ long long g_check_n_rays;   // rays of the current cast (set by the host before each cast)
+#endif
 __device__ __forceinline__ void record_hit(unsigned long long *hits, unsigned long long *mc, unsigned *allhits, int g,
                                            float t, uint32_t id) {
     const unsigned long long key = ((unsigned long long)__float_as_uint(t) << 32) | id;
+#ifdef GRCA_CHECK
+    g = (int)chk_idx(g, g_check_n_rays, CHK_RAY);
+#endif
     if (allhits) atomicAdd(allhits + g, 1u);
     if (mc)
         asm volatile("multimem.red.relaxed.sys.global.min.u64 [%0], %1;" ::"l"(mc + g), "l"(key) : "memory");
