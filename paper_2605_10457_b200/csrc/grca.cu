@@ -325,6 +325,36 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
     rng = rb;
 }
 
+#ifndef K2_L2PF
+#define K2_L2PF 0   // K2: bulk L2 prefetch of the block's next tile (cp.async.bulk.prefetch.L2, evict-first)
+#endif
+// One-instruction L2 prefetch of [p, p + bytes) (16-byte aligned, multiple of 16), evict-first like the
+// streaming loads that consume it (the ray table and hit keys stay L2-resident).
+__device__ __forceinline__ void l2_prefetch_bulk(const void *p, unsigned bytes) {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
+                 : "memory");
+}
+// The triangle-stream bytes of K2 tile `tile` (float4 soup part and index part) pulled into L2 ahead of use.
+__device__ __forceinline__ void k2_prefetch_tile(const KParams &P, long long tile) {
+    const long long t0 = tile * K2_TILE, t1 = min(t0 + K2_TILE, P.n_tri);
+    if (t0 >= t1) return;
+    const TriSrc &T = P.tri;
+    const long long a1 = min(t1, T.n_a);
+    if (t0 < a1) l2_prefetch_bulk(T.va + 3 * t0, (unsigned)(48 * (a1 - t0)));
+    const long long b0 = max(t0, T.n_a) - T.n_a, b1 = t1 - T.n_a;
+    if (b0 < b1) {
+        if (T.idx) {   // 12 B per triangle: widen to 16-byte boundaries
+            const uintptr_t lo = reinterpret_cast<uintptr_t>(T.idx + 3 * b0) & ~(uintptr_t)15;
+            const uintptr_t hi = (reinterpret_cast<uintptr_t>(T.idx + 3 * b1) + 15) & ~(uintptr_t)15;
+            l2_prefetch_bulk(reinterpret_cast<const void *>(lo), (unsigned)(hi - lo));
+        } else if (T.v) {
+            l2_prefetch_bulk(T.v + 3 * b0, (unsigned)(48 * (b1 - b0)));
+        }
+    }
+}
+
 // The persistent tile loop of k_cull_fixed (one instantiation per mode, see k2_tri).
 template <int NE, bool kLevel, bool kFast>
 __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL, const float *sSin,
@@ -333,6 +363,9 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
                                          unsigned &c_area) {
     const long long ntiles = (P.n_tri + K2_TILE - 1) / K2_TILE;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+#if K2_L2PF
+        if (threadIdx.x == 0) k2_prefetch_tile(P, tile + gridDim.x);
+#endif
         // K2_TILE / K2_THREADS triangles per thread (one block scan, barrier pair and atomic for all)
         unsigned keeps[K2_TILE / K2_THREADS];
         int cntk = 0;

@@ -44,7 +44,7 @@ def main():
         else:
             names.append(args[i]); i += 1
     res = {n: [] for n in names}
-    kms = {}
+    kms, sts = {}, {}
     for p in range(passes):
         for n in names:
             env = dict(os.environ, GRCA_LIB=os.path.join(OUT, f"lib_{n}.so"))
@@ -59,9 +59,17 @@ def main():
             d = json.loads(line[-1])
             res[n].append(d["ms_per_step"])
             kms[n] = d["kernel_ms"]
+            sts[n] = {k: d["stats"][k] for k in ("prefilter_survivors", "survivors", "hits_recorded")}
             print(f"pass {p} {n}: {d['ms_per_step']:.4f} ms", flush=True)
     for n in names:
         print(f"{n:16s} ms/frame {res[n]}  kernels " + " ".join(f"{k}={v:.4f}" for k, v in kms.get(n, {}).items()))
+    # a variant must do the same work (culling is exact-conservative: survivors may only grow, hits never change)
+    ref = sts.get(names[0])
+    for n in names[1:]:
+        if ref and n in sts and sts[n]["hits_recorded"] != ref["hits_recorded"]:
+            print(f"WARNING {n}: hits_recorded {sts[n]['hits_recorded']} != {ref['hits_recorded']} ({names[0]})")
+        if ref and n in sts:
+            print(f"{n}: stats {sts[n]} vs {names[0]} {ref}")
 
 
 if __name__ == "__main__":
