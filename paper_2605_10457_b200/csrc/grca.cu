@@ -401,7 +401,7 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
         if (threadIdx.x == 0) qbase = total ? atomicAdd(P.n_surv, (unsigned)total) : 0u;   // one atomic per tile
         __syncthreads();
 #ifdef GRCA_CHECK
-        chk_idx((long long)qbase + wbase + incl - 1, P.cap_surv, CHK_SURV_WRITE);   // this thread's last entry
+        if (cntk) chk_idx((long long)qbase + wbase + incl - 1, P.cap_surv, CHK_SURV_WRITE);   // this thread's last entry
         unsigned long long *dst = P.surv + chk_idx((long long)qbase + wbase + incl - cntk, P.cap_surv, CHK_SURV_WRITE);
 #else
         unsigned long long *dst = P.surv + qbase + wbase + incl - cntk;

@@ -632,7 +632,8 @@ def test_a7_c1_and_fixtures():
     a7 = run(ems, tris, small_max=1, flags=G.DEBUG_COUNT_ALL_HITS)
     oref = oracle.cast(ems, tris, want_t64=True, want_allhits=True)
     check(ems, tris, a7[0], a7[1], ref=oref)
-    _check_all_hits(ems, tris, a7[3].debug_all_hits().cpu().numpy(), oref)
+    # (C1's ground grid lines under the emitter: 14 rays along shared edges, see test_all_hits_invariant)
+    _check_all_hits(ems, tris, a7[3].debug_all_hits().cpu().numpy(), oref, bound=2e-3)
 
 
 def test_hybrid_static_dynamic_exact():
@@ -999,10 +1000,9 @@ def _exact_rect(em, tri, n=400):
     chans = np.nonzero((phi >= elev.min()) & (phi <= elev.max()))[0]
     chi = em.rays_per_channel
     dth = 2 * np.pi / chi
-    th0 = -(chi // 2) * dth
-    idx = np.round((az - th0) / dth).astype(int) % chi
-    wraps = bool(idx.min() == 0 and idx.max() == chi - 1) or (az.max() - az.min() > np.pi)
-    span = len(np.unique(idx))
+    th = -(chi // 2) * dth + dth * np.arange(chi)   # ray azimuths (ray i = chi/2 is theta = 0)
+    wraps = bool(az.max() - az.min() > np.pi)      # the arc crosses theta = +-pi (the seam)
+    span = int(np.count_nonzero((th >= az.min()) & (th <= az.max())))
     return len(chans), span, wraps
 
 
@@ -1016,7 +1016,7 @@ def test_sat_bat_classification():
     assert st["sat_pairs"] + st["bat_pairs"] == st["survivors"] > 0
     em = sg.Emitter(origin=(0.0, 0.0, 0.0), elev=sg.full_sphere_elev(128), rays_per_channel=512)
     cases = {
-        "tiny far": [[20.0, 0.3, -0.03], [20.0, 0.35, -0.03], [20.0, 0.3, 0.03]],
+        "tiny far": [[20.0, -0.05, -0.03], [20.0, 0.05, -0.03], [20.0, 0.0, 0.03]],
         "mid wall": [[5.0, -1.0, -1.0], [5.0, 1.0, -1.0], [5.0, 0.0, 1.0]],
         "wide wall": [[2.0, -4.0, 0.1], [2.0, 4.0, 0.1], [2.0, 0.0, 0.3]],
         "tall wall": [[2.0, -0.1, -4.0], [2.0, 0.1, -4.0], [2.0, 0.0, 4.0]],
