@@ -45,6 +45,9 @@ constexpr int K4_THREADS = 256;
 #define KF_FETCH 2   // 32-survivor rounds per dynamic fetch of the fused kernel (measured: 1 -> 1.048, 2 -> 1.033,
                      // 4 -> 1.121 ms at C4: half the fetch atomics vs a coarser tail)
 #endif
+#ifndef KF_SMAX_MUL
+#define KF_SMAX_MUL 16   // fused kernel: small-rectangle cap = max(64, rounds per warp x this) (<= small_max)
+#endif
 #ifndef KF_PREFETCH
 #define KF_PREFETCH 0   // fused item loop: issue the next step's ray load before this step's test
 #endif
@@ -127,7 +130,8 @@ __device__ __forceinline__ void block_flush(unsigned long long *acc_smem, unsign
 
 // ------------------------------------------------------------------- K0 init --
 __global__ void k_init(unsigned long long *hits, unsigned *allhits, long long n, unsigned *ctrl,
-                       unsigned long long *stats, const unsigned long long *src, const unsigned *src_allhits) {
+                       unsigned long long *stats, const unsigned long long *src, const unsigned *src_allhits,
+                       int reset = 1) {
     // hits = MISS, or the cached static-scene keys (hybrid mode, NEXT-f2)
     const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long stride = (long long)gridDim.x * blockDim.x;
@@ -143,8 +147,8 @@ __global__ void k_init(unsigned long long *hits, unsigned *allhits, long long n,
     }
     if (allhits)
         for (long long i = tid; i < n; i += stride) allhits[i] = src_allhits ? src_allhits[i] : 0u;
-    if (tid < ST_COUNT) stats[tid] = 0ull;
-    if (tid < 7) ctrl[tid] = 0u;   // (ctrl[7]: sticky NVLS barrier timeout flag)
+    if (reset && tid < ST_COUNT) stats[tid] = 0ull;
+    if (reset && tid < 7) ctrl[tid] = 0u;   // (ctrl[7]: sticky NVLS barrier timeout flag)
 }
 
 // NEXT-f3 device-side barrier over the NVLS group (one thread): every rank adds 1 to every rank's
@@ -325,36 +329,6 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
     rng = rb;
 }
 
-#ifndef K2_L2PF
-#define K2_L2PF 0   // K2: bulk L2 prefetch of the block's next tile (cp.async.bulk.prefetch.L2, evict-first)
-#endif
-// One-instruction L2 prefetch of [p, p + bytes) (16-byte aligned, multiple of 16), evict-first like the
-// streaming loads that consume it (the ray table and hit keys stay L2-resident).
-__device__ __forceinline__ void l2_prefetch_bulk(const void *p, unsigned bytes) {
-    unsigned long long pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p), "r"(bytes), "l"(pol)
-                 : "memory");
-}
-// The triangle-stream bytes of K2 tile `tile` (float4 soup part and index part) pulled into L2 ahead of use.
-__device__ __forceinline__ void k2_prefetch_tile(const KParams &P, long long tile) {
-    const long long t0 = tile * K2_TILE, t1 = min(t0 + K2_TILE, P.n_tri);
-    if (t0 >= t1) return;
-    const TriSrc &T = P.tri;
-    const long long a1 = min(t1, T.n_a);
-    if (t0 < a1) l2_prefetch_bulk(T.va + 3 * t0, (unsigned)(48 * (a1 - t0)));
-    const long long b0 = max(t0, T.n_a) - T.n_a, b1 = t1 - T.n_a;
-    if (b0 < b1) {
-        if (T.idx) {   // 12 B per triangle: widen to 16-byte boundaries
-            const uintptr_t lo = reinterpret_cast<uintptr_t>(T.idx + 3 * b0) & ~(uintptr_t)15;
-            const uintptr_t hi = (reinterpret_cast<uintptr_t>(T.idx + 3 * b1) + 15) & ~(uintptr_t)15;
-            l2_prefetch_bulk(reinterpret_cast<const void *>(lo), (unsigned)(hi - lo));
-        } else if (T.v) {
-            l2_prefetch_bulk(T.v + 3 * b0, (unsigned)(48 * (b1 - b0)));
-        }
-    }
-}
-
 // The persistent tile loop of k_cull_fixed (one instantiation per mode, see k2_tri).
 template <int NE, bool kLevel, bool kFast>
 __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL, const float *sSin,
@@ -363,9 +337,6 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
                                          unsigned &c_area) {
     const long long ntiles = (P.n_tri + K2_TILE - 1) / K2_TILE;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-#if K2_L2PF
-        if (threadIdx.x == 0) k2_prefetch_tile(P, tile + gridDim.x);
-#endif
         // K2_TILE / K2_THREADS triangles per thread (one block scan, barrier pair and atomic for all)
         unsigned keeps[K2_TILE / K2_THREADS];
         int cntk = 0;
@@ -906,23 +877,25 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
     // kernel's tail, so big rectangles go to the chunk-balanced K3/K4 path instead (same results:
     // both paths run the same certified test).  C4: ~56 rounds/warp -> small_max; C2: ~1 -> 64.
     const unsigned rpw = nr / (gridDim.x * (KF_THREADS / 32));
-    const int smax = min(P.small_max, (int)max(64u, min(rpw, 1024u) * 16u));
-    // dynamic round fetching (one global atomic per warp per KF_FETCH rounds): no tail imbalance
+    const int smax = min(P.small_max, (int)max(64u, min(rpw, 1024u) * (unsigned)KF_SMAX_MUL));
+    // dynamic round fetching (one global atomic per warp per `fetch` rounds): fewer same-address atomics
+    // when every warp has many rounds, single rounds (the finest tail) when it has few
+    const unsigned fetch = rpw >= 16u ? (unsigned)KF_FETCH : 1u;
     unsigned w = 0;
     if (lane == 0) w = atom_add_u32(P.n_surv + 2, 1u);
-    w = __shfl_sync(FULL, w, 0) * KF_FETCH;
+    w = __shfl_sync(FULL, w, 0) * fetch;
     for (; w < nr;) {
         unsigned wn = 0;
         if (lane == 0) wn = atom_add_u32(P.n_surv + 2, 1u);   // next group, fetched early (latency hidden)
 #pragma unroll 1
-        for (int f = 0; f < KF_FETCH; ++f) {
+        for (unsigned f = 0; f < fetch; ++f) {
             const unsigned idx = (w + f) * 32u + (unsigned)lane;
             const bool valid = idx < ns;
             if (!__any_sync(FULL, valid)) break;
             refine_round<kFast, kLevel>(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
                                         valid ? __ldcs(P.surv + idx) : 0ull);
         }
-        w = __shfl_sync(FULL, wn, 0) * KF_FETCH;
+        w = __shfl_sync(FULL, wn, 0) * fetch;
     }
     __syncthreads();
     if (threadIdx.x < ST_COUNT) {   // block total of each counter, one global atomic each
@@ -2169,9 +2142,20 @@ static grca_status launch_packed(grca_t h) {
     {   // K0 (a reduce-scatter merges ceil(n / P) * P keys: the padding starts as MISS too)
         const int grid = h->num_sms * 8;   // full occupancy: stores in flight for HBM bandwidth
         const long long n_init = rs_merge(h) ? rs_chunk(h) * h->nranks : h->n_rays;
-        k_init<<<grid, 256, 0, h->stream>>>(P.hits, P.allhits, h->st_set ? h->n_rays : n_init, h->d_ctrl, h->d_stats,
-                                            h->st_set ? h->d_static_keys : nullptr,
-                                            (h->st_set && P.allhits) ? h->d_static_allhits : nullptr);
+        if (h->shard == GRCA_SHARD_EMITTERS && !h->ci.gather_outputs && !h->st_set) {
+            // emitter shards write only their own emitters' rays: initialise just those slices
+            k_init<<<1, 256, 0, h->stream>>>(P.hits, nullptr, 0, h->d_ctrl, h->d_stats, nullptr, nullptr, 1);
+            for (int m : h->own) {
+                const long long o = h->offsets[m], c = h->offsets[m + 1] - o;
+                const int gr = (int)std::min<long long>((long long)grid, (c / 2 + 255) / 256 + 1);
+                k_init<<<gr, 256, 0, h->stream>>>(P.hits + o, P.allhits ? P.allhits + o : nullptr, c, h->d_ctrl,
+                                                  h->d_stats, nullptr, nullptr, 0);
+            }
+        } else {
+            k_init<<<grid, 256, 0, h->stream>>>(P.hits, P.allhits, h->st_set ? h->n_rays : n_init, h->d_ctrl, h->d_stats,
+                                                h->st_set ? h->d_static_keys : nullptr,
+                                                (h->st_set && P.allhits) ? h->d_static_allhits : nullptr);
+        }
         CK(cudaGetLastError());
         if (h->st_set && n_init > h->n_rays)
             k_init<<<1, 256, 0, h->stream>>>(P.hits + h->n_rays, nullptr, n_init - h->n_rays, h->d_ctrl, h->d_stats,

@@ -959,6 +959,8 @@ def test_cast_is_capturable_by_the_caller():
     """grca_cast allocates nothing and syncs nothing, so a caller can capture it into its own
     CUDA graph (torch.cuda.graph on the handle's stream) and replay it after rewriting the borrowed
     vertex buffer in place: each replay equals a plain cast of the new vertices."""
+    if "bounds-checked" in G.version():
+        pytest.skip("the bounds-checked build synchronizes inside grca_cast (not capturable by design)")
     ems, tris = sg.random_scene(95, n_tris=1200, n_emitters=2, gamma=12, chi=128, extent=8.0)
     _, tris_b = sg.random_scene(96, n_tris=1200, n_emitters=2, gamma=12, chi=128, extent=8.0)
     s = torch.cuda.Stream()
