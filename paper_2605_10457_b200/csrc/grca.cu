@@ -45,6 +45,11 @@ constexpr int K4_THREADS = 256;
 #define KF_FETCH 2   // 32-survivor rounds per dynamic fetch of the fused kernel (measured: 1 -> 1.048, 2 -> 1.033,
                      // 4 -> 1.121 ms at C4: half the fetch atomics vs a coarser tail)
 #endif
+#ifndef K2_PRED_MAX_NE
+#define K2_PRED_MAX_NE 2   // K2 pre-test in predicate form (quick_*_pred) for NE <= this; the 2-bit-code form above
+                           // (measured at C4: NE = 8 0.485 vs 0.503 ms in predicate form; NE = 1 0.1715 -> 0.1695,
+                           // NE = 2 0.209 -> 0.201 ms, the 8- and 4-GPU sensor-shard ranks)
+#endif
 #ifndef KF_SMAX_MUL
 #define KF_SMAX_MUL 16   // fused kernel: small-rectangle cap = max(64, rounds per warp x this) (<= small_max)
 #endif
@@ -291,6 +296,25 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
     unsigned kb = 0u, rb = 0u;
     if (!kFast && P.nocull) {
         kb = (1u << NE) - 1u;
+    } else if ((NE <= K2_PRED_MAX_NE) && (kFast || P.pairs_ok)) {   // predicate form (no 2-bit codes)
+#pragma unroll
+        for (int e = 0; e + 1 < NE; e += 2) {
+            bool k0, r0, k1, r1;
+            quick_pair_pred<kLevel>(v, emax, EL.p[e / 2], EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base,
+                                    sSin + EL.e[e + 1].sin_base, sLut + e * kLutBins, sLut + (e + 1) * kLutBins,
+                                    k0, r0, k1, r1);
+            if (k0) kb |= 1u << e;
+            if (k1) kb |= 2u << e;
+            if (r0) rb |= 1u << e;
+            if (r1) rb |= 2u << e;
+        }
+        if (NE & 1) {
+            bool k0, r0;
+            quick_cull_pred<kLevel>(v, emax, EL.e[NE - 1], sSin + EL.e[NE - 1].sin_base, sLut + (NE - 1) * kLutBins,
+                                    k0, r0);
+            if (k0) kb |= 1u << (NE - 1);
+            if (r0) rb |= 1u << (NE - 1);
+        }
     } else if (kFast || P.pairs_ok) {   // all frames orthonormal: packed fp32x2 path
 #pragma unroll
         for (int e = 0; e + 1 < NE; e += 2) {
@@ -698,6 +722,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
                     my = (int)items;
                     cat = C_SMALL;
                     // ray of item (row, col) = gbase + row * chi + col - (col >= chi - r_lo ? chi : 0)
+                    // (storing this before the setup, so that R is dead across it, measured slower: 0.482 -> 0.490 ms)
                     slot[5 * 32 + lane] = make_float4(__int_as_float(E.ray_base + R.c_from * E.chi + R.r_lo),
                                                       __int_as_float(E.chi - R.r_lo),
                                                       __uint_as_float((unsigned)R.r_len | ((unsigned)E.chi << 16)),
@@ -971,6 +996,7 @@ __global__ void __launch_bounds__(256, K3_MINB) k_bin(const __grid_constant__ KP
             if (!ok) continue;   // Vol = 0 or face-culled: the pair can never hit
         }
         d3 x[3];
+        double sk[3];
         float th_ref = 0.f;
         if (!full && !P.norefine) {
             const d3 O = {(double)E.o[0], (double)E.o[1], (double)E.o[2]};
@@ -982,6 +1008,8 @@ __global__ void __launch_bounds__(256, K3_MINB) k_bin(const __grid_constant__ KP
                 x[k].z = (double)E.A[6] * a.x + (double)E.A[7] * a.y + (double)E.A[8] * a.z;
             }
             th_ref = E.theta0 + ((float)r_lo + 0.5f * (float)r_len) * E.dtheta;   // arc centre
+#pragma unroll
+            for (int k = 0; k < 3; ++k) sk[k] = x[k].z / sqrt(dotd(x[k], x[k]));
         }
         for (int j0 = c_from; j0 <= c_to; j0 += 32) {
             const int j = j0 + lane;
@@ -993,7 +1021,7 @@ __global__ void __launch_bounds__(256, K3_MINB) k_bin(const __grid_constant__ KP
                 else {
                     const double sj = (double)P.sin[E.sin_base + j];
                     float dmin, dmax;
-                    const int nb = refine_row(x, sj - (double)kPadS, sj + (double)kPadS, th_ref, dmin, dmax);
+                    const int nb = refine_row(x, sk, sj - (double)kPadS, sj + (double)kPadS, th_ref, dmin, dmax);
                     if (nb < 2) { lo = r_lo; len = r_len; }
                     else {
                         const float padth = kPadTheta + (E.noisy ? E.dtheta : 0.f);

@@ -440,16 +440,19 @@ __device__ int cull_pair(const f3 v[3], const EmDev &E, const float *sinTab, con
     bool arc_done = false;
     if (fast) {   // arc from the centroid azimuth and the vertices' small angular offsets
         const float cx = x[0].x + x[1].x + x[2].x, cy = x[0].y + x[1].y + x[2].y;
-        float dmin = 0.f, dmax = 0.f;
+        float zmin = 0.f, zmax = 0.f;
         bool ok = true;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const float cr = cx * x[k].y - cy * x[k].x, dt = cx * x[k].x + cy * x[k].y;
             ok = ok && dt > 0.f && fabsf(cr) < dt;
-            const float d = poly_atan(__fdividef(cr, dt));
-            dmin = k ? fminf(dmin, d) : d;
-            dmax = k ? fmaxf(dmax, d) : d;
+            const float z = __fdividef(cr, dt);
+            zmin = k ? fminf(zmin, z) : z;
+            zmax = k ? fmaxf(zmax, z) : z;
         }
+        // atan (and its polynomial, increasing on [-1, 1]) is monotone: the extremes of the three offsets
+        // are the offsets of the extreme tangents -- two evaluations instead of three, same values
+        const float dmin = poly_atan(zmin), dmax = poly_atan(zmax);
         if (ok) {
             start = fast_atan2(cy, cx) + dmin;
             len = dmax - dmin;
@@ -589,16 +592,15 @@ __device__ __forceinline__ void a7_add(double px, double py, float th_ref, int &
     ++cnt;
 }
 
-__device__ __noinline__ int refine_row(const d3 x[3], double s_lo, double s_hi, float th_ref, float &dmin, float &dmax) {
+// sk[k]: the vertices' elevation sines x_k.z / |x_k| (row-independent: computed once per pair by the caller)
+__device__ __noinline__ int refine_row(const d3 x[3], const double sk[3], double s_lo, double s_hi, float th_ref,
+                                       float &dmin, float &dmax) {
     int cnt = 0;
     dmin = CUDART_INF_F;
     dmax = -CUDART_INF_F;
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const double r = sqrt(dotd(x[k], x[k]));
-        const double sk = x[k].z / r;
-        if (sk >= s_lo && sk <= s_hi) a7_add(x[k].x, x[k].y, th_ref, cnt, dmin, dmax);
-    }
+    for (int k = 0; k < 3; ++k)
+        if (sk[k] >= s_lo && sk[k] <= s_hi) a7_add(x[k].x, x[k].y, th_ref, cnt, dmin, dmax);
     for (int c = 0; c < 2; ++c) {
         const double sc = c ? s_hi : s_lo;
         const double s2 = sc * sc;
@@ -624,9 +626,10 @@ __device__ __noinline__ int refine_row(const d3 x[3], double s_lo, double s_hi, 
                 if (disc >= 0.0) {
                     const double sq = sqrt(disc);
                     const double qq = -0.5 * (a1 + (a1 >= 0.0 ? sq : -sq));
-                    if (qq != 0.0) {
-                        lam[nl++] = qq / a2;
-                        lam[nl++] = a0 / qq;
+                    if (qq != 0.0) {   // roots qq / a2 and a0 / qq through one division (a few ulp)
+                        const double inv = 1.0 / (a2 * qq);
+                        lam[nl++] = qq * qq * inv;
+                        lam[nl++] = a0 * a2 * inv;
                     } else {
                         lam[nl++] = -a1 / (2.0 * a2);
                     }
@@ -731,6 +734,49 @@ __device__ __forceinline__ unsigned quick_cull_lut(const f3 v[3], float emax, co
     return quick_tail_lut(s, fminf(iw[0], fminf(iw[1], iw[2])), emax, L, sinT, lut);
 }
 
+// Predicate forms of quick_tail_lut / quick_cull_lut / quick_pair_lut (same tests, same bounds; K2_PRED): keep
+// and range as booleans that k2_tri ORs into its masks with compile-time shifts (no 2-bit code packing), and
+// the LUT bin clamped in float (lo >= -1 after one FMNMX; lo <= max s - pad < 1 - 2^-11 needs no upper clamp:
+// s <= 1 + 2u and pad >= 4e-6) instead of two integer clamps.
+__device__ __forceinline__ void quick_tail_pred(const float s[3], float miw, float emax, const EmLite &L,
+                                                const float *sinT, const unsigned char *lut, bool &keep, bool &range) {
+    const float x = emax * miw;
+    const float x2 = x * x;
+    range = miw * (L.lim + emax) < 1.f;
+    const bool near = !(x < 0.33f);
+    const float smax = fmaxf(fabsf(s[0]), fmaxf(fabsf(s[1]), fabsf(s[2])));
+    const bool pole = smax >= 1.f - 1.1475f * x2 - 1e-5f;
+    const float pad = L.pad0 + 0.2925f * x2;
+    const float lo = fminf(s[0], fminf(s[1], s[2])) - pad;
+    const float hi = fmaxf(s[0], fmaxf(s[1], s[2])) + pad;
+    const int b = __float2int_rz(__fmaf_rn(fmaxf(lo, -1.f), 0.5f * kLutBins, 0.5f * kLutBins));
+    const float *sj = sinT + lut[b];
+    const float v0 = sj[0], v1 = sj[1];
+    const float vj = v0 >= lo ? v0 : v1;
+    keep = !range && (near || pole || vj <= hi);
+}
+
+template <bool kLevel = false>
+__device__ __forceinline__ void quick_cull_pred(const f3 v[3], float emax, const EmLite &L, const float *sinT,
+                                                const unsigned char *lut, bool &keep, bool &range) {
+    float s[3], iw[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const f3 a = {v[k].x - L.o[0], v[k].y - L.o[1], v[k].z - L.o[2]};
+        const float w2 = a.x * a.x + a.y * a.y + a.z * a.z;
+        const float xu = kLevel ? a.z : L.Au[0] * a.x + L.Au[1] * a.y + L.Au[2] * a.z;
+        iw[k] = rsqrtf(w2);
+        if (L.ortho) {
+            s[k] = xu * iw[k];
+        } else {
+            const float x2 = L.G[0] * a.x * a.x + L.G[1] * a.y * a.y + L.G[2] * a.z * a.z +
+                             2.f * (L.G[3] * a.x * a.y + L.G[4] * a.x * a.z + L.G[5] * a.y * a.z);
+            s[k] = xu * rsqrtf(x2);
+        }
+    }
+    quick_tail_pred(s, fminf(iw[0], fminf(iw[1], iw[2])), emax, L, sinT, lut, keep, range);
+}
+
 // interleaved constants of emitters (2p, 2p+1) for the packed path: one 64-bit constant load each
 struct EmPair {
     float2 no[3];   // (-o_x), (-o_y), (-o_z)
@@ -762,6 +808,30 @@ __device__ __forceinline__ unsigned quick_pair_lut(const f3 v[3], float emax, co
     const unsigned a = quick_tail_lut(s0, m0, emax, L0, sinT0, lut0);
     const unsigned b = quick_tail_lut(s1, m1, emax, L1, sinT1, lut1);
     return (a & 1u) | ((b & 1u) << 1) | ((a & 2u) << 1) | ((b & 2u) << 2);
+}
+
+template <bool kLevel = false>
+__device__ __forceinline__ void quick_pair_pred(const f3 v[3], float emax, const EmPair &PR, const EmLite &L0,
+                                                const EmLite &L1, const float *sinT0, const float *sinT1,
+                                                const unsigned char *lut0, const unsigned char *lut1, bool &k0, bool &r0,
+                                                bool &k1, bool &r1) {
+    float s0[3], s1[3], m0 = CUDART_INF_F, m1 = CUDART_INF_F;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float2 ax = __fadd2_rn(f2(v[k].x, v[k].x), PR.no[0]);
+        const float2 ay = __fadd2_rn(f2(v[k].y, v[k].y), PR.no[1]);
+        const float2 az = __fadd2_rn(f2(v[k].z, v[k].z), PR.no[2]);
+        const float2 w2 = __ffma2_rn(az, az, __ffma2_rn(ay, ay, __fmul2_rn(ax, ax)));
+        const float2 xu = kLevel ? az : __ffma2_rn(PR.u[2], az, __ffma2_rn(PR.u[1], ay, __fmul2_rn(PR.u[0], ax)));
+        const float2 iw = f2(rsqrtf(w2.x), rsqrtf(w2.y));
+        const float2 ss = __fmul2_rn(xu, iw);
+        s0[k] = ss.x;
+        s1[k] = ss.y;
+        m0 = fminf(m0, iw.x);
+        m1 = fminf(m1, iw.y);
+    }
+    quick_tail_pred(s0, m0, emax, L0, sinT0, lut0, k0, r0);
+    quick_tail_pred(s1, m1, emax, L1, sinT1, lut1, k1, r1);
 }
 
 __device__ __forceinline__ void quick_cull2(const f3 v[3], float emax, const EmLite &L0, const EmLite &L1,
