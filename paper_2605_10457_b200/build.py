@@ -50,9 +50,10 @@ def build_variant(out: str, defines: list) -> str:
 def build(force: bool = False, verbose: bool = False) -> str:
     stale = force or not os.path.exists(LIB) or any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS)
     if stale:
-        cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + SRC + ["-o", LIB + ".tmp"]
+        tmp = f"{LIB}.{os.getpid()}.tmp"
+        cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + SRC + ["-o", tmp]
         subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
+        os.replace(tmp, LIB)
     return LIB
 
 

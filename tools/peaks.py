@@ -20,9 +20,10 @@ LIB = os.path.join(HERE, "libpeaks.so")
 
 def build() -> str:
     if not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        tmp = f"{LIB}.{os.getpid()}.tmp"   # per process: ranks building at once never share a partial file
         subprocess.check_call(["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-                               "-Xcompiler", "-fPIC", "-shared", SRC, "-o", LIB + ".tmp"])
-        os.replace(LIB + ".tmp", LIB)
+                               "-Xcompiler", "-fPIC", "-shared", SRC, "-o", tmp])
+        os.replace(tmp, LIB)
     return LIB
 
 
