@@ -682,6 +682,24 @@ __device__ __forceinline__ int quick_tail(const float s[3], float rmax, float em
     return range ? CULL_RANGE : (keep ? CULL_KEEP : CULL_CHANNEL);
 }
 
+// LUT bin of lo (sin units; lo < 1 - 4e-6 since lo = min s - pad, s <= 1 + 2u, pad >= kPadS).
+#ifndef K2_FADD_BIN
+#define K2_FADD_BIN 0
+#endif
+__device__ __forceinline__ int lut_bin(float lo) {
+#if K2_FADD_BIN
+    // floor((lo' + 1) * 1024) or one less, lo' = max(lo, -1), without F2I (an XU-pipe op) or integer clamps:
+    // y - 1/2 = lo' * 1024 + 1023.5 (one rounding, <= 2^-14), then + 1.5 * 2^23 rounds it to an integer (ties to
+    // even).  The result is in [0, 2047]; it exceeds floor(y) only when y lies within 2^-14 (6e-8 in sin units)
+    // below an integer, i.e. inside the LUT's 1e-6 under-estimate margin; one less only starts the scan earlier.
+    return __float_as_int(__fadd_rn(__fmaf_rn(fmaxf(lo, -1.f), 0.5f * kLutBins, 0.5f * kLutBins - 0.5f), 12582912.f)) -
+           0x4B400000;
+#else
+    // one rounding (<= 2.4e-7 in sin units) against the LUT's 1e-6 under-estimate margin
+    return min(max(__float2int_rz(__fmaf_rn(lo, 0.5f * kLutBins, 0.5f * kLutBins)), 0), kLutBins - 1);
+#endif
+}
+
 // Fixed-kernel variants (k_cull_fixed, NE <= 8; LUT always present).  Same bounds as quick_tail;
 // differences: (i) no scan past the second LUT channel -- when a bin holds more channels below lo
 // the pair is kept (v1 < lo <= hi), which is conservative since K2b/cull_pair recomputes the exact
@@ -702,8 +720,7 @@ __device__ __forceinline__ unsigned quick_tail_lut(const float s[3], float miw, 
     const float pad = L.pad0 + 0.2925f * x2;
     const float lo = fminf(s[0], fminf(s[1], s[2])) - pad;
     const float hi = fmaxf(s[0], fmaxf(s[1], s[2])) + pad;
-    // bin of lo: one rounding (<= 2.4e-7 in sin units) against the LUT's 1e-6 under-estimate margin
-    const int b = min(max(__float2int_rz(__fmaf_rn(lo, 0.5f * kLutBins, 0.5f * kLutBins)), 0), kLutBins - 1);
+    const int b = lut_bin(lo);
     const float *sj = sinT + lut[b];
     const float v0 = sj[0], v1 = sj[1];   // two +inf sentinels: j + 1 <= gamma + 1
     const float vj = v0 >= lo ? v0 : v1;
@@ -749,7 +766,7 @@ __device__ __forceinline__ void quick_tail_pred(const float s[3], float miw, flo
     const float pad = L.pad0 + 0.2925f * x2;
     const float lo = fminf(s[0], fminf(s[1], s[2])) - pad;
     const float hi = fmaxf(s[0], fmaxf(s[1], s[2])) + pad;
-    const int b = __float2int_rz(__fmaf_rn(fmaxf(lo, -1.f), 0.5f * kLutBins, 0.5f * kLutBins));
+    const int b = lut_bin(lo);
     const float *sj = sinT + lut[b];
     const float v0 = sj[0], v1 = sj[1];
     const float vj = v0 >= lo ? v0 : v1;
