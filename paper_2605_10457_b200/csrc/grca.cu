@@ -53,6 +53,9 @@ constexpr int K4_THREADS = 256;
 #ifndef KF_SMAX_MUL
 #define KF_SMAX_MUL 16   // fused kernel: small-rectangle cap = max(64, rounds per warp x this) (<= small_max)
 #endif
+#ifndef KF_MAGIC_DIV
+#define KF_MAGIC_DIV 0   // fused item loop: row = local / len by a per-pair magic multiplier (no float round trip)
+#endif
 #ifndef KF_PREFETCH
 #define KF_PREFETCH 0   // fused item loop: issue the next step's ray load before this step's test
 #endif
@@ -726,7 +729,14 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
                     slot[5 * 32 + lane] = make_float4(__int_as_float(E.ray_base + R.c_from * E.chi + R.r_lo),
                                                       __int_as_float(E.chi - R.r_lo),
                                                       __uint_as_float((unsigned)R.r_len | ((unsigned)E.chi << 16)),
+#if KF_MAGIC_DIV
+                                                      // row = local / len exactly as umulhi(local, ceil(2^32 / len))
+                                                      // (local < 2^16, len < 2^16); len = 1 -> 0 (row = local)
+                                                      __uint_as_float(R.r_len > 1 ? (unsigned)((0x100000000ull + (unsigned)R.r_len - 1) /
+                                                                                               (unsigned)R.r_len) : 0u));
+#else
                                                       __fdividef(1.f, (float)R.r_len));   // row guess, corrected by +-1
+#endif
                 } else {
                     cat = C_DEGEN;
                 }
@@ -793,10 +803,16 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             const int local = qi - excl[ow];
             const unsigned lc = __float_as_uint(r5.z);
             const int len = (int)(lc & 0xffffu), chi = (int)(lc >> 16);
+#if KF_MAGIC_DIV
+            const unsigned mg = __float_as_uint(r5.w);
+            const int row = mg ? (int)__umulhi((unsigned)local, mg) : local;
+            const int col = local - row * len;
+#else
             int row = (int)(((float)local + 0.5f) * r5.w);
             int col = local - row * len;
             if (col < 0) { --row; col += len; }
             if (col >= len) { ++row; col -= len; }
+#endif
             g = __float_as_int(r5.x) + row * chi + col - (col >= __float_as_int(r5.y) ? chi : 0);
         }
     };
