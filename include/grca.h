@@ -228,6 +228,23 @@ grca_status grca_update_scene(grca_t h, const float *d_soup, int64_t n_soup_tria
                               int64_t n_mesh_vertices, const uint32_t *d_mesh_indices, int64_t n_mesh_triangles,
                               const int32_t *d_tri_ids, int32_t tri_id_base);
 
+/* Rigid instances (ABI extension named in SURVEY 8(a) row A1: "an optional per-instance 3x4 affine applied
+ * inside K1"): the dynamic objects of the paper's motion modes (f.i; poses and per-axis scales
+ * redrawn every frame) are instances of one mesh, so a frame's input is one 48-byte matrix per
+ * instance instead of every posed vertex.  Appends part C to the triangle set of the last grca_update_scene /
+ * grca_update_triangles[_f3] call (or to an empty set): triangle n_ab + i * n_faces + f (n_ab = that call's
+ * triangle count) is face f of instance i, with vertices d_local_xyz[d_local_faces[3 f + c]] (packed float3,
+ * object space; n_local_vertices of them) mapped by the row-major 3x4 matrix M_i = d_poses[12 i .. 12 i + 11]
+ * (rows (m00 m01 m02 m03), (m10 ...), (m20 ...), 16-byte aligned): world_r = ((m_r0 x + m_r1 y) + m_r2 z) + m_r3
+ * in fp32 with every product and sum rounded in this order (no FMA), so a host reproduces the world vertices bit
+ * for bit.  Ids as the set's (d_tri_ids covering all parts, or tri_id_base + k).  Buffers borrowed as in
+ * grca_update_triangles.  Every later grca_update_scene / grca_update_triangles[_f3] drops part C.
+ * Errors: GRCA_E_INVALID (negative counts, n_faces or n_instances >= 2^31, missing or misaligned buffers),
+ * GRCA_E_CAPACITY (n_ab + n_faces * n_instances > max_triangles). */
+grca_status grca_update_instances(grca_t h, const float *d_local_xyz, int64_t n_local_vertices,
+                                  const uint32_t *d_local_faces, int64_t n_faces, const float *d_poses,
+                                  int64_t n_instances);
+
 /* Hybrid static/dynamic mode (NEXT-f2; "GRCA on dynamic, static BVH on static,
  * per-ray min merge", here without any BVH): borrow a static triangle set (same conventions as
  * grca_update_triangles; buffers must stay alive and unmodified while set).  The next cast (and the

@@ -19,6 +19,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <climits>
 #include <string>
 #include <vector>
 
@@ -1236,6 +1237,12 @@ using namespace grca;
 static constexpr int kRing = 64;
 static constexpr int kEv = 8;   // start, after K0, K2, K2b, K4s, K3, K4, K5
 
+static TriSrc no_part_c() {
+    TriSrc T{};
+    T.n_c0 = LLONG_MAX;
+    return T;
+}
+
 struct grca_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -1283,11 +1290,12 @@ struct grca_ctx {
     unsigned long long *d_stats = nullptr;
     long long cap_large = 0, cap_chunks = 0;
     // triangles (dynamic / per frame)
-    TriSrc tri{};
+    TriSrc tri = no_part_c();
     long long n_tri = 0;
+    long long n_tri_ab = 0;   // parts A + B of the dynamic set (part C, the instances, follows them)
     bool have_tri = false;
     // hybrid static/dynamic (NEXT-f2): static triangles cast once into cached keys
-    TriSrc st_tri{};
+    TriSrc st_tri = no_part_c();
     long long st_n = 0;
     bool st_set = false, st_dirty = false;
     unsigned long long *d_static_keys = nullptr;
@@ -1983,6 +1991,8 @@ grca_status grca_update_triangles(grca_t h, const float *d_vertices, int64_t n_v
     h->tri.id_base = tri_id_base;
     h->tri.n_v = n_vertices;
     h->tri.n_t = n_triangles;
+    h->tri.n_c0 = LLONG_MAX;   // (part C: grca_update_instances after this call)
+    h->n_tri_ab = n_triangles;
     h->n_tri = n_triangles;
     h->have_tri = true;
     return GRCA_OK;
@@ -2002,6 +2012,8 @@ grca_status grca_update_triangles_f3(grca_t h, const float *d_xyz, int64_t n_ver
     h->tri.id_base = tri_id_base;
     h->tri.n_v = n_vertices;
     h->tri.n_t = n_triangles;
+    h->tri.n_c0 = LLONG_MAX;   // (part C: grca_update_instances after this call)
+    h->n_tri_ab = n_triangles;
     h->n_tri = n_triangles;
     h->have_tri = true;
     return GRCA_OK;
@@ -2030,7 +2042,42 @@ grca_status grca_update_scene(grca_t h, const float *d_soup, int64_t n_soup_tria
     h->tri.id_base = tri_id_base;
     h->tri.n_v = n_mesh_vertices;
     h->tri.n_t = n_soup_triangles + n_mesh_triangles;
+    h->tri.n_c0 = LLONG_MAX;   // (part C: grca_update_instances after this call)
+    h->n_tri_ab = n_soup_triangles + n_mesh_triangles;
     h->n_tri = n_soup_triangles + n_mesh_triangles;
+    h->have_tri = true;
+    return GRCA_OK;
+}
+
+grca_status grca_update_instances(grca_t h, const float *d_local_xyz, int64_t n_local_vertices,
+                                  const uint32_t *d_local_faces, int64_t n_faces, const float *d_poses,
+                                  int64_t n_instances) {
+    if (!h) return GRCA_E_INVALID;
+    if (n_faces < 0 || n_instances < 0 || n_local_vertices < 0) return fail(h, GRCA_E_INVALID, "negative count");
+    if (n_faces > 0x7fffffffll || n_instances > 0x7fffffffll)
+        return fail(h, GRCA_E_INVALID, "n_faces and n_instances must be < 2^31");
+    const long long n_c = n_faces * n_instances;
+    if (n_c > 0 && (!d_local_xyz || !d_local_faces || !d_poses || n_local_vertices < 1))
+        return fail(h, GRCA_E_INVALID, "instances: local vertices, faces and poses required");
+    if (((uintptr_t)d_poses & 15) || ((uintptr_t)d_local_xyz & 3) || ((uintptr_t)d_local_faces & 3))
+        return fail(h, GRCA_E_INVALID, "poses must be 16-byte aligned (3 float4 rows each); vertices / faces 4-byte");
+    if (!h->have_tri) {   // no grca_update_scene / _triangles before: parts A and B are empty
+        h->tri = no_part_c();
+        h->n_tri_ab = 0;
+    }
+    if (h->n_tri_ab + n_c > h->ci.max_triangles) return fail(h, GRCA_E_CAPACITY, "triangles exceed max_triangles");
+    if (!h->tri.ids && (long long)h->tri.id_base + h->n_tri_ab + n_c > 0x7fffffffll)
+        return fail(h, GRCA_E_INVALID, "triangle ids must be in [0, 2^31)");
+    h->tri.n_c0 = n_c > 0 ? h->n_tri_ab : LLONG_MAX;
+    h->tri.cv = d_local_xyz;
+    h->tri.cidx = d_local_faces;
+    h->tri.cpose = reinterpret_cast<const float4 *>(d_poses);
+    h->tri.c_faces = n_faces;
+    h->tri.c_nv = n_local_vertices;
+    h->tri.c_ninst = n_instances;
+    h->tri.c_inv_faces = n_faces > 0 ? (float)(1.0 / (double)n_faces) : 0.f;
+    h->tri.n_t = h->n_tri_ab + n_c;
+    h->n_tri = h->n_tri_ab + n_c;
     h->have_tri = true;
     return GRCA_OK;
 }
@@ -2049,6 +2096,7 @@ grca_status grca_set_static_triangles(grca_t h, const float *d_vertices, int64_t
     h->st_tri.id_base = tri_id_base;
     h->st_tri.n_v = n_vertices;
     h->st_tri.n_t = n_triangles;
+    h->st_tri.n_c0 = LLONG_MAX;
     h->st_n = n_triangles;
     h->st_set = true;
     h->st_dirty = true;

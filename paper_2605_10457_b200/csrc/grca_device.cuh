@@ -162,15 +162,54 @@ struct TriSrc {
     const int32_t *ids;    // NULL -> id_base + local (global triangle index, parts A and B alike)
     int32_t id_base;
     long long n_v;         // vertices of part B (bounds-checked build only)
-    long long n_t;         // triangles of parts A + B (bounds-checked build only)
+    long long n_t;         // triangles of parts A + B (+ C) (bounds-checked build only)
+    // part C (grca_update_instances): triangles [n_c0, n_t) are rigid instances of one local mesh: triangle
+    // n_c0 + i * c_faces + f is face f of instance i, its local vertices mapped by the instance's 3x4 matrix
+    long long n_c0;        // first triangle of part C (LLONG_MAX: no part C)
+    const float *cv;       // local vertices, packed float3 (object space)
+    const uint32_t *cidx;  // local faces, 3 indices each
+    const float4 *cpose;   // per instance 3 float4 rows (m00 m01 m02 m03), (m10 ...), (m20 ...)
+    long long c_faces, c_nv, c_ninst;
+    float c_inv_faces;     // 1 / c_faces (instance estimate, corrected exactly)
 };
 __device__ __forceinline__ f3 ldcs3(const float *p) { return {__ldcs(p), __ldcs(p + 1), __ldcs(p + 2)}; }
 // Streaming (evict-first) loads: the ~1 GB triangle stream must not evict the L2-resident ray
 // table (67 MB at C4) and hit buffer (33.5 MB) that the intersection kernels gather from.
+// world = M [v; 1] with every product and sum rounded, in this order (no FMA contraction): a host evaluating
+// ((m0 x + m1 y) + m2 z) + m3 in IEEE fp32 reproduces it bit for bit (include/grca.h grca_update_instances)
+__device__ __forceinline__ float pose_row(float4 m, f3 p) {
+    return __fadd_rn(__fadd_rn(__fadd_rn(__fmul_rn(m.x, p.x), __fmul_rn(m.y, p.y)), __fmul_rn(m.z, p.z)), m.w);
+}
+#if GRCA_INST_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__   // (kept out of line: the soup / mesh hot paths do not carry its registers)
+#endif
+void load_instance_tri(const TriSrc &T, long long u, f3 v[3]) {
+    long long i = (long long)__float2ll_rz(__ll2float_rn(u) * T.c_inv_faces);
+    long long f = u - i * T.c_faces;
+    while (f < 0) { --i; f += T.c_faces; }
+    while (f >= T.c_faces) { ++i; f -= T.c_faces; }
+#ifdef GRCA_CHECK
+    i = chk_idx(i, T.c_ninst, CHK_TRI);
+#endif
+    const float4 r0 = __ldg(T.cpose + 3 * i), r1 = __ldg(T.cpose + 3 * i + 1), r2 = __ldg(T.cpose + 3 * i + 2);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const long long vi = chk_idx(__ldg(T.cidx + 3 * f + k), T.c_nv, CHK_VERTEX);
+        const f3 p = {__ldg(T.cv + 3 * vi), __ldg(T.cv + 3 * vi + 1), __ldg(T.cv + 3 * vi + 2)};
+        v[k] = {pose_row(r0, p), pose_row(r1, p), pose_row(r2, p)};
+    }
+}
+
 __device__ __forceinline__ void load_tri(const TriSrc &T, long long t, f3 v[3]) {
 #ifdef GRCA_CHECK
     t = chk_idx(t, T.n_t, CHK_TRI);
 #endif
+    if (t >= T.n_c0) {   // part C: a rigid instance of the local mesh (grca_update_instances)
+        load_instance_tri(T, t - T.n_c0, v);
+        return;
+    }
     if (t < T.n_a) {   // part A: float4 triplets, no indirection (static scenery)
         v[0] = mk(__ldcs(T.va + 3 * t));
         v[1] = mk(__ldcs(T.va + 3 * t + 1));

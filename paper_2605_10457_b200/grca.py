@@ -31,7 +31,7 @@ EXPORTS = [
     "grca_cast_packed", "grca_hits_packed", "grca_set_static_triangles", "grca_clear_static", "grca_unpack", "grca_get_stats", "grca_kernel_times", "grca_set_distance_noise",
     "grca_debug_all_hits", "grca_debug_large_list", "grca_debug_fast_atan2", "grca_get_layout", "grca_debug_ray_table", "grca_last_error", "grca_version",
     "grca_set_nvls", "grca_nvls_status", "grca_update_triangles_f3", "grca_update_scene",
-    "grca_unpack_range", "grca_nccl_unique_id", "grca_get_shard",
+    "grca_unpack_range", "grca_nccl_unique_id", "grca_get_shard", "grca_update_instances",
 ]
 
 
@@ -92,6 +92,7 @@ def load(path: str = LIB_PATH):
         "grca_update_triangles": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
         "grca_update_triangles_f3": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
         "grca_update_scene": ([vp, vp, i64, vp, i64, vp, i64, vp, i32], C.c_int),
+        "grca_update_instances": ([vp, vp, i64, vp, i64, vp, i64], C.c_int),
         "grca_cast": ([vp, vp, vp, C.POINTER(Stats)], C.c_int),
         "grca_cast_packed": ([vp], C.c_int),
         "grca_set_static_triangles": ([vp, vp, i64, vp, i64, vp, i32], C.c_int),
@@ -296,6 +297,22 @@ class Grca:
                                               _ptr(tri_ids), int(tri_id_base)))
         self._tri_refs = (soup, mesh_xyz, mesh_indices, tri_ids)
         self.n_triangles = ns + nm
+        return self
+
+    # -- grca_update_instances: local_xyz float32 CUDA [V, 3], faces int32/uint32 [F, 3], poses float32 CUDA
+    #    [n_instances, 3, 4] (row-major 3x4 per instance); appended to the last update_scene / update_triangles set
+    def update_instances(self, local_xyz, faces, poses):
+        import torch
+
+        assert local_xyz.is_cuda and local_xyz.dtype == torch.float32 and local_xyz.shape[-1] == 3
+        assert faces.is_cuda and faces.dtype in (torch.int32, torch.uint32) and faces.is_contiguous()
+        assert poses.is_cuda and poses.dtype == torch.float32 and poses.is_contiguous() and poses.shape[-2:] == (3, 4)
+        assert local_xyz.is_contiguous()
+        n_inst = poses.numel() // 12
+        self._check(self._L.grca_update_instances(self._h, _ptr(local_xyz), local_xyz.numel() // 3, _ptr(faces),
+                                                  faces.numel() // 3, _ptr(poses), n_inst))
+        self._inst_refs = (local_xyz, faces, poses)
+        self.n_triangles = getattr(self, "n_triangles", 0) + (faces.numel() // 3) * n_inst
         return self
 
     # -- grca_set_nvls / grca_nvls_status (NEXT-f3 fused NVLS merge on caller-bound buffers; the library binds

@@ -362,6 +362,23 @@ def apply_pose(local: np.ndarray, pose: InstancePose) -> np.ndarray:
     return v.astype(np.float32)
 
 
+def pose_matrix(pose: InstancePose) -> np.ndarray:
+    """The instance's row-major 3x4 fp32 matrix [R diag(s) | p] (grca_update_instances), rounded once from fp64."""
+    M = np.concatenate([pose.rotation * pose.scale[None, :], pose.position[:, None]], axis=1)
+    return M.astype(np.float32)
+
+
+def apply_pose_f32(local: np.ndarray, M: np.ndarray) -> np.ndarray:
+    """World vertices of an instance exactly as grca_update_instances defines them: per row r,
+    ((m_r0 x + m_r1 y) + m_r2 z) + m_r3 in IEEE fp32, every product and sum rounded (numpy float32 ops)."""
+    v = np.asarray(local, dtype=np.float32)
+    M = np.asarray(M, dtype=np.float32)
+    out = np.empty(v.shape, dtype=np.float32)
+    for r in range(3):
+        out[..., r] = ((M[r, 0] * v[..., 0] + M[r, 1] * v[..., 1]) + M[r, 2] * v[..., 2]) + M[r, 3]
+    return out
+
+
 def swd(tris: np.ndarray, bbox, seed: int, frame: int) -> np.ndarray:
     """Scene-wide deformation: each triangle keeps its shape; its centroid is redrawn
     uniformly in the world bbox."""

@@ -1053,3 +1053,46 @@ def test_sat_bat_classification():
         _, _, st, g = run([em], np.array([t], np.float32))
         assert (st["sat_pairs"], st["bat_pairs"]) == ((1, 0) if sat else (0, 1)), (name, st["sat_pairs"], st["bat_pairs"])
         g.close()
+
+
+def test_instances_match_posed_soup_and_oracle():
+    """grca_update_instances (rigid instances, ABI extension of SURVEY 8(a) A1): a static soup (part A) followed
+    by 6 posed instances of a local mesh (part C) equals, bit for bit, the cast of the same triangles given as
+    one soup whose instance vertices the host posed with the documented fp32 operation order
+    (scenegen.apply_pose_f32); parity with the oracle on that soup; instances alone (no part A) too."""
+    car_v, car_f = sg.car_mesh(24, 24, dims=(4.0, 2.0, 1.2))
+    poses = sg.pose_instances(6, (40.0, 30.0, 6.0), seed=5, frame=1, scale_lo=0.3, scale_hi=3.0)
+    Ms = np.stack([sg.pose_matrix(p) for p in poses])                       # (6, 3, 4) fp32
+    posed = np.concatenate([sg.apply_pose_f32(car_v, M)[car_f] for M in Ms], 0)   # (6 F, 3, 3)
+    static = sg.grid_mesh(8, 8, -5, -5, 45, 35, 0.0)
+    soup = np.ascontiguousarray(np.concatenate([static, posed], 0))
+    ems = [sg.Emitter(origin=(10.0, 12.0, 2.0), elev=sg.full_sphere_elev(32), rays_per_channel=720),
+           sg.Emitter(origin=(30.0, 5.0, 1.5), forward=(0, 1, 0), right=(1, 0, 0), elev=sg.vlp16_elev(),
+                      rays_per_channel=500, hfov_deg=180)]
+    ref = run(ems, soup)
+    check(ems, soup, ref[0], ref[1])
+    g = Grca(device=0, max_triangles=len(soup), max_rays=sg.n_rays_total(ems))
+    g.set_emitters(ems)
+    lv = torch.as_tensor(car_v.astype(np.float32), device="cuda")
+    lf = torch.as_tensor(car_f.astype(np.int32), device="cuda")
+    pm = torch.as_tensor(Ms, device="cuda")
+    g.update_scene(soup=tris_to_float4(static))
+    g.update_instances(lv, lf, pm)
+    d, t = g.cast()
+    torch.cuda.synchronize()
+    assert np.array_equal(t.cpu().numpy(), ref[1]) and np.array_equal(d.cpu().numpy().view(np.uint32), ref[0].view(np.uint32))
+    # instances alone: ids start at 0 for the first instance triangle
+    g2 = Grca(device=0, max_triangles=len(posed), max_rays=sg.n_rays_total(ems))
+    g2.set_emitters(ems)
+    g2.update_instances(lv, lf, pm)
+    d2, t2 = g2.cast()
+    torch.cuda.synchronize()
+    ref2 = run(ems, posed)
+    assert np.array_equal(t2.cpu().numpy(), ref2[1]) and np.array_equal(d2.cpu().numpy().view(np.uint32), ref2[0].view(np.uint32))
+    # errors: misaligned poses, capacity
+    E_INVALID, E_CAPACITY = 1, 3
+    L = g._L
+    assert L.grca_update_instances(g._h, lv.data_ptr(), len(car_v), lf.data_ptr(), len(car_f), pm.data_ptr() + 4, 6) == E_INVALID
+    assert L.grca_update_instances(g._h, lv.data_ptr(), len(car_v), lf.data_ptr(), len(car_f), pm.data_ptr(), 7) == E_CAPACITY
+    g.close()
+    g2.close()
