@@ -141,8 +141,11 @@ class Scene:
         self.deformation = deformation
         self.device = device
         cm = w.get("car_mesh")
-        self.indexed = mesh == "indexed" and cm is not None and deformation == "ND" and n_dyn > 0
-        self.mesh = "indexed" if self.indexed else "soup"
+        self.indexed = mesh in ("indexed", "instances") and cm is not None and deformation == "ND" and n_dyn > 0
+        # rigid instances (grca_update_instances): a frame is one 3x4 matrix per car; needs whole instances in
+        # order on this rank (one GPU or sensor shards)
+        self.instanced = self.indexed and mesh == "instances" and self.identity
+        self.mesh = "instances" if self.instanced else "indexed" if self.indexed else "soup"
         self.idx_dyn = self.static_soup = None
         if self.indexed:
             car_v, car_f = cm
@@ -156,13 +159,24 @@ class Scene:
             # Algorithmic K2 read per cast: static 48 B (3 float4); cars 12 B indices per triangle +
             # 12 B per shared float3 vertex
             self.tri_bytes = self.n_static_local * 48 + len(self.own_dyn) * 12 + self.n_dyn_vert * 12
+            if self.instanced:   # local mesh (faces + vertices) once, 48 B of matrix per instance
+                self.car_v_dev = torch.as_tensor(self.car_v_np, device=device)
+                self.car_f_np = np.asarray(car_f, dtype=np.int32)
+                self.car_f_dev = torch.as_tensor(self.car_f_np, device=device)
+                self.tri_bytes = self.n_static_local * 48 + nf_car * 12 + nv_car * 12 + self.n_cars * 48
         else:
             self.car_np = np.asarray(w.get("car_local", np.zeros((0, 3, 3))), dtype=np.float32)   # (m, 3, 3) local
             self.tri_bytes = self.n_tri * 48
-        # frame buffers: soup = [static | dynamic] float4 rows; indexed = the car vertices only
+        # frame buffers: soup = [static | dynamic] float4 rows; indexed = the car vertices only; instances = the
+        # cars' 3x4 matrices as rows of 4 floats (3 per car)
         self.fs = 0 if self.indexed else self.ns3   # static rows at the head of a frame buffer
         self.frames = []
-        for fr in range(N_FRAMES):
+        for fr in range(N_FRAMES if self.instanced else 0):
+            poses = sg.pose_instances(self.n_cars, self.bbox, int(self.config[1:]), fr, scale_lo=self.scale[0],
+                                      scale_hi=self.scale[1])
+            Ms = np.stack([sg.pose_matrix(p) for p in poses]).reshape(-1, 4)
+            self.frames.append(torch.as_tensor(np.ascontiguousarray(Ms), device=device))
+        for fr in range(0 if self.instanced else N_FRAMES):
             nd = self.n_dyn_vert if self.indexed else 3 * (self.n_tri - self.n_static_local)
             buf = torch.zeros((self.fs + nd, 3 if self.indexed else 4), dtype=torch.float32, device=device)
             buf[: self.fs, :3] = static[: self.fs]
@@ -172,11 +186,24 @@ class Scene:
         torch.cuda.synchronize()
 
     def bind(self, g, buf, n_triangles=None):
-        """Point handle g at one frame buffer (public API: grca_update_scene / grca_update_triangles)."""
-        if self.indexed:
+        """Point handle g at one frame buffer (public API: grca_update_scene / grca_update_triangles /
+        grca_update_instances)."""
+        if self.instanced:
+            g.update_scene(soup=self.static_soup, tri_ids=self.ids_arg)
+            g.update_instances(self.car_v_dev, self.car_f_dev, buf.view(-1, 3, 4))
+        elif self.indexed:
             g.update_scene(soup=self.static_soup, mesh_xyz=buf, mesh_indices=self.idx_dyn, tri_ids=self.ids_arg)
         else:
             g.update_triangles(buf, tri_ids=self.ids_arg, n_triangles=n_triangles)
+
+    def frame_tris(self, frame: int, w_tris):
+        """The triangles frame `frame` casts, on the host (the oracle's input): scenegen's frame, except that
+        instanced cars are posed with the documented fp32 order of grca_update_instances."""
+        if not self.instanced:
+            return w_tris
+        Ms = self.frames[frame].cpu().numpy().reshape(-1, 3, 4)
+        cars = [sg.apply_pose_f32(self.car_v_np, M)[self.car_f_np] for M in Ms]
+        return np.ascontiguousarray(np.concatenate([w_tris[: self.n_static_local]] + cars, 0))
 
     def dynamic(self, frame: int):
         """Motion f.i: per-frame random pose/scale of every car instance; world
@@ -361,6 +388,8 @@ def main():
                     "as one CUDA graph, the default: C4 1.053 vs 1.064 ms, C2 0.105 vs 0.115 ms)")
     ap.add_argument("--collective", action="store_true", help="N=1: cast through a one-rank NCCL communicator "
                     "(the library's collective path, merge included) instead of a plain handle")
+    ap.add_argument("--instances", action="store_true", help="cars as rigid instances (grca_update_instances): a frame's "
+                    "input is one 3x4 matrix per car (e2e upload 1.4 KB instead of 54.5 MB of posed vertices)")
     ap.add_argument("--soup", action="store_true", help="triangle-soup scene (float4 triplets) instead of the indexed "
                     "car meshes (same triangles; the e2e upload is then every dynamic triangle's vertices)")
     ap.add_argument("--shard", default="auto", choices=["auto", "triangles", "emitters", "mixed"])
@@ -446,7 +475,7 @@ def main():
     car_scale = tuple(float(x) for x in args.car_scale.split(",")) if args.car_scale else None
     scene = Scene(args.config, s_rank, s_world, device, args.deformation, shard=shard,
                   max_range=(None if args.max_range == 0 else args.max_range), subdiv=args.subdiv, car_scale=car_scale,
-                  mesh="soup" if args.soup else "indexed")
+                  mesh="soup" if args.soup else "instances" if args.instances else "indexed")
     # The library casts the partition itself: sensor shards pass EVERY emitter (the handle casts n mod P),
     # triangle shards pass every emitter and their own triangles, a mixed partition passes its group's
     # emitters and its triangle shard; grca_cast is collective and merges in-stream (NCCL).
@@ -688,8 +717,12 @@ def main():
             dyn_ids, dyn_base = scene.ids[scene.n_static_local:], 0
 
         def hstep(k):
-            gh.update_triangles(scene.frames[k % N_FRAMES][ns3:], indices=scene.idx_dyn, tri_ids=dyn_ids,
-                                tri_id_base=dyn_base)
+            if scene.instanced:   # the dynamic set is only the instances (ids after the static ones)
+                gh.update_scene(tri_id_base=dyn_base)
+                gh.update_instances(scene.car_v_dev, scene.car_f_dev, scene.frames[k % N_FRAMES].view(-1, 3, 4))
+            else:
+                gh.update_triangles(scene.frames[k % N_FRAMES][ns3:], indices=scene.idx_dyn, tri_ids=dyn_ids,
+                                    tri_id_base=dyn_base)
             gh.cast(dist_out, tri_out)
 
         for k in range(3):
@@ -730,7 +763,7 @@ def main():
         cast_once()
         torch.cuda.synchronize()
         gd, gt = dist_out.cpu().numpy(), tri_out.cpu().numpy()
-        tris_np = scene.w["tris"]
+        tris_np = scene.frame_tris(0, scene.w["tris"])
         cpu, ref = time_oracle(ems_lib, tris_np, target_s=15.0)
         rep = oracle.compare(ems_lib, tris_np, gd[ref["rays"]], gt[ref["rays"]], ref)
         parity = {k: rep[k] for k in ("rays", "agree_frac", "disagree", "excused", "unexcused", "near_ties",
@@ -757,6 +790,11 @@ def main():
                                     f"triangle shards, all-reduce(MIN) within a group"
                                     if shard.startswith("mixed") else f"emitters (n mod P) x {world}, no reduction"),
                        "l2": (f"inputs > L2: every cast streams the resident {scene.static_soup.numel() * 4 / 1e9:.2f} GB "
+                              f"static float4 soup; the cars are rigid instances of one local mesh ("
+                              f"{(scene.car_v_np.nbytes + scene.car_f_np.nbytes) / 1e6:.1f} MB) posed by one of {N_FRAMES} "
+                              f"cycled sets of {scene.n_cars} 3x4 matrices"
+                              if scene.instanced else
+                              f"inputs > L2: every cast streams the resident {scene.static_soup.numel() * 4 / 1e9:.2f} GB "
                               f"static float4 soup + {scene.idx_dyn.numel() * 4 / 1e9:.3f} GB car indices + one of "
                               f"{N_FRAMES} cycled {scene.frames[0].numel() * 4 / 1e9:.3f} GB car-vertex frames"
                               if scene.indexed else
