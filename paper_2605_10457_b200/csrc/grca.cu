@@ -283,12 +283,12 @@ struct EmLitePack {
 // channel-culled count; c_area counts paper-mode apparent-area culls.
 // kFast: culling on, packed pairs usable, no apparent-area cull -- the mode flags are then checked
 // once per kernel instead of per triangle (k_cull_fixed picks the instantiation)
-template <int NE, bool kLevel, bool kFast>
+template <int NE, bool kLevel, bool kFast, bool kC>
 __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, const float *sSin,
                                        const unsigned char *sLut, long long t, unsigned &keep, unsigned &rng,
                                        unsigned &c_area) {
     f3 v[3];
-    load_tri(P.tri, t, v);   // A1 (fused K1)
+    load_tri<kC>(P.tri, t, v);   // A1 (fused K1)
     const float l0 = (v[1].x - v[0].x) * (v[1].x - v[0].x) + (v[1].y - v[0].y) * (v[1].y - v[0].y) +
                      (v[1].z - v[0].z) * (v[1].z - v[0].z);
     const float l1 = (v[2].x - v[1].x) * (v[2].x - v[1].x) + (v[2].y - v[1].y) * (v[2].y - v[1].y) +
@@ -358,7 +358,7 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
 }
 
 // The persistent tile loop of k_cull_fixed (one instantiation per mode, see k2_tri).
-template <int NE, bool kLevel, bool kFast>
+template <int NE, bool kLevel, bool kFast, bool kC>
 __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL, const float *sSin,
                                          const unsigned char *sLut, int *wsum, unsigned &qbase, int lane, int wib,
                                          unsigned &c_pairs, unsigned &c_range, unsigned &c_surv,
@@ -373,7 +373,7 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
             const long long t = tile * K2_TILE + h * K2_THREADS + threadIdx.x;
             unsigned keep = 0u, rng = 0u;
             if (t < P.n_tri) {
-                k2_tri<NE, kLevel, kFast>(P, EL, sSin, sLut, t, keep, rng, c_area);
+                k2_tri<NE, kLevel, kFast, kC>(P, EL, sSin, sLut, t, keep, rng, c_area);
                 c_pairs += NE;
             }
             keeps[h] = keep;
@@ -419,7 +419,7 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
     }
 }
 
-template <int NE, bool kLevel>
+template <int NE, bool kLevel, bool kC>
 __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid_constant__ KParams P, const EmLitePack EL) {
     extern __shared__ __align__(16) unsigned char smem[];
     float *sSin = reinterpret_cast<float *>(smem);
@@ -435,9 +435,9 @@ __global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned c_pairs = 0, c_range = 0, c_surv = 0, c_area = 0;
     if (!P.nocull && (P.pairs_ok || NE == 1) && !(P.area_eps2 > 0.f))
-        k2_tiles<NE, kLevel, true>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_surv, c_area);
+        k2_tiles<NE, kLevel, true, kC>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_surv, c_area);
     else
-        k2_tiles<NE, kLevel, false>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_surv, c_area);
+        k2_tiles<NE, kLevel, false, kC>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_surv, c_area);
     unsigned cnt[ST_COUNT];
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0u;
@@ -694,7 +694,7 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KP
 // list.  Warp-collective; slot / excl are this warp's shared-memory staging areas.
 // kFast: no debug / multicast modes (no-cull, forced fp64, all-hit counts, NVLS keys), so the per-
 // candidate checks of those flags compile away (the host launches this instantiation when they are off)
-template <bool kFast, bool kLevel>
+template <bool kFast, bool kLevel, bool kC>
 __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, const float *sSin,
                                              const unsigned char *sLut, float4 *slot, int *excl,
                                              unsigned long long *wc, int smax, int lane, bool valid,
@@ -711,7 +711,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
         e = (int)(ent & 255u);
         t = (long long)(ent >> 8);
         f3 v[3];
-        load_tri(P.tri, t, v);
+        load_tri<kC>(P.tri, t, v);
         const EmDev &E = sE[e];
         const int st = cull_pair<kLevel>(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
                                          !kFast && P.nocull != 0, R);
@@ -861,7 +861,7 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
             fb = r == 2;
             if (r == 2) {   // rare: reload the ray (keeping d live into the fp64 code spills it)
                 f3 wv[3];
-                load_tri(P.tri, (long long)__float_as_int(r4.z), wv);
+                load_tri<kC>(P.tri, (long long)__float_as_int(r4.z), wv);
                 const float4 d2 = __ldcg(P.raytab + chk_idx(g, P.n_rays, CHK_RAY));
                 r = test_exact_r<true>(wv, em_o(EO), d2, EO.dmax, P.faces, th);
             }
@@ -890,7 +890,7 @@ __device__ __forceinline__ unsigned atom_add_u32(unsigned *p, unsigned v) {
     return old;
 }
 
-template <bool kFast, bool kLevel>
+template <bool kFast, bool kLevel, bool kC>
 __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __grid_constant__ KParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     float4 *sSlot = reinterpret_cast<float4 *>(smem);   // [warp][6][32]
@@ -934,7 +934,7 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
             const unsigned idx = (w + f) * 32u + (unsigned)lane;
             const bool valid = idx < ns;
             if (!__any_sync(FULL, valid)) break;
-            refine_round<kFast, kLevel>(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
+            refine_round<kFast, kLevel, kC>(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
                                         valid ? __ldcs(P.surv + idx) : 0ull);
         }
         w = __shfl_sync(FULL, wn, 0) * fetch;
@@ -1487,17 +1487,28 @@ KParams params(grca_t h) {
 }
 }  // namespace
 
-static const void *k2_fixed_fn(int ne, bool level) {
+template <bool kC>
+static const void *k2_fixed_fn_c(int ne, bool level) {
     switch (ne) {
-        case 1: return level ? (const void *)k_cull_fixed<1, true> : (const void *)k_cull_fixed<1, false>;
-        case 2: return level ? (const void *)k_cull_fixed<2, true> : (const void *)k_cull_fixed<2, false>;
-        case 3: return level ? (const void *)k_cull_fixed<3, true> : (const void *)k_cull_fixed<3, false>;
-        case 4: return level ? (const void *)k_cull_fixed<4, true> : (const void *)k_cull_fixed<4, false>;
-        case 5: return level ? (const void *)k_cull_fixed<5, true> : (const void *)k_cull_fixed<5, false>;
-        case 6: return level ? (const void *)k_cull_fixed<6, true> : (const void *)k_cull_fixed<6, false>;
-        case 7: return level ? (const void *)k_cull_fixed<7, true> : (const void *)k_cull_fixed<7, false>;
-        default: return level ? (const void *)k_cull_fixed<8, true> : (const void *)k_cull_fixed<8, false>;
+        case 1: return level ? (const void *)k_cull_fixed<1, true, kC> : (const void *)k_cull_fixed<1, false, kC>;
+        case 2: return level ? (const void *)k_cull_fixed<2, true, kC> : (const void *)k_cull_fixed<2, false, kC>;
+        case 3: return level ? (const void *)k_cull_fixed<3, true, kC> : (const void *)k_cull_fixed<3, false, kC>;
+        case 4: return level ? (const void *)k_cull_fixed<4, true, kC> : (const void *)k_cull_fixed<4, false, kC>;
+        case 5: return level ? (const void *)k_cull_fixed<5, true, kC> : (const void *)k_cull_fixed<5, false, kC>;
+        case 6: return level ? (const void *)k_cull_fixed<6, true, kC> : (const void *)k_cull_fixed<6, false, kC>;
+        case 7: return level ? (const void *)k_cull_fixed<7, true, kC> : (const void *)k_cull_fixed<7, false, kC>;
+        default: return level ? (const void *)k_cull_fixed<8, true, kC> : (const void *)k_cull_fixed<8, false, kC>;
     }
+}
+// kc: the triangle set has part C (instances): the instantiation whose loads handle it
+static const void *k2_fixed_fn(int ne, bool level, bool kc = false) {
+    return kc ? k2_fixed_fn_c<true>(ne, level) : k2_fixed_fn_c<false>(ne, level);
+}
+// the fused kernel's instantiations: (fast modes, level frames, part C)
+static const void *kf_fn(bool fast, bool level, bool kc) {
+    if (!fast) return kc ? (const void *)k_refine_small<false, false, true> : (const void *)k_refine_small<false, false, false>;
+    if (level) return kc ? (const void *)k_refine_small<true, true, true> : (const void *)k_refine_small<true, true, false>;
+    return kc ? (const void *)k_refine_small<true, false, true> : (const void *)k_refine_small<true, false, false>;
 }
 
 static size_t k2_smem_bytes(int n_em, int n_sin, bool lut) {
@@ -1600,9 +1611,9 @@ grca_status grca_create(const grca_create_info *ci, grca_t *out) {
     cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k2b_smem_bytes(kMaxEmitters, kMaxSin, false));
     cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)k4s_smem_bytes(kMaxEmitters));
-    for (const void *f : {(const void *)k_refine_small<true, true>, (const void *)k_refine_small<true, false>,
-                          (const void *)k_refine_small<false, false>})
-        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kfused_smem_bytes(kMaxEmitters, kMaxSin, false));
+    for (bool kc : {false, true})
+        for (const void *f : {kf_fn(true, true, kc), kf_fn(true, false, kc), kf_fn(false, false, kc)})
+            cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kfused_smem_bytes(kMaxEmitters, kMaxSin, false));
     for (const void *f : {(const void *)k_isect<true>, (const void *)k_isect<false>})
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(sizeof(EmDev) * kMaxEmitters));
     {   // opt-in persisting L2 window for the ray table + hits (measured: no gain at C4 after the
@@ -1929,14 +1940,15 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
                                                " B of shared memory per block (> the device's opt-in limit)");
         if (n_own >= 1 && n_own <= kFixedEm && use_lut)
             for (bool lv : {false, true})
-                CK(cudaFuncSetAttribute(k2_fixed_fn(n_own, lv), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)h->k2f_smem));
+                for (bool kc : {false, true})
+                    CK(cudaFuncSetAttribute(k2_fixed_fn(n_own, lv, kc), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)h->k2f_smem));
         CK(cudaFuncSetAttribute(k_cull, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k2_smem));
         CK(cudaFuncSetAttribute(k_refine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k2b_smem));
         CK(cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->k4s_smem));
-        for (const void *f : {(const void *)k_refine_small<true, true>, (const void *)k_refine_small<true, false>,
-                              (const void *)k_refine_small<false, false>})
-            CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->kf_smem));
+        for (bool kc : {false, true})
+            for (const void *f : {kf_fn(true, true, kc), kf_fn(true, false, kc), kf_fn(false, false, kc)})
+                CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->kf_smem));
     }
     int b2 = 0, b2b = 0, b4s = 0, b4 = 0;
     if (n_own >= 1 && n_own <= kFixedEm && use_lut) {   // the fixed kernel relies on the LUT (gamma <= 255)
@@ -1949,7 +1961,7 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4s, k_small, K2_THREADS, h->k4s_smem));
     h->k4s_blocks_per_sm = std::max(1, b4s);
     int bf = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, k_refine_small<true, false>, KF_THREADS, h->kf_smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bf, kf_fn(true, false, false), KF_THREADS, h->kf_smem));
     h->kf_blocks_per_sm = std::max(1, bf);
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b4, k_isect<true>, K4_THREADS, sizeof(EmDev) * std::max(1, n_own)));
     h->k2_blocks_per_sm = std::max(1, b2);
@@ -2146,7 +2158,8 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
         const long long grid = std::min<long long>(tiles, (long long)h->num_sms * h->k2_blocks_per_sm);
         if (h->n_em <= kFixedEm && h->use_lut) {
             void *args[] = {(void *)&P, (void *)&h->lite_pack};
-            CK(cudaLaunchKernel(k2_fixed_fn(h->n_em, h->all_level && P.pairs_ok), dim3((unsigned)grid), dim3(K2_THREADS), args, h->k2f_smem,
+            CK(cudaLaunchKernel(k2_fixed_fn(h->n_em, h->all_level && P.pairs_ok, P.tri.n_c0 != LLONG_MAX), dim3((unsigned)grid),
+                                dim3(K2_THREADS), args, h->k2f_smem,
                                 h->stream));
         } else {
             k_cull<<<(unsigned)grid, K2_THREADS, h->k2_smem, h->stream>>>(P);
@@ -2166,9 +2179,7 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
             k_small<<<(unsigned)grid, K2_THREADS, h->k4s_smem, h->stream>>>(P);
         } else {
             const long long grid = (long long)h->num_sms * h->kf_blocks_per_sm;
-            const void *kf = !fast_modes(P) ? (const void *)k_refine_small<false, false>
-                             : h->all_dev_level ? (const void *)k_refine_small<true, true>
-                                                : (const void *)k_refine_small<true, false>;
+            const void *kf = kf_fn(fast_modes(P), h->all_dev_level, P.tri.n_c0 != LLONG_MAX);
             CK(launch_l2(h, kf, (unsigned)grid, KF_THREADS, h->kf_smem, P));
         }
         CK(cudaGetLastError());

@@ -202,11 +202,14 @@ void load_instance_tri(const TriSrc &T, long long u, f3 v[3]) {
     }
 }
 
+// kC: the set may have part C (instances).  The hot kernels (K2, the fused kernel) are instantiated with
+// kC = false for sets without instances, so their triangle loads carry no part-C branch at all.
+template <bool kC = true>
 __device__ __forceinline__ void load_tri(const TriSrc &T, long long t, f3 v[3]) {
 #ifdef GRCA_CHECK
     t = chk_idx(t, T.n_t, CHK_TRI);
 #endif
-    if (t >= T.n_c0) {   // part C: a rigid instance of the local mesh (grca_update_instances)
+    if (kC && t >= T.n_c0) {   // part C: a rigid instance of the local mesh (grca_update_instances)
         load_instance_tri(T, t - T.n_c0, v);
         return;
     }

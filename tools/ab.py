@@ -47,7 +47,7 @@ def main():
     kms, sts = {}, {}
     for p in range(passes):
         for n in names:
-            env = dict(os.environ, GRCA_LIB=os.path.join(OUT, f"lib_{n}.so"))
+            env = dict(os.environ, GRCA_LIB=os.path.join(OUT, f"lib_{n}.so"), GRCA_AB_OLD_LIB="1")
             cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", config, "--steps", steps, "--warmup", "10",
                    "--no-cpu-baseline", "--no-e2e", "--no-hybrid"] + extra
             r = subprocess.run(cmd, env=env, capture_output=True, text=True)
