@@ -101,13 +101,14 @@ class Scene:
     float4 triplets per triangle, one buffer per frame (static part copied into each)."""
 
     def __init__(self, config: str, rank: int, world: int, device, deformation: str = "ND", shard: str = "triangles",
-                 max_range=-1.0, subdiv: int = 0, car_scale=None, mesh: str = "indexed"):
+                 max_range=-1.0, subdiv: int = 0, car_scale=None, mesh: str = "indexed", w=None):
         import torch
 
         from paper_2605_10457_b200 import dist as D
         from paper_2605_10457_b200 import tris_to_float4
 
-        w = sg.workload(config, frame=0, deformation=deformation, max_range=max_range, subdiv=subdiv)
+        if w is None:
+            w = sg.workload(config, frame=0, deformation=deformation, max_range=max_range, subdiv=subdiv)
         self.w = w
         self.scale = car_scale or sg.WORKLOADS.get(config, (0,) * 7)[6] if config != "C1" else (1.0, 1.0)
         self.emitters = w["emitters"]
@@ -388,6 +389,8 @@ def main():
                     "as one CUDA graph, the default: C4 1.053 vs 1.064 ms, C2 0.105 vs 0.115 ms)")
     ap.add_argument("--collective", action="store_true", help="N=1: cast through a one-rank NCCL communicator "
                     "(the library's collective path, merge included) instead of a plain handle")
+    ap.add_argument("--e2e-vertices", action="store_true", help="e2e uploads the posed car vertices (54.5 MB per C4 "
+                    "frame) instead of one 3x4 matrix per car")
     ap.add_argument("--instances", action="store_true", help="cars as rigid instances (grca_update_instances): a frame's "
                     "input is one 3x4 matrix per car (e2e upload 1.4 KB instead of 54.5 MB of posed vertices)")
     ap.add_argument("--soup", action="store_true", help="triangle-soup scene (float4 triplets) instead of the indexed "
@@ -592,15 +595,23 @@ def main():
     # are inside the timed region (which starts before the first H2D and ends after the last D2H).
     e2e = None
     if not args.no_e2e:
+        # rigid cars: the e2e input is one 3x4 matrix per car per frame (grca_update_instances), the natural host
+        # input for the paper's rigid dynamic instances; --e2e-vertices (or a layout without whole instances on
+        # this rank) uploads the posed vertices instead
+        es = scene
+        if not args.e2e_vertices and scene.indexed and scene.identity:
+            es = Scene(args.config, s_rank, s_world, device, args.deformation, shard=shard,
+                       max_range=(None if args.max_range == 0 else args.max_range), subdiv=args.subdiv,
+                       car_scale=car_scale, mesh="instances", w=scene.w)
         # N > 1: each rank uploads 1/N of the dynamic vertices over its own PCIe link and an
         # all-gather over NVLink assembles the rest (inside the timed region); each rank reads back
         # only its own results (sensor shards: its emitters' rays; triangle shards: 1/N of the rays)
-        ns3 = scene.fs                                  # static rows carried in a frame buffer
-        comps = scene.frames[0].shape[1]
-        n_dyn = scene.frames[0].shape[0] - ns3          # dynamic vertices per frame
+        ns3 = es.fs                                  # static rows carried in a frame buffer
+        comps = es.frames[0].shape[1]
+        n_dyn = es.frames[0].shape[0] - ns3          # dynamic vertices per frame
         # split only when every rank needs the same dynamic data (indexed scene: all car vertices;
         # sensor shards: all triangles); a triangle-sharded soup holds per-rank data
-        split = world > 1 and (scene.indexed or shard == "emitters")
+        split = world > 1 and (es.indexed or shard == "emitters")
         nsplit = world if split else 1
         chunk = -(-n_dyn // nsplit)                     # per-rank upload slice (padded)
         lo_v = (rank if split else 0) * chunk
@@ -608,12 +619,12 @@ def main():
         host_dyn = []
         for f in range(N_FRAMES):
             hs = torch.zeros((chunk, comps), dtype=torch.float32)
-            hs[:n_mine] = scene.frames[f][ns3 + lo_v: ns3 + lo_v + n_mine].cpu()
+            hs[:n_mine] = es.frames[f][ns3 + lo_v: ns3 + lo_v + n_mine].cpu()
             host_dyn.append(hs.pin_memory())
         dev_bufs = []
         for _ in range(2):   # static part resident; dynamic part (padded to world * chunk) uploaded
             db = torch.zeros((ns3 + chunk * nsplit, comps), dtype=torch.float32, device=device)
-            db[:ns3] = scene.frames[0][:ns3]
+            db[:ns3] = es.frames[0][:ns3]
             dev_bufs.append(db)
         outs = [(torch.empty(n_rays, dtype=torch.float32, device=device),
                  torch.empty(n_rays, dtype=torch.int32, device=device)) for _ in range(2)]
@@ -635,7 +646,7 @@ def main():
         ev_h2d = [torch.cuda.Event() for _ in range(2)]
         ev_cast = [torch.cuda.Event() for _ in range(2)]
         ev_d2h = [torch.cuda.Event() for _ in range(2)]
-        k_e2e = max(4, min(args.steps, 40))
+        k_e2e = max(50, min(args.steps, 200))   # >= 50 frames, like the headline pacing
 
         def issue_h2d(k):
             b = k % 2
@@ -657,7 +668,7 @@ def main():
                 stream.wait_event(ev_h2d[b])
                 if k >= 2:
                     stream.wait_event(ev_d2h[b])   # host copy of step k-2 done with outs[b]
-                scene.bind(g, dev_bufs[b], n_triangles=scene.n_tri)
+                es.bind(g, dev_bufs[b], n_triangles=es.n_tri)
                 cast_once(*outs[b])
                 ev_cast[b].record(stream)
                 if k + 1 < n:
@@ -692,15 +703,19 @@ def main():
         last = (k_e2e - 1) % 2
         assert torch.equal(host_out[last][1], torch.cat([outs[last][1][lo: lo + nn] for lo, nn in ranges]).cpu())
         fr = (k_e2e - 1) % N_FRAMES
-        assert torch.equal(dev_bufs[last][ns3: ns3 + n_dyn], scene.frames[fr][ns3:])
+        assert torch.equal(dev_bufs[last][ns3: ns3 + n_dyn], es.frames[fr][ns3:])
         e2e = {"value": n_rays_job * k_e2e / (ems_e2e / 1e3), "unit": "rays/s", "ms_per_step": ems_e2e / k_e2e,
                "h2d_bytes_per_step": int(chunk * comps * 4), "d2h_bytes_per_step": int(r_n * 8), "steps": k_e2e,
                "bytes_scope": "per rank" if world > 1 else "job",
-               "what": f"pinned H2D of this frame's dynamic vertices ({scene.mesh} mesh"
+               "what": (f"pinned H2D of this frame's car poses (one 3x4 matrix per car: rigid instances, "
+                        f"grca_update_instances" if es.instanced else
+                        f"pinned H2D of this frame's dynamic vertices ({es.mesh} mesh") +
                        f"{', 1/N per rank + NVLink all-gather' if split else ''}) + grca_cast + D2H of "
                        "(dist, id) per ray; pipelined over frames (double buffers, H2D/D2H on two copy "
                        "streams overlap the previous/next cast)"}
         del dev_bufs
+        if es is not scene:
+            del es
 
     # ---- hybrid static/dynamic (NEXT-f2; NOT the headline: static triangles cached across frames)
     hybrid = None
