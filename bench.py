@@ -387,6 +387,8 @@ def main():
                          "multimem.red.min into an NCCL symmetric window (NEXT-f3; needs NVLS multicast)")
     ap.add_argument("--no-graph", action="store_true", help="plain launches instead of GRCA_USE_CUDA_GRAPH (each cast "
                     "as one CUDA graph, the default: C4 1.053 vs 1.064 ms, C2 0.105 vs 0.115 ms)")
+    ap.add_argument("--logic-check", action="store_true", help="N > 1 on one GPU over gloo with virtual-rank handles: "
+                    "a check of the multi-rank host logic, not a measurement")
     ap.add_argument("--collective", action="store_true", help="N=1: cast through a one-rank NCCL communicator "
                     "(the library's collective path, merge included) instead of a plain handle")
     ap.add_argument("--e2e-vertices", action="store_true", help="e2e uploads the posed car vertices (54.5 MB per C4 "
@@ -455,10 +457,17 @@ def main():
     from paper_2605_10457_b200 import dist as D
     from paper_2605_10457_b200 import grca as G
 
-    dev_index = local_rank
+    # --logic-check: several ranks on ONE GPU over gloo, handles in virtual-rank mode (no NCCL: it refuses two
+    # ranks on one device) -- exercises the N > 1 host logic (partitions, e2e split / all-gather / readback
+    # ranges, timing); not a measurement, and triangle shards are left unmerged
+    logic = world > 1 and args.logic_check
+    dev_index = local_rank % max(1, torch.cuda.device_count()) if logic else local_rank
     if world > 1:
         torch.cuda.set_device(dev_index)
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev_index}"))
+        if logic:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev_index}"))
     device = torch.device(f"cuda:{dev_index}")
     torch.cuda.set_device(device)
     # one non-default stream for everything (scene set-up, casts, events): a stream the library can capture
@@ -498,14 +507,16 @@ def main():
             gi, ti, T = D.mixed_partition(rank, world, n_groups)
             subs = [dist.new_group(ranks=[gg * T + t for t in range(T)]) for gg in range(n_groups)]
             coll_group, c_ranks, c_rank = subs[gi], T, ti
+        if logic:
+            mode_flags |= G.DEBUG_VIRTUAL_RANKS
     elif args.emulate_world > 1:        # this rank's exact share, no collective (library virtual ranks)
         c_ranks, c_rank = s_world, s_rank
         mode_flags |= G.DEBUG_VIRTUAL_RANKS
-    collective = world > 1 or args.collective
+    collective = (world > 1 and not logic) or args.collective
 
     def new_handle(flags):
         uid = None
-        if world > 1:
+        if world > 1 and not logic:
             uid = D.nccl_uid(coll_group)
         elif args.collective:
             uid = G.nccl_unique_id()
