@@ -54,3 +54,24 @@ def test_indexed_frame_reproduces_the_soup():
     v, idx = sg.indexed_frame(w)
     assert idx.shape == (3 * len(w["tris"]),) and v.shape[0] == 3 * w["n_static"] + 2 * 389 * 389
     assert np.array_equal(v[idx].reshape(-1, 3, 3), w["tris"])
+
+
+def test_pose_f32_matches_definition():
+    """scenegen.apply_pose_f32 is grca_update_instances' documented fp32 order (include/grca.h): per row,
+    ((m0 x + m1 y) + m2 z) + m3 with every product and sum rounded; it agrees with the fp64 pose to fp32
+    accuracy, and equals an element-by-element Python-float32 evaluation bit for bit."""
+    import numpy as np
+    import scenegen as sg
+
+    v, f = sg.car_mesh(12, 12)
+    p = sg.pose_instances(1, (50.0, 40.0, 10.0), seed=3, frame=2)[0]
+    M = sg.pose_matrix(p)
+    a = sg.apply_pose_f32(v, M)
+    b = sg.apply_pose(v, p)
+    np.testing.assert_allclose(a, b, rtol=0, atol=2e-5 * (1 + np.abs(b).max()))
+    f32 = np.float32
+    for k in (0, 7, len(v) - 1):
+        x, y, z = (f32(c) for c in v[k])
+        for r in range(3):
+            want = f32(f32(f32(f32(M[r, 0] * x) + f32(M[r, 1] * y)) + f32(M[r, 2] * z)) + M[r, 3])
+            assert a[k, r] == want
