@@ -850,6 +850,8 @@ def main():
                        "(3.9e8 rays/s), 1.98x OptiX 9.1; other hardware, not a target",
         }
         print(json.dumps(line))
+    torch.cuda.synchronize()
+    g.close()   # (its NCCL communicator, if any, before the process group)
     if world > 1:
         dist.destroy_process_group()
 
