@@ -274,6 +274,8 @@ grca_status grca_cast(grca_t h, float *d_out_dist, int32_t *d_out_tri, grca_stat
  * min-allreduce merges shards exactly).  grca_hits_packed returns its device pointer.
  * grca_unpack runs K5 from that buffer (after the caller's merge). */
 grca_status grca_cast_packed(grca_t h);
+/* (Under emitter shards without gather_outputs only this rank's emitters' keys are initialised and valid; under a
+ * reduce-scatter merge the buffer holds this rank's unmerged keys -- the merged slice is what grca_cast unpacks.) */
 grca_status grca_hits_packed(grca_t h, uint64_t **d_hits, int64_t *n_rays);
 grca_status grca_unpack(grca_t h, float *d_out_dist, int32_t *d_out_tri);
 /* K5 over a slice of the rays, for ray-sharded merges (a reduce-scatter(MIN) leaves
