@@ -283,10 +283,12 @@ struct EmLitePack {
 // channel-culled count; c_area counts paper-mode apparent-area culls.
 // kFast: culling on, packed pairs usable, no apparent-area cull -- the mode flags are then checked
 // once per kernel instead of per triangle (k_cull_fixed picks the instantiation)
-template <int NE, bool kLevel, bool kFast>
-__device__ __forceinline__ void k2_tri_v(const KParams &P, const EmLitePack &EL, const float *sSin,
-                                         const unsigned char *sLut, const f3 v[3], unsigned &keep, unsigned &rng,
-                                         unsigned &c_area) {
+template <int NE, bool kLevel, bool kFast, bool kC>
+__device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, const float *sSin,
+                                       const unsigned char *sLut, long long t, unsigned &keep, unsigned &rng,
+                                       unsigned &c_area) {
+    f3 v[3];
+    load_tri<kC>(P.tri, t, v);   // A1 (fused K1)
     const float l0 = (v[1].x - v[0].x) * (v[1].x - v[0].x) + (v[1].y - v[0].y) * (v[1].y - v[0].y) +
                      (v[1].z - v[0].z) * (v[1].z - v[0].z);
     const float l1 = (v[2].x - v[1].x) * (v[2].x - v[1].x) + (v[2].y - v[1].y) * (v[2].y - v[1].y) +
@@ -355,78 +357,14 @@ __device__ __forceinline__ void k2_tri_v(const KParams &P, const EmLitePack &EL,
     rng = rb;
 }
 
-template <int NE, bool kLevel, bool kFast, bool kC>
-__device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, const float *sSin,
-                                       const unsigned char *sLut, long long t, unsigned &keep, unsigned &rng,
-                                       unsigned &c_area) {
-    f3 v[3];
-    load_tri<kC>(P.tri, t, v);   // A1 (fused K1)
-    k2_tri_v<NE, kLevel, kFast>(P, EL, sSin, sLut, v, keep, rng, c_area);
-}
-
-// ---- bulk-copy staging of the triangle stream (K2 for NE <= 2: the sensor-shard ranks of a multi-GPU run)
-// A tile of K2_TILE float4-soup triangles (48 KB) is copied global -> shared by one cp.async.bulk (TMA bulk
-// copy engine, completion on an mbarrier), double-buffered: the next tile streams in while this one is
-// tested, and the threads read their vertices with LDS instead of carrying global-load latency.
-constexpr unsigned kBulkTileBytes = K2_TILE * 48u;
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-    return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void bulk_issue(unsigned long long *mbar, void *dst, const void *src, unsigned bytes) {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of dst before the copy
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes)
-                 : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(mbar))
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_wait(unsigned long long *mbar, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
-            smem_u32(mbar)),
-        "r"(parity)
-        : "memory");
-}
-// the tile's float4 triplets when it lies entirely in a float4 soup (part A, or a non-indexed float4 part B),
-// else NULL: bulk-copyable tiles
-__device__ __forceinline__ const float4 *k2_bulk_src(const KParams &P, long long tile) {
-    const long long t0 = tile * K2_TILE, t1 = t0 + K2_TILE;
-    if (t1 > P.n_tri) return nullptr;
-    if (t1 <= P.tri.n_a) return P.tri.va + 3 * t0;
-    if (t0 >= P.tri.n_a && P.tri.v && !P.tri.idx && !P.tri.v3) return P.tri.v + 3 * (t0 - P.tri.n_a);
-    return nullptr;
-}
-
 // The persistent tile loop of k_cull_fixed (one instantiation per mode, see k2_tri).
-template <int NE, bool kLevel, bool kFast, bool kC, bool kBulk>
+template <int NE, bool kLevel, bool kFast, bool kC>
 __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL, const float *sSin,
                                          const unsigned char *sLut, int *wsum, unsigned &qbase, int lane, int wib,
                                          unsigned &c_pairs, unsigned &c_range, unsigned &c_surv,
-                                         unsigned &c_area, float4 *stage, unsigned long long *mbar) {
+                                         unsigned &c_area) {
     const long long ntiles = (P.n_tri + K2_TILE - 1) / K2_TILE;
-    unsigned phase = 0u;   // kBulk: parity of each stage's next completion (bit s)
-    if (kBulk && threadIdx.x == 0 && blockIdx.x < ntiles) {
-        const float4 *src = k2_bulk_src(P, blockIdx.x);
-        if (src) bulk_issue(mbar, stage, src, kBulkTileBytes);
-    }
-    int it = 0;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-        const int sb = it & 1;
-        bool bulk = false;
-        if (kBulk) {
-            const long long nxt = tile + gridDim.x;
-            // the other stage was last read in the previous iteration, before its closing barrier
-            if (threadIdx.x == 0 && nxt < ntiles) {
-                const float4 *src = k2_bulk_src(P, nxt);
-                if (src) bulk_issue(mbar + (sb ^ 1), stage + (sb ^ 1) * 3 * K2_TILE, src, kBulkTileBytes);
-            }
-            bulk = k2_bulk_src(P, tile) != nullptr;
-            if (bulk) {
-                bulk_wait(mbar + sb, (phase >> sb) & 1u);
-                phase ^= 1u << sb;
-            }
-        }
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         // K2_TILE / K2_THREADS triangles per thread (one block scan, barrier pair and atomic for all)
         unsigned keeps[K2_TILE / K2_THREADS];
         int cntk = 0;
@@ -435,13 +373,7 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
             const long long t = tile * K2_TILE + h * K2_THREADS + threadIdx.x;
             unsigned keep = 0u, rng = 0u;
             if (t < P.n_tri) {
-                if (kBulk && bulk) {
-                    const float4 *q = stage + sb * 3 * K2_TILE + 3 * (h * K2_THREADS + threadIdx.x);
-                    const f3 v[3] = {mk(q[0]), mk(q[1]), mk(q[2])};
-                    k2_tri_v<NE, kLevel, kFast>(P, EL, sSin, sLut, v, keep, rng, c_area);
-                } else {
-                    k2_tri<NE, kLevel, kFast, kC>(P, EL, sSin, sLut, t, keep, rng, c_area);
-                }
+                k2_tri<NE, kLevel, kFast, kC>(P, EL, sSin, sLut, t, keep, rng, c_area);
                 c_pairs += NE;
             }
             keeps[h] = keep;
@@ -487,23 +419,14 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
     }
 }
 
-template <int NE, bool kLevel, bool kC, bool kBulk = false>
-__global__ void __launch_bounds__(K2_THREADS, kBulk ? 2 : K2_MINB)
-    k_cull_fixed(const __grid_constant__ KParams P, const EmLitePack EL) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    // kBulk: [2 stages of K2_TILE float4 triplets][sin table][LUTs]; else [sin table][LUTs]
-    float4 *stage = reinterpret_cast<float4 *>(smem);
-    float *sSin = reinterpret_cast<float *>(smem + (kBulk ? 2 * kBulkTileBytes : 0));
+template <int NE, bool kLevel, bool kC>
+__global__ void __launch_bounds__(K2_THREADS, K2_MINB) k_cull_fixed(const __grid_constant__ KParams P, const EmLitePack EL) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float *sSin = reinterpret_cast<float *>(smem);
     unsigned char *sLut = reinterpret_cast<unsigned char *>(sSin + ((P.n_sin + 3) & ~3));
     __shared__ int wsum[K2_THREADS / 32];
     __shared__ unsigned qbase;
     __shared__ unsigned long long acc[ST_COUNT];
-    __shared__ __align__(8) unsigned long long mbar[2];
-    if (kBulk && threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar + 1)) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
     for (int i = threadIdx.x; i < P.n_sin; i += blockDim.x) sSin[i] = P.sin[i];
     if (P.lut)
         for (int i = threadIdx.x; i < NE * kLutBins; i += blockDim.x) sLut[i] = P.lut[i];
@@ -512,11 +435,9 @@ __global__ void __launch_bounds__(K2_THREADS, kBulk ? 2 : K2_MINB)
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     unsigned c_pairs = 0, c_range = 0, c_surv = 0, c_area = 0;
     if (!P.nocull && (P.pairs_ok || NE == 1) && !(P.area_eps2 > 0.f))
-        k2_tiles<NE, kLevel, true, kC, kBulk>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_surv,
-                                              c_area, stage, mbar);
+        k2_tiles<NE, kLevel, true, kC>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_surv, c_area);
     else
-        k2_tiles<NE, kLevel, false, kC, kBulk>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_surv,
-                                               c_area, stage, mbar);
+        k2_tiles<NE, kLevel, false, kC>(P, EL, sSin, sLut, wsum, qbase, lane, wib, c_pairs, c_range, c_surv, c_area);
     unsigned cnt[ST_COUNT];
 #pragma unroll
     for (int c = 0; c < ST_COUNT; ++c) cnt[c] = 0u;
@@ -1362,8 +1283,6 @@ struct grca_ctx {
     bool all_dev_level = false;   // every EmDev.level (cull_pair's level instantiation)
     unsigned long long noise_seed = 0;   // persisting window over ray table + hits (num_bytes 0 = off)
     size_t k2f_smem = 0;
-    size_t k2bulk_smem = 0;   // bulk-staged K2: 2 tile stages + k2f_smem (0: not used for these emitters)
-    int k2bulk_blocks_per_sm = 0;
     int4 *d_large = nullptr;
     int4 *d_chunks = nullptr;
     float4 *d_large_setup = nullptr;
@@ -1584,14 +1503,6 @@ static const void *k2_fixed_fn_c(int ne, bool level) {
 // kc: the triangle set has part C (instances): the instantiation whose loads handle it
 static const void *k2_fixed_fn(int ne, bool level, bool kc = false) {
     return kc ? k2_fixed_fn_c<true>(ne, level) : k2_fixed_fn_c<false>(ne, level);
-}
-#ifndef K2_BULK_MAX_NE
-#define K2_BULK_MAX_NE 0   // K2 with bulk-copy staged soup tiles for NE <= this (0: off)
-#endif
-// the bulk-staged K2 (NE <= 2, no part C)
-static const void *k2_bulk_fn(int ne, bool level) {
-    if (ne == 1) return level ? (const void *)k_cull_fixed<1, true, false, true> : (const void *)k_cull_fixed<1, false, false, true>;
-    return level ? (const void *)k_cull_fixed<2, true, false, true> : (const void *)k_cull_fixed<2, false, false, true>;
 }
 // the fused kernel's instantiations: (fast modes, level frames, part C)
 static const void *kf_fn(bool fast, bool level, bool kc) {
@@ -2039,23 +1950,6 @@ grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitte
             for (const void *f : {kf_fn(true, true, kc), kf_fn(true, false, kc), kf_fn(false, false, kc)})
                 CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->kf_smem));
     }
-    h->k2bulk_smem = 0;
-    h->k2bulk_blocks_per_sm = 0;
-    if (n_own >= 1 && n_own <= std::min(2, K2_BULK_MAX_NE) && use_lut) {
-        const size_t bs = 2 * (size_t)kBulkTileBytes + h->k2f_smem;
-        int max_optin = 0;
-        cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
-        if ((size_t)max_optin >= bs) {
-            int bb = 0;
-            for (bool lv : {false, true})
-                CK(cudaFuncSetAttribute(k2_bulk_fn(n_own, lv), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bs));
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bb, k2_bulk_fn(n_own, false), K2_THREADS, bs));
-            if (bb > 0) {
-                h->k2bulk_smem = bs;
-                h->k2bulk_blocks_per_sm = bb;
-            }
-        }
-    }
     int b2 = 0, b2b = 0, b4s = 0, b4 = 0;
     if (n_own >= 1 && n_own <= kFixedEm && use_lut) {   // the fixed kernel relies on the LUT (gamma <= 255)
         const void *fn = k2_fixed_fn(n_own, false);
@@ -2262,16 +2156,9 @@ static grca_status launch_core(grca_t h, KParams &P, long long n_tri, bool prof,
     if (n_tri > 0) {   // K2
         const long long tiles = (n_tri + K2_THREADS - 1) / K2_THREADS;
         const long long grid = std::min<long long>(tiles, (long long)h->num_sms * h->k2_blocks_per_sm);
-        const bool part_c = P.tri.n_c0 != LLONG_MAX;
-        const bool soup = P.tri.n_a >= K2_TILE || (P.tri.v && !P.tri.idx && !P.tri.v3 && n_tri >= K2_TILE);
-        if (h->k2bulk_smem && !part_c && soup) {   // bulk-staged soup tiles (NE <= 2)
+        if (h->n_em <= kFixedEm && h->use_lut) {
             void *args[] = {(void *)&P, (void *)&h->lite_pack};
-            const long long gb = std::min<long long>(tiles, (long long)h->num_sms * h->k2bulk_blocks_per_sm);
-            CK(cudaLaunchKernel(k2_bulk_fn(h->n_em, h->all_level && P.pairs_ok), dim3((unsigned)gb), dim3(K2_THREADS), args,
-                                h->k2bulk_smem, h->stream));
-        } else if (h->n_em <= kFixedEm && h->use_lut) {
-            void *args[] = {(void *)&P, (void *)&h->lite_pack};
-            CK(cudaLaunchKernel(k2_fixed_fn(h->n_em, h->all_level && P.pairs_ok, part_c), dim3((unsigned)grid),
+            CK(cudaLaunchKernel(k2_fixed_fn(h->n_em, h->all_level && P.pairs_ok, P.tri.n_c0 != LLONG_MAX), dim3((unsigned)grid),
                                 dim3(K2_THREADS), args, h->k2f_smem,
                                 h->stream));
         } else {
