@@ -683,100 +683,11 @@ __global__ void __launch_bounds__(K2_THREADS) k_small(const __grid_constant__ KP
     block_flush(acc, P.stats, cnt);
 }
 
-// ----------------------------------------- K2b+K4s fused: refine + small work --
-// One warp per 32-survivor round (interleaved over all warps): lane-per-survivor exact rectangle
-// (cull_pair), certified setup of small rectangles into shared-memory float4 slots, then the
-// warp expands all items of its small rectangles with a prefix scan (A5) and tests them 32 at a
-// time (A6).  Large rectangles go to the large list (K3/K4).  One vertex fetch per survivor.
-// One round of the fused refine + small expansion (A4-A6) for up to 32 survivor entries
-// (tri << 8 | emitter, one per lane, valid lanes only): exact rectangle (cull_pair), small
-// rectangles set up and expanded over the warp (prefix scan), large ones appended to the large
-// list.  Warp-collective; slot / excl are this warp's shared-memory staging areas.
-// kFast: no debug / multicast modes (no-cull, forced fp64, all-hit counts, NVLS keys), so the per-
-// candidate checks of those flags compile away (the host launches this instantiation when they are off)
-template <bool kFast, bool kLevel, bool kC>
-__device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, const float *sSin,
-                                             const unsigned char *sLut, float4 *slot, int *excl,
-                                             unsigned long long *wc, int smax, int lane, bool valid,
-                                             unsigned long long ent) {
-    // per-lane category = the stat it counts (warp-private counters wc[], no atomics)
-    enum { C_NONE = -1, C_SMALL = ST_SMALL, C_LARGE = ST_LARGE, C_OVF = ST_OVF_LARGE, C_RANGE = ST_RANGE,
-           C_CHAN = ST_CHANNEL, C_AZI = ST_AZIMUTH, C_DEGEN = ST_DEGEN };
-    int my = 0, e = 0, cat = C_NONE;
-    bool sat = false, bat = false;   // paper classification counters (PAPER.md:727-752)
-    long long t = 0;
-    Rect R;
-    bool large = false;
-    if (valid) {
-        e = (int)(ent & 255u);
-        t = (long long)(ent >> 8);
-        f3 v[3];
-        load_tri<kC>(P.tri, t, v);
-        const EmDev &E = sE[e];
-        const int st = cull_pair<kLevel>(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
-                                         !kFast && P.nocull != 0, R);
-        if (st == CULL_KEEP) {
-            // Eq. sat_cond with (gamma_T, chi_T) = (64, 64); all-CW = the arc does not wrap the seam
-            const bool wraps = R.r_len >= E.chi || R.r_lo + R.r_len > E.chi || R.pole_rows;
-            sat = !wraps && (R.c_to - R.c_from + 1) <= 64 && R.r_len <= 64;
-            bat = !sat;
-            const long long items = rect_items(R, E);
-            if (items <= smax && !R.pole_rows) {
-                if (setup_to_slot(v, em_o(E), P.faces, slot + lane, tri_id(P.tri, t), (int)t, e)) {
-                    my = (int)items;
-                    cat = C_SMALL;
-                    // ray of item (row, col) = gbase + row * chi + col - (col >= chi - r_lo ? chi : 0)
-                    // (storing this before the setup, so that R is dead across it, measured slower: 0.482 -> 0.490 ms)
-                    slot[5 * 32 + lane] = make_float4(__int_as_float(E.ray_base + R.c_from * E.chi + R.r_lo),
-                                                      __int_as_float(E.chi - R.r_lo),
-                                                      __uint_as_float((unsigned)R.r_len | ((unsigned)E.chi << 16)),
-#if KF_MAGIC_DIV
-                                                      // row = local / len exactly as umulhi(local, ceil(2^32 / len))
-                                                      // (local < 2^16, len < 2^16); len = 1 -> 0 (row = local)
-                                                      __uint_as_float(R.r_len > 1 ? (unsigned)((0x100000000ull + (unsigned)R.r_len - 1) /
-                                                                                               (unsigned)R.r_len) : 0u));
-#else
-                                                      __fdividef(1.f, (float)R.r_len));   // row guess, corrected by +-1
-#endif
-                } else {
-                    cat = C_DEGEN;
-                }
-            } else {
-                large = true;
-            }
-        } else cat = st == CULL_RANGE ? C_RANGE : st == CULL_CHANNEL ? C_CHAN : st == CULL_AZIMUTH ? C_AZI : C_DEGEN;
-    }
-    const unsigned lm = __ballot_sync(FULL, large);
-    if (lm) {
-        const int leader = __ffs(lm) - 1;
-        unsigned base = 0;
-        if (lane == leader) base = atomicAdd(P.n_large, (unsigned)__popc(lm));
-        base = __shfl_sync(FULL, base, leader);
-        if (large) {
-            const long long pos = (long long)base + __popc(lm & ((1u << lane) - 1u));
-            if (pos < P.cap_large) {
-                P.large[pos] = make_int4((int)t, e | (R.c_from << 8), R.c_to,
-                                         (int)((unsigned)R.r_lo | ((unsigned)R.r_len << 16)));
-                cat = C_LARGE;
-            } else {   // capacity fallback: intersect here (slow, never dropped)
-                cat = C_OVF;
-                if (R.pole_rows) { R.r_lo = 0; R.r_len = sE[e].chi; }
-                intersect_rect_serial(P, sE[e], t, R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len);
-            }
-        }
-    }
-    {   // stats of this round: one match over the category codes, each category's leader lane adds
-        // its count to the warp's private counter row (distinct addresses: no atomics)
-        const unsigned grp = __match_any_sync(FULL, cat);
-        if (cat >= 0 && lane == __ffs(grp) - 1) wc[cat] += (unsigned long long)__popc(grp);
-        const unsigned msat = __ballot_sync(FULL, sat), mbat = __ballot_sync(FULL, bat);
-        const unsigned items = __reduce_add_sync(FULL, (unsigned)my);
-        if (lane == 0) {
-            wc[ST_SAT] += __popc(msat);
-            wc[ST_BAT] += __popc(mbat);
-            wc[ST_ITEMS_SMALL] += items;
-        }
-    }
+// A5 + A6 for one warp: the items of the lanes' small rectangles (slot columns already written, `my` items
+// for this lane) expanded by an inclusive prefix scan and tested 32 at a time.  Warp-collective.
+template <bool kFast, bool kC>
+__device__ __forceinline__ void expand_items(const KParams &P, const EmDev *sE, const float4 *slot, int *excl,
+                                             unsigned long long *wc, int lane, int my) {
     // A5: warp-level prefix-scan work expansion
     int incl = my;
 #pragma unroll
@@ -881,6 +792,103 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
         wc[ST_FP64] += fw;
     }
     __syncwarp();
+}
+
+// ----------------------------------------- K2b+K4s fused: refine + small work --
+// One warp per 32-survivor round (interleaved over all warps): lane-per-survivor exact rectangle
+// (cull_pair), certified setup of small rectangles into shared-memory float4 slots, then the
+// warp expands all items of its small rectangles with a prefix scan (A5) and tests them 32 at a
+// time (A6).  Large rectangles go to the large list (K3/K4).  One vertex fetch per survivor.
+// One round of the fused refine + small expansion (A4-A6) for up to 32 survivor entries
+// (tri << 8 | emitter, one per lane, valid lanes only): exact rectangle (cull_pair), small
+// rectangles set up and expanded over the warp (prefix scan), large ones appended to the large
+// list.  Warp-collective; slot / excl are this warp's shared-memory staging areas.
+// kFast: no debug / multicast modes (no-cull, forced fp64, all-hit counts, NVLS keys), so the per-
+// candidate checks of those flags compile away (the host launches this instantiation when they are off)
+template <bool kFast, bool kLevel, bool kC>
+__device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, const float *sSin,
+                                             const unsigned char *sLut, float4 *slot, int *excl,
+                                             unsigned long long *wc, int smax, int lane, bool valid,
+                                             unsigned long long ent) {
+    // per-lane category = the stat it counts (warp-private counters wc[], no atomics)
+    enum { C_NONE = -1, C_SMALL = ST_SMALL, C_LARGE = ST_LARGE, C_OVF = ST_OVF_LARGE, C_RANGE = ST_RANGE,
+           C_CHAN = ST_CHANNEL, C_AZI = ST_AZIMUTH, C_DEGEN = ST_DEGEN };
+    int my = 0, e = 0, cat = C_NONE;
+    bool sat = false, bat = false;   // paper classification counters (PAPER.md:727-752)
+    long long t = 0;
+    Rect R;
+    bool large = false;
+    if (valid) {
+        e = (int)(ent & 255u);
+        t = (long long)(ent >> 8);
+        f3 v[3];
+        load_tri<kC>(P.tri, t, v);
+        const EmDev &E = sE[e];
+        const int st = cull_pair<kLevel>(v, E, sSin + E.sin_base, P.lut ? sLut + e * kLutBins : nullptr,
+                                         !kFast && P.nocull != 0, R);
+        if (st == CULL_KEEP) {
+            // Eq. sat_cond with (gamma_T, chi_T) = (64, 64); all-CW = the arc does not wrap the seam
+            const bool wraps = R.r_len >= E.chi || R.r_lo + R.r_len > E.chi || R.pole_rows;
+            sat = !wraps && (R.c_to - R.c_from + 1) <= 64 && R.r_len <= 64;
+            bat = !sat;
+            const long long items = rect_items(R, E);
+            if (items <= smax && !R.pole_rows) {
+                if (setup_to_slot(v, em_o(E), P.faces, slot + lane, tri_id(P.tri, t), (int)t, e)) {
+                    my = (int)items;
+                    cat = C_SMALL;
+                    // ray of item (row, col) = gbase + row * chi + col - (col >= chi - r_lo ? chi : 0)
+                    // (storing this before the setup, so that R is dead across it, measured slower: 0.482 -> 0.490 ms)
+                    slot[5 * 32 + lane] = make_float4(__int_as_float(E.ray_base + R.c_from * E.chi + R.r_lo),
+                                                      __int_as_float(E.chi - R.r_lo),
+                                                      __uint_as_float((unsigned)R.r_len | ((unsigned)E.chi << 16)),
+#if KF_MAGIC_DIV
+                                                      // row = local / len exactly as umulhi(local, ceil(2^32 / len))
+                                                      // (local < 2^16, len < 2^16); len = 1 -> 0 (row = local)
+                                                      __uint_as_float(R.r_len > 1 ? (unsigned)((0x100000000ull + (unsigned)R.r_len - 1) /
+                                                                                               (unsigned)R.r_len) : 0u));
+#else
+                                                      __fdividef(1.f, (float)R.r_len));   // row guess, corrected by +-1
+#endif
+                } else {
+                    cat = C_DEGEN;
+                }
+            } else {
+                large = true;
+            }
+        } else cat = st == CULL_RANGE ? C_RANGE : st == CULL_CHANNEL ? C_CHAN : st == CULL_AZIMUTH ? C_AZI : C_DEGEN;
+    }
+    const unsigned lm = __ballot_sync(FULL, large);
+    if (lm) {
+        const int leader = __ffs(lm) - 1;
+        unsigned base = 0;
+        if (lane == leader) base = atomicAdd(P.n_large, (unsigned)__popc(lm));
+        base = __shfl_sync(FULL, base, leader);
+        if (large) {
+            const long long pos = (long long)base + __popc(lm & ((1u << lane) - 1u));
+            if (pos < P.cap_large) {
+                P.large[pos] = make_int4((int)t, e | (R.c_from << 8), R.c_to,
+                                         (int)((unsigned)R.r_lo | ((unsigned)R.r_len << 16)));
+                cat = C_LARGE;
+            } else {   // capacity fallback: intersect here (slow, never dropped)
+                cat = C_OVF;
+                if (R.pole_rows) { R.r_lo = 0; R.r_len = sE[e].chi; }
+                intersect_rect_serial(P, sE[e], t, R.c_from, R.c_to - R.c_from + 1, R.r_lo, R.r_len);
+            }
+        }
+    }
+    {   // stats of this round: one match over the category codes, each category's leader lane adds
+        // its count to the warp's private counter row (distinct addresses: no atomics)
+        const unsigned grp = __match_any_sync(FULL, cat);
+        if (cat >= 0 && lane == __ffs(grp) - 1) wc[cat] += (unsigned long long)__popc(grp);
+        const unsigned msat = __ballot_sync(FULL, sat), mbat = __ballot_sync(FULL, bat);
+        const unsigned items = __reduce_add_sync(FULL, (unsigned)my);
+        if (lane == 0) {
+            wc[ST_SAT] += __popc(msat);
+            wc[ST_BAT] += __popc(mbat);
+            wc[ST_ITEMS_SMALL] += items;
+        }
+    }
+    expand_items<kFast, kC>(P, sE, slot, excl, wc, lane, my);
 }
 
 // lane-0 atomic add without the compiler's warp-aggregation wrapper (a single issuing lane)
@@ -1520,7 +1528,8 @@ static size_t k2b_smem_bytes(int n_em, int n_sin, bool lut) {
 }
 static size_t k4s_smem_bytes(int n_em) { return sizeof(EmDev) * n_em + sizeof(float) * NF * K2_THREADS; }
 static size_t kfused_smem_bytes(int n_em, int n_sin, bool lut) {
-    return sizeof(float4) * (KF_THREADS / 32) * 6 * 32 + sizeof(int) * KF_THREADS + sizeof(EmDev) * n_em +
+    return sizeof(float4) * (KF_THREADS / 32) * 6 * 32 + sizeof(int) * KF_THREADS +
+           sizeof(EmDev) * n_em +
            sizeof(float) * ((n_sin + 3) & ~3) + (lut ? (size_t)n_em * kLutBins : 0);
 }
 
