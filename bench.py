@@ -275,7 +275,13 @@ def ncu_traffic():
     """DRAM bytes per launch from the latest committed `ncu --set full` capture (profiles/)."""
     import glob
 
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    import re
+
+    def order(path):   # rNN<letter>_traffic.json: mid-round snapshots (r02b) before the round's final r02_
+        m = re.match(r"r(\d+)([a-z]*)_traffic\.json$", os.path.basename(path))
+        return (int(m.group(1)), m.group(2) == "", m.group(2)) if m else (-1, False, "")
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")), key=order)
     if not files:
         return {}, None
     d = json.load(open(files[-1]))

@@ -42,3 +42,12 @@ def test_kernel_rooflines_follow_8d_units():
     assert abs(fr["t_hbm_floor_ms"] - (tri_bytes + 24 * n_rays) / (pk["hbm_gbs"] * 1e9) * 1e3) < 1e-12
     assert abs(fr["frac"] - max(fr["t_alu_floor_ms"], fr["t_hbm_floor_ms"]) / 1.06) < 1e-12
     assert 0 < fr["frac"] < 1
+
+
+def test_traffic_from_the_latest_full_capture():
+    # the round's final capture (rNN_) outranks its mid-round snapshots (rNNb_, ...) and every earlier round
+    _, src = bench.ncu_traffic()
+    names = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_traffic.json"))
+    last_round = max(int(f[1:3]) for f in names)
+    assert src == f"r{last_round:02d}_traffic.json" or (src.startswith(f"r{last_round:02d}")
+                                                        and f"r{last_round:02d}_traffic.json" not in names)
