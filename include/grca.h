@@ -196,7 +196,8 @@ grca_status grca_destroy(grca_t h);
  * and uploads it with the per-emitter records and sin(phi_j) tables (synchronous).
  * Errors: GRCA_E_INVALID for n_emitters not in [1, 255], gamma/chi out of range, an
  * unsorted or non-strict elevation table, |phi| > RN32(pi/2), a non-orthonormal frame,
- * hfov not 180/360, sum gamma > 4096; GRCA_E_CAPACITY if sum gamma chi > max_rays. */
+ * hfov not 180/360, sum over emitters of (gamma_n + 2) > 4096 (each sin table carries two +inf sentinels);
+ * GRCA_E_CAPACITY if sum gamma chi > max_rays. */
 grca_status grca_set_emitters(grca_t h, const grca_emitter *em, int32_t n_emitters);
 
 /* Borrow this frame's triangles (no copy).  d_vertices: device float4 (x, y, z, w unused),

@@ -312,6 +312,42 @@ def test_edge_cases():
     assert set(np.unique(tri)) <= {-1, 4}
 
 
+@pytest.mark.parametrize("shape", ["1x1", "chi_max", "gamma_max", "tile_edges"])
+def test_extreme_emitter_shapes_and_counts(shape):
+    """Boundary sizes of the ABI (include/grca.h: gamma, chi in [1, 65535], sum (gamma + 2) <= 4096) and triangle
+    counts on both sides of a K2 tile (1024): every ray against the oracle."""
+    rng = np.random.default_rng(7)
+    tris = sg.random_triangles(rng, 300, center=(0, 0, 0), half_extent=8.0, edge_lo=0.05, edge_hi=6.0)
+    if shape == "1x1":   # one channel, one ray (theta = 0): a triangle straight ahead and one behind
+        ems = [sg.Emitter(origin=(0, 0, 0), elev=np.float32([0.0]), rays_per_channel=1)]
+        tris = np.array([[[4, -1, -1], [4, 1, -1], [4, 0, 1]], [[-4, -1, -1], [-4, 1, -1], [-4, 0, 1]]],
+                        np.float32)
+    elif shape == "chi_max":   # 65,535 rays in one channel (16-bit ray ranges), 360 and 180 deg
+        ems = [sg.Emitter(origin=(0.1, -0.2, 0.0), elev=np.float32([0.05]), rays_per_channel=65535),
+               sg.Emitter(origin=(0.3, 0.2, 0.1), elev=np.float32([-0.1]), rays_per_channel=65535, hfov_deg=180)]
+    elif shape == "gamma_max":   # the channel limit, sum (gamma + 2) = 4096, over two emitters (no channel LUT)
+        ems = [sg.Emitter(origin=(0, 0, 0), elev=sg.full_sphere_elev(4000), rays_per_channel=3),
+               sg.Emitter(origin=(0.5, 0.5, 0.5), elev=sg.full_sphere_elev(92), rays_per_channel=5, hfov_deg=180)]
+    else:
+        ems = [sg.Emitter(origin=(0, 0, 0), elev=sg.full_sphere_elev(16), rays_per_channel=97)]
+    counts = [len(tris)] if shape != "tile_edges" else [1, 1023, 1024, 1025, 2049]
+    for n in counts:
+        t = tris if shape != "tile_edges" else sg.random_triangles(rng, n, center=(0, 0, 0), half_extent=8.0,
+                                                                   edge_lo=0.05, edge_hi=6.0)
+        dist, tri, st, _ = run(ems, t)
+        rep, _ = check(ems, t, dist, tri)
+        assert st["pairs"] == len(t) * len(ems)
+    if shape == "1x1":
+        assert tri[0] == 0 and dist[0] == np.float32(4.0)
+    if shape == "chi_max":
+        assert rep["oracle_hits"] > 1000
+    if shape == "gamma_max":   # one channel more is refused
+        g = Grca(device=0, max_triangles=1, max_rays=20000)
+        with pytest.raises(GrcaError) as e:
+            g.set_emitters([ems[0], sg.Emitter(origin=(0.5, 0.5, 0.5), elev=sg.full_sphere_elev(93), rays_per_channel=5)])
+        assert e.value.status == G.GRCA_E_INVALID
+
+
 def test_api_errors():
     g = Grca(device=0, max_triangles=10, max_rays=1000)
     with pytest.raises(GrcaError) as e:
