@@ -57,6 +57,16 @@ constexpr int K4_THREADS = 256;
 #ifndef KF_MAGIC_DIV
 #define KF_MAGIC_DIV 0   // fused item loop: row = local / len by a per-pair magic multiplier (no float round trip)
 #endif
+#ifndef KF_ROWCOL_EXACT
+// fused item loop: row = floor((local + 1/2) / len) from the approximate reciprocal needs no +-1 correction for a
+// small rectangle: its items (rows x len) are <= small_max <= 1023, so (local + 1/2) / len lies >= 1/(2 len) from an
+// integer while the float error is <= rows x 2^-21 <= (1023 / len) x 2^-21, under 1e-3 of that distance
+#define KF_ROWCOL_EXACT 1   // (measured: C4 fused 0.478 -> 0.470 ms; tests/test_kernel_arith_cpu.py checks the bound)
+#endif
+#ifndef KF_LANE_COUNT
+#define KF_LANE_COUNT 1   // fused item loop: hit / fp64 counts per lane, reduced once per round (no ballots per step;
+                          // measured: C4 fused 0.481 -> 0.477 ms)
+#endif
 #ifndef KF_PREFETCH
 #define KF_PREFETCH 0   // fused item loop: issue the next step's ray load before this step's test
 #endif
@@ -722,8 +732,10 @@ __device__ __forceinline__ void expand_items(const KParams &P, const EmDev *sE, 
 #else
             int row = (int)(((float)local + 0.5f) * r5.w);
             int col = local - row * len;
+#if !KF_ROWCOL_EXACT
             if (col < 0) { --row; col += len; }
             if (col >= len) { ++row; col -= len; }
+#endif
 #endif
             g = __float_as_int(r5.x) + row * chi + col - (col >= __float_as_int(r5.y) ? chi : 0);
         }
@@ -784,9 +796,18 @@ __device__ __forceinline__ void expand_items(const KParams &P, const EmDev *sE, 
         }
         // hit / fp64 counts: warp-uniform sums (a per-lane counter live across the loop would be
         // spilled at the 64-register cap), flushed once per round
+#if KF_LANE_COUNT   // per-lane counts packed in one register (hits | fp64 << 16), reduced once per round
+        hw += (hit ? 1u : 0u) + (fb ? 0x10000u : 0u);
+#else
         hw += __popc(__ballot_sync(FULL, hit));
         fw += __popc(__ballot_sync(FULL, fb));
+#endif
     }
+#if KF_LANE_COUNT
+    hw = __reduce_add_sync(FULL, hw);   // each half <= 32 x small_max (<= 1023) < 2^16: no carry
+    fw = hw >> 16;
+    hw &= 0xffffu;
+#endif
     if (lane == 0) {
         wc[ST_HITS] += hw;
         wc[ST_FP64] += fw;
