@@ -332,6 +332,12 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
     } else if (kFast || P.pairs_ok) {   // all frames orthonormal: packed fp32x2 path
 #pragma unroll
         for (int e = 0; e + 1 < NE; e += 2) {
+#if K2_TAIL_SEL
+            quick_pair_sel<kLevel>(v, emax, EL.p[e / 2], EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base,
+                                   sSin + EL.e[e + 1].sin_base, sLut + e * kLutBins, sLut + (e + 1) * kLutBins,
+                                   1u << e, kb, rb);
+            continue;
+#endif
             const unsigned r = quick_pair_lut<kLevel>(v, emax, EL.p[e / 2], EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base,
                                               sSin + EL.e[e + 1].sin_base, sLut + e * kLutBins,
                                               sLut + (e + 1) * kLutBins);

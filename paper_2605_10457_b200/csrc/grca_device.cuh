@@ -728,6 +728,9 @@ __device__ __forceinline__ int quick_tail(const float s[3], float rmax, float em
     return range ? CULL_RANGE : (keep ? CULL_KEEP : CULL_CHANNEL);
 }
 
+#ifndef K2_TAIL_SEL
+#define K2_TAIL_SEL 0
+#endif
 #ifndef K2_FOLD_NEAR
 #define K2_FOLD_NEAR 1   // K2: the near test folded into the pole bound (measured: C4 K2 0.461 -> 0.457 ms, K2 survivors
                          // +0.07 %, exact survivors and hits unchanged)
@@ -927,6 +930,36 @@ __device__ __forceinline__ unsigned quick_pair_lut(const f3 v[3], float emax, co
     const unsigned b = quick_tail_lut(s1, m1, emax, L1, sinT1, lut1);
     return (a & 1u) | ((b & 1u) << 1) | ((a & 2u) << 1) | ((b & 2u) << 2);
 }
+
+#if K2_TAIL_SEL
+// quick_pair_lut with the per-emitter results as ready-made mask bits (keep ? bit : 0, range ? bit : 0) instead of a
+// 4-bit code that k2_tri unpacks: two selects per emitter, one OR per pair of emitters for each mask
+template <bool kLevel = false>
+__device__ __forceinline__ void quick_pair_sel(const f3 v[3], float emax, const EmPair &PR, const EmLite &L0,
+                                               const EmLite &L1, const float *sinT0, const float *sinT1,
+                                               const unsigned char *lut0, const unsigned char *lut1, unsigned bit0,
+                                               unsigned &kb, unsigned &rb) {
+    float s0[3], s1[3], m0 = CUDART_INF_F, m1 = CUDART_INF_F;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float2 ax = __fadd2_rn(f2(v[k].x, v[k].x), PR.no[0]);
+        const float2 ay = __fadd2_rn(f2(v[k].y, v[k].y), PR.no[1]);
+        const float2 az = __fadd2_rn(f2(v[k].z, v[k].z), PR.no[2]);
+        const float2 w2 = __ffma2_rn(az, az, __ffma2_rn(ay, ay, __fmul2_rn(ax, ax)));
+        const float2 xu = kLevel ? az : __ffma2_rn(PR.u[2], az, __ffma2_rn(PR.u[1], ay, __fmul2_rn(PR.u[0], ax)));
+        const float2 iw = f2(rsqrtf(w2.x), rsqrtf(w2.y));
+        const float2 ss = __fmul2_rn(xu, iw);
+        s0[k] = ss.x;
+        s1[k] = ss.y;
+        m0 = fminf(m0, iw.x);
+        m1 = fminf(m1, iw.y);
+    }
+    const unsigned a = quick_tail_lut(s0, m0, emax, L0, sinT0, lut0);
+    const unsigned b = quick_tail_lut(s1, m1, emax, L1, sinT1, lut1);
+    kb |= (a == 1u ? bit0 : 0u) | (b == 1u ? bit0 << 1 : 0u);
+    rb |= (a == 2u ? bit0 : 0u) | (b == 2u ? bit0 << 1 : 0u);
+}
+#endif
 
 template <bool kLevel = false>
 __device__ __forceinline__ void quick_pair_pred(const f3 v[3], float emax, const EmPair &PR, const EmLite &L0,
