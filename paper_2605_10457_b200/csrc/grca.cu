@@ -336,13 +336,13 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
             quick_pair_sel<kLevel>(v, emax, EL.p[e / 2], EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base,
                                    sSin + EL.e[e + 1].sin_base, sLut + e * kLutBins, sLut + (e + 1) * kLutBins,
                                    1u << e, kb, rb);
-            continue;
-#endif
+#else
             const unsigned r = quick_pair_lut<kLevel>(v, emax, EL.p[e / 2], EL.e[e], EL.e[e + 1], sSin + EL.e[e].sin_base,
                                               sSin + EL.e[e + 1].sin_base, sLut + e * kLutBins,
                                               sLut + (e + 1) * kLutBins);
             kb |= (r & 3u) << e;
             rb |= (r >> 2) << e;
+#endif
         }
         if (NE & 1) {
             const unsigned r = quick_cull_lut<kLevel>(v, emax, EL.e[NE - 1], sSin + EL.e[NE - 1].sin_base,

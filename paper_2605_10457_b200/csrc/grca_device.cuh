@@ -729,7 +729,7 @@ __device__ __forceinline__ int quick_tail(const float s[3], float rmax, float em
 }
 
 #ifndef K2_TAIL_SEL
-#define K2_TAIL_SEL 0
+#define K2_TAIL_SEL 1   // K2 packed path: mask bits by selects (measured: C4 K2 0.455 -> 0.437 ms; NE = 4 0.286 -> 0.280)
 #endif
 #ifndef K2_FOLD_NEAR
 #define K2_FOLD_NEAR 1   // K2: the near test folded into the pole bound (measured: C4 K2 0.461 -> 0.457 ms, K2 survivors
