@@ -347,8 +347,13 @@ __device__ __forceinline__ void k2_tri(const KParams &P, const EmLitePack &EL, c
         if (NE & 1) {
             const unsigned r = quick_cull_lut<kLevel>(v, emax, EL.e[NE - 1], sSin + EL.e[NE - 1].sin_base,
                                               sLut + (NE - 1) * kLutBins);
+#if K2_TAIL_SEL
+            kb |= r == 1u ? 1u << (NE - 1) : 0u;
+            rb |= r == 2u ? 1u << (NE - 1) : 0u;
+#else
             kb |= (r & 1u) << (NE - 1);
             rb |= (r >> 1) << (NE - 1);
+#endif
         }
     } else {
 #pragma unroll
