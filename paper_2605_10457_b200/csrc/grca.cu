@@ -57,6 +57,9 @@ constexpr int K4_THREADS = 256;
 #ifndef KF_MAGIC_DIV
 #define KF_MAGIC_DIV 0   // fused item loop: row = local / len by a per-pair magic multiplier (no float round trip)
 #endif
+#ifndef KF_SB_INT
+#define KF_SB_INT 0
+#endif
 #ifndef KF_ROWCOL_EXACT
 // fused item loop: row = floor((local + 1/2) / len) from the approximate reciprocal needs no +-1 correction for a
 // small rectangle: its items (rows x len) are <= small_max <= 1023, so (local + 1/2) / len lies >= 1/(2 len) from an
@@ -846,7 +849,11 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
     enum { C_NONE = -1, C_SMALL = ST_SMALL, C_LARGE = ST_LARGE, C_OVF = ST_OVF_LARGE, C_RANGE = ST_RANGE,
            C_CHAN = ST_CHANNEL, C_AZI = ST_AZIMUTH, C_DEGEN = ST_DEGEN };
     int my = 0, e = 0, cat = C_NONE;
+#if KF_SB_INT
+    unsigned sb = 0u;   // paper classification: 1 = SAT, 2 = BAT (a value, not two live predicates)
+#else
     bool sat = false, bat = false;   // paper classification counters
+#endif
     long long t = 0;
     Rect R;
     bool large = false;
@@ -861,8 +868,12 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
         if (st == CULL_KEEP) {
             // Eq. sat_cond with (gamma_T, chi_T) = (64, 64); all-CW = the arc does not wrap the seam
             const bool wraps = R.r_len >= E.chi || R.r_lo + R.r_len > E.chi || R.pole_rows;
+#if KF_SB_INT
+            sb = (!wraps && (R.c_to - R.c_from + 1) <= 64 && R.r_len <= 64) ? 1u : 2u;
+#else
             sat = !wraps && (R.c_to - R.c_from + 1) <= 64 && R.r_len <= 64;
             bat = !sat;
+#endif
             const long long items = rect_items(R, E);
             if (items <= smax && !R.pole_rows) {
                 if (setup_to_slot(v, em_o(E), P.faces, slot + lane, tri_id(P.tri, t), (int)t, e)) {
@@ -912,7 +923,11 @@ __device__ __forceinline__ void refine_round(const KParams &P, const EmDev *sE, 
         // its count to the warp's private counter row (distinct addresses: no atomics)
         const unsigned grp = __match_any_sync(FULL, cat);
         if (cat >= 0 && lane == __ffs(grp) - 1) wc[cat] += (unsigned long long)__popc(grp);
+#if KF_SB_INT
+        const unsigned msat = __ballot_sync(FULL, sb & 1u), mbat = __ballot_sync(FULL, sb & 2u);
+#else
         const unsigned msat = __ballot_sync(FULL, sat), mbat = __ballot_sync(FULL, bat);
+#endif
         const unsigned items = __reduce_add_sync(FULL, (unsigned)my);
         if (lane == 0) {
             wc[ST_SAT] += __popc(msat);
