@@ -151,6 +151,10 @@ __device__ __forceinline__ void block_flush(unsigned long long *acc_smem, unsign
 }
 
 // ------------------------------------------------------------------- K0 init --
+#ifdef GRCA_CHECK
+__global__ void k_check_set_n_rays(long long n) { g_check_n_rays = n; }
+#endif
+
 __global__ void k_init(unsigned long long *hits, unsigned *allhits, long long n, unsigned *ctrl,
                        unsigned long long *stats, const unsigned long long *src, const unsigned *src_allhits,
                        int reset = 1) {
@@ -2269,10 +2273,10 @@ static cudaError_t nvls_barrier(grca_t h) {
 static grca_status launch_packed(grca_t h) {
     if (h->n_em_global < 1) return fail(h, GRCA_E_STATE, "grca_set_emitters has not been called");
 #ifdef GRCA_CHECK
-    {
-        const long long nr = h->n_rays;
-        CK(cudaMemcpyToSymbolAsync(g_check_n_rays, &nr, sizeof(nr), 0, cudaMemcpyHostToDevice, h->stream));
-    }
+    // the value travels as a kernel argument: captured by value into a CUDA graph (a copy from a host stack
+    // variable would be replayed from a stale address)
+    k_check_set_n_rays<<<1, 1, 0, h->stream>>>(h->n_rays);
+    CK(cudaGetLastError());
 #endif
     if (!h->have_tri && !h->st_set) return fail(h, GRCA_E_STATE, "grca_update_triangles has not been called");
     if (h->nvls_mc && h->st_set)
