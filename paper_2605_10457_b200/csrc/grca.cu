@@ -60,6 +60,10 @@ constexpr int K4_THREADS = 256;
 #ifndef KF_SB_INT
 #define KF_SB_INT 0
 #endif
+#ifndef KF_FETCH_TAIL
+#define KF_FETCH_TAIL 12   // fused kernel: the last 12 rounds per warp fetched one at a time (measured: C4 fused 0.4695 -> 0.4579 ms;
+                          // 2 / 6 / 20 / 30: 0.4683 / 0.4591 / 0.4592 / 0.4622)
+#endif
 #ifndef KF_ROWCOL_EXACT
 // fused item loop: row = floor((local + 1/2) / len) from the approximate reciprocal needs no +-1 correction for a
 // small rectangle: its items (rows x len) are <= small_max <= 1023, so (local + 1/2) / len lies >= 1/(2 len) from an
@@ -982,6 +986,18 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
     // dynamic round fetching (one global atomic per warp per `fetch` rounds): fewer same-address atomics
     // when every warp has many rounds, single rounds (the finest tail) when it has few
     const unsigned fetch = rpw >= 16u ? (unsigned)KF_FETCH : 1u;
+#if KF_FETCH_TAIL   // the counter counts rounds; the last KF_FETCH_TAIL rounds per warp are fetched one at a time
+    const unsigned tail_rounds = (unsigned)KF_FETCH_TAIL * gridDim.x * (KF_THREADS / 32);
+    unsigned w = 0, cnt = fetch;
+    if (lane == 0) w = atom_add_u32(P.n_surv + 2, fetch);
+    w = __shfl_sync(FULL, w, 0);
+    for (; w < nr;) {
+        const unsigned fn = (w + cnt + tail_rounds >= nr) ? 1u : fetch;
+        unsigned wn = 0;
+        if (lane == 0) wn = atom_add_u32(P.n_surv + 2, fn);   // next group, fetched early (latency hidden)
+#pragma unroll 1
+        for (unsigned f = 0; f < cnt; ++f) {
+#else
     unsigned w = 0;
     if (lane == 0) w = atom_add_u32(P.n_surv + 2, 1u);
     w = __shfl_sync(FULL, w, 0) * fetch;
@@ -990,13 +1006,19 @@ __global__ void __launch_bounds__(KF_THREADS, KF_MINB) k_refine_small(const __gr
         if (lane == 0) wn = atom_add_u32(P.n_surv + 2, 1u);   // next group, fetched early (latency hidden)
 #pragma unroll 1
         for (unsigned f = 0; f < fetch; ++f) {
+#endif
             const unsigned idx = (w + f) * 32u + (unsigned)lane;
             const bool valid = idx < ns;
             if (!__any_sync(FULL, valid)) break;
             refine_round<kFast, kLevel, kC>(P, sE, sSin, sLut, slot, excl, sWc + wib * 32, smax, lane, valid,
                                         valid ? __ldcs(P.surv + idx) : 0ull);
         }
+#if KF_FETCH_TAIL
+        w = __shfl_sync(FULL, wn, 0);
+        cnt = fn;
+#else
         w = __shfl_sync(FULL, wn, 0) * fetch;
+#endif
     }
     __syncthreads();
     if (threadIdx.x < ST_COUNT) {   // block total of each counter, one global atomic each
