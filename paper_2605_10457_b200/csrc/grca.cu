@@ -46,6 +46,10 @@ constexpr int K4_THREADS = 256;
 #define KF_FETCH 2   // 32-survivor rounds per dynamic fetch of the fused kernel (measured: 1 -> 1.048, 2 -> 1.033,
                      // 4 -> 1.121 ms at C4: half the fetch atomics vs a coarser tail)
 #endif
+#ifndef K2_DYN_TILES
+#define K2_DYN_TILES 1   // K2 tiles after the first wave fetched dynamically (measured: C4 K2 0.438 -> 0.387 ms; statically
+                         // strided tiles left blocks with more car (indexed) tiles finishing last)
+#endif
 #ifndef K2_PRED_MAX_NE
 #define K2_PRED_MAX_NE 2   // K2 pre-test in predicate form (quick_*_pred) for NE <= this; the 2-bit-code form above
                            // (measured at C4: NE = 8 0.485 vs 0.503 ms in predicate form; NE = 1 0.1715 -> 0.1695,
@@ -396,7 +400,12 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
                                          unsigned &c_pairs, unsigned &c_range, unsigned &c_surv,
                                          unsigned &c_area) {
     const long long ntiles = (P.n_tri + K2_TILE - 1) / K2_TILE;
+#if K2_DYN_TILES   // tiles after the first wave fetched dynamically (one atomic per tile, at the tile's closing barrier)
+    __shared__ long long s_next;
+    for (long long tile = blockIdx.x; tile < ntiles;) {
+#else
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+#endif
         // K2_TILE / K2_THREADS triangles per thread (one block scan, barrier pair and atomic for all)
         unsigned keeps[K2_TILE / K2_THREADS];
         int cntk = 0;
@@ -447,7 +456,13 @@ __device__ __forceinline__ void k2_tiles(const KParams &P, const EmLitePack &EL,
                 *dst++ = ((unsigned long long)t << 8) | (unsigned)e;
             }
         }
+#if K2_DYN_TILES
+        if (threadIdx.x == 0) s_next = (long long)gridDim.x + (long long)atomicAdd(P.n_surv + 3, 1u);
+        __syncthreads();   // wsum / qbase reuse, s_next visible
+        tile = s_next;
+#else
         __syncthreads();   // wsum / qbase reuse
+#endif
     }
 }
 
